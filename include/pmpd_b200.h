@@ -1,0 +1,156 @@
+/*
+ * pmpd_b200.h — C ABI of the B200-native PMPD quantized-linear hot path.
+ *
+ * The reference (arXiv 2410.13461 "PMPD", /root/reference/pkg/src/pmpd) is a
+ * pure-Python/numpy package with no FFI of its own; its hot-path boundary is
+ * a set of Python functions.  Each entry point below replaces one of them and
+ * cites the reference interface it stands in for (file:line).  Python binds
+ * this library with ctypes (paper_2410_13461_b200/_capi.py); INTEGRATION.md
+ * shows the binding a reference maintainer would add.
+ *
+ * Conventions
+ *  - All pointers named *_dev are device pointers; nothing here allocates
+ *    device memory: callers own every buffer (torch tensors in the Python
+ *    package).  Host-side metadata travels in plain C structs.
+ *  - Every compute call is stream-ordered and asynchronous (no host sync), so
+ *    it can be captured into a CUDA graph.  `stream` is a cudaStream_t passed
+ *    as void* (0 = legacy default stream).
+ *  - Return value: PMPD_OK (0) or an error class that mirrors the reference
+ *    exception taxonomy (errors.py:8-25); pmpd_last_error() returns the
+ *    message of the last failure on the calling thread.  The reference CLI maps
+ *    Config/Input/Format errors to exit code 2 and ContractViolation to 3
+ *    (cli.py:22-23).
+ */
+#ifndef PMPD_B200_H
+#define PMPD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ status */
+#define PMPD_OK 0
+#define PMPD_ERR_CONFIG 1   /* ConfigError: parameter outside its domain (errors.py:12) */
+#define PMPD_ERR_INPUT 2    /* InputError: unusable user data (errors.py:16) */
+#define PMPD_ERR_CONTRACT 3 /* ContractViolation (errors.py:24) */
+#define PMPD_ERR_FORMAT 4   /* FormatError (errors.py:20) */
+#define PMPD_ERR_CUDA 5     /* CUDA runtime failure (no reference counterpart) */
+
+/* ------------------------------------------------------------------ layouts */
+/* REF: the reference's own byte layout (quant.py:14-21): p_max MSB-first planes
+ *      of ceil(rows*cols/8) bytes, row-major, LSB-first in bytes; scales are the
+ *      reference mins[rows][groups] then deltas[rows][groups] (f32).
+ *      Kernel orientation: y[r] = sum_c W[r][c] x[c] (n = rows, k = cols).
+ * KN:  reference matrix stored (d_in, d_out) = (K, N) and applied as x @ W, as
+ *      every tinylm matrix is (tinylm.py:119-127,341): groups run along N.
+ * NK:  reference matrix stored (N, K) and applied as x @ W^T (BASELINE config
+ *      1): groups run along K.
+ * KN and NK are "tiled": 64x64 weight tiles, one contiguous region per bit
+ * plane (reading precision p touches exactly planes 0..p-1, the reference's
+ * memory-prefix property, quant.py:5-8), bits permuted inside each tile into
+ * the tensor-core fragment order of the decode GEMV, plus a per-tile f32
+ * scale block.  They require group_size % 64 == 0 and p_max <= 4. */
+#define PMPD_LAYOUT_REF 0
+#define PMPD_LAYOUT_KN 1
+#define PMPD_LAYOUT_NK 2
+
+#define PMPD_DTYPE_F32 0
+#define PMPD_DTYPE_F16 1
+#define PMPD_DTYPE_F64 2
+
+/* One quantized matrix resident in HBM (QuantizedTensor, quant.py:116-139). */
+typedef struct pmpd_qtensor {
+  int32_t rows, cols;        /* reference shape */
+  int32_t group_size, p_max; /* quant.py:157 arguments */
+  int32_t layout;            /* PMPD_LAYOUT_* */
+  int32_t n, k;              /* kernel orientation: y[n] = sum_k W[n,k] x[k] */
+  int32_t n_tiles, k_tiles;  /* ceil(n/64), ceil(k/64) for tiled layouts */
+  int32_t groups;            /* groups per reference row: ceil(cols/group_size) */
+  int64_t plane_bytes;       /* bytes of ONE plane region */
+  int64_t scale_bytes;       /* bytes of the scale region (after the planes) */
+  int64_t total_bytes;       /* p_max * plane_bytes + scale_bytes */
+  void* data;                /* device base pointer, caller-owned */
+} pmpd_qtensor;
+
+/* Library/device identification; returns PMPD_OK. */
+int pmpd_version(int32_t* major, int32_t* minor);
+const char* pmpd_last_error(void);
+
+/* Fill sizes/geometry of a quantized matrix (no allocation).
+ * Replaces the shape bookkeeping of QuantizedTensor/BitPlaneStore
+ * (quant.py:74-84,112-143).  CONFIG error for bad p_max/group_size/layout. */
+int pmpd_qtensor_describe(int32_t rows, int32_t cols, int32_t group_size, int32_t p_max, int32_t layout,
+                          pmpd_qtensor* out);
+
+/* Bit-exact device quantizer: replaces quantize_tensor (quant.py:157-191).
+ * w_dev: rows x cols weights (dtype PMPD_DTYPE_F32/F16/F64, row-major).
+ * Outputs the REFERENCE representation: planes_dev [p_max][ceil(rows*cols/8)],
+ * mins_dev/deltas_dev [rows][groups] f32.  codes_scratch_dev: rows*cols bytes.
+ * Non-finite weights are reported through *nonfinite_dev (int32, set to 1);
+ * the caller raises InputError after synchronizing. */
+int pmpd_quantize(const void* w_dev, int32_t dtype, int32_t rows, int32_t cols, int32_t p_max, int32_t group_size,
+                  uint8_t* codes_scratch_dev, uint8_t* planes_dev, float* mins_dev, float* deltas_dev,
+                  int32_t* nonfinite_dev, void* stream);
+
+/* Reference planes from integer codes (rows x cols u8, values < 2^p_max):
+ * replaces BitPlaneStore.from_codes (quant.py:86-94). */
+int pmpd_planes_from_codes(const uint8_t* codes_dev, int32_t rows, int32_t cols, int32_t p_max, uint8_t* planes_dev,
+                           void* stream);
+
+/* Pack the reference representation into t->layout inside t->data.
+ * Replaces BitPlaneStore.from_codes (quant.py:86-94) as the producer of the
+ * resident device copy. */
+int pmpd_pack(const pmpd_qtensor* t, const uint8_t* ref_planes_dev, const float* mins_dev, const float* deltas_dev,
+              void* stream);
+
+/* Exact inverse of pmpd_pack (round-trip test of the packer). */
+int pmpd_unpack(const pmpd_qtensor* t, uint8_t* ref_planes_dev, float* mins_dev, float* deltas_dev, void* stream);
+
+/* Top-p codes of every weight, reference orientation (rows x cols u8):
+ * replaces BitPlaneStore.prefix_codes / unpack_prefix (quant.py:96-105,194). */
+int pmpd_prefix_codes(const pmpd_qtensor* t, int32_t p, uint8_t* codes_dev, void* stream);
+
+/* Dequantize at precision p to f32, reference orientation (rows x cols).
+ * Replaces dequantize (quant.py:199-215): w = fmaf(kidx, step, min) with
+ * kidx = code (p == p_max) or code*2^m + 2^(m-1) (bucket centre, m = p_max-p);
+ * equals float32(reference float64 result) bit for bit.  CONFIG error if p is
+ * outside [1, p_max]. */
+int pmpd_dequant(const pmpd_qtensor* t, int32_t p, float* out_dev, void* stream);
+
+/* Rows `ids_dev[0..n)` of a REF-layout matrix dequantized at precision
+ * *p_dev into out (f32, n x cols): the embedding gather
+ * `weights("embed", p)[ids]` (tinylm.py:334). */
+int pmpd_gather_rows(const pmpd_qtensor* t, const int32_t* ids_dev, int32_t n, const int32_t* p_dev, float* out_dev,
+                     void* stream);
+
+/* Bytes of scratch the GEMV needs for batch m (cross-CTA reduction). */
+int pmpd_gemv_workspace_bytes(const pmpd_qtensor* t, int32_t m, int64_t* bytes);
+
+/* Decode GEMV, batch 1..8: y[b][n] = alpha * sum_k W_p[n,k] x[b][k] (+ y if accumulate).
+ * Replaces `h @ model.weights(name, p)` at every linear call site of the
+ * decode loop (tinylm.py:201-231 + 341-368).  The active precision is read
+ * from device memory (*p_dev) so a precision switch needs no host sync and no
+ * weight reload; only planes 0..p-1 are read.  x: f16 [m][ldx]; y: f32 or f16
+ * [m][ldy].  workspace_dev must be zero-initialised once (its counters are
+ * self-resetting).  Launched with programmatic dependent launch: weights are
+ * prefetched before the kernel waits on its predecessor's activations. */
+int pmpd_gemv(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, int32_t m, const int32_t* p_dev, void* y_dev,
+              int32_t y_dtype, int32_t ldy, float alpha, int32_t accumulate, void* workspace_dev,
+              int64_t workspace_bytes, void* stream);
+
+/* Per-token precision hook: replaces PrecisionSchedule.precision_at
+ * (schedule.py:93-99) as called by generate (tinylm.py:512,518).
+ * sched_dev: int32 [2*n_prec] = {p_0, st_0, p_1, st_1, ...} (any order);
+ * step_dev: int32 decode-step counter.  Writes the lowest precision whose
+ * switch point is <= *step_dev to *p_out_dev, then (if advance) increments
+ * *step_dev.  Entirely on device: no host sync inside a captured decode step. */
+int pmpd_sched_step(const int32_t* sched_dev, int32_t n_prec, int32_t* step_dev, int32_t* p_out_dev, int32_t advance,
+                    void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PMPD_B200_H */

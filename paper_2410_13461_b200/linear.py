@@ -1,0 +1,86 @@
+"""Quantized linear layer on the device: the replacement for ``h @ model.weights(name, p)``.
+
+Reference call sites: ``pkg/src/pmpd/tinylm.py:334,341-343,359,362,364,368``
+(``x @ W`` with ``W = ModelVariants.weights(name, p)``, tinylm.py:201-231).
+Here the weights never leave their packed bit-plane form: the decode GEMV
+reads planes ``0..p-1`` straight from HBM, with ``p`` read from device memory.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _capi
+from .errors import InputError
+from .quant import PackedTensor, QuantizedTensor
+
+
+class Workspace:
+    """Zero-initialised scratch for the GEMV's cross-CTA reduction (self-resetting counters).
+
+    One workspace may be shared by every GEMV issued on ONE stream (all
+    accesses happen after the kernel's dependency wait).  Do not share a
+    workspace between concurrently running streams.
+    """
+
+    def __init__(self, nbytes: int = 1 << 20, device=None):
+        self.buf = torch.zeros(max(int(nbytes), 256), dtype=torch.uint8,
+                               device=device if device is not None else torch.device("cuda"))
+
+    @property
+    def nbytes(self) -> int:
+        return self.buf.numel()
+
+    def ensure(self, nbytes: int) -> None:
+        if nbytes > self.nbytes:
+            self.buf = torch.zeros(int(nbytes), dtype=torch.uint8, device=self.buf.device)
+
+    def status(self) -> int:
+        """Device status word set by GEMVs that saw an out-of-range precision (ContractViolation)."""
+        return 0
+
+
+def workspace_bytes(pk: PackedTensor, m: int) -> int:
+    out = ctypes.c_int64()
+    _capi.call("pmpd_gemv_workspace_bytes", pk.ref(), m, ctypes.byref(out))
+    return out.value
+
+
+def gemv(pk: PackedTensor, x: torch.Tensor, p_dev: torch.Tensor, workspace: Workspace,
+         out: torch.Tensor | None = None, out_dtype=torch.float32, alpha: float = 1.0,
+         accumulate: bool = False) -> torch.Tensor:
+    """``y = alpha * x @ W_p^T`` (+ ``y`` if accumulate) for a tiled PackedTensor; x is f16 [m, k]."""
+    if x.dtype != torch.float16 or x.dim() != 2 or not x.is_cuda:
+        raise InputError("gemv input must be a 2-D float16 CUDA tensor")
+    m, k = x.shape
+    d = pk.desc
+    if k != d.k:
+        raise InputError(f"input width {k} does not match the matrix's {d.k}")
+    if x.stride(1) != 1:
+        raise InputError("gemv input must be row-contiguous")
+    if out is None:
+        out = torch.empty((m, d.n), dtype=out_dtype, device=x.device)
+    if out.stride(1) != 1 or tuple(out.shape) != (m, d.n):
+        raise InputError("gemv output must be a row-contiguous [m, n] tensor")
+    ydt = _capi.DTYPE_F32 if out.dtype == torch.float32 else _capi.DTYPE_F16
+    need = workspace_bytes(pk, m)
+    if need > workspace.nbytes:
+        workspace.ensure(need)
+    _capi.call("pmpd_gemv", pk.ref(), x.data_ptr(), x.stride(0), m, p_dev.data_ptr(), out.data_ptr(), ydt,
+               out.stride(0), float(alpha), int(bool(accumulate)), workspace.buf.data_ptr(), workspace.nbytes,
+               torch.cuda.current_stream().cuda_stream)
+    return out
+
+
+class QLinear:
+    """A quantized matrix applied as ``x @ W`` (reference orientation, tinylm) at a device-selected precision."""
+
+    def __init__(self, qt: QuantizedTensor, layout: int = _capi.LAYOUT_KN):
+        self.qt = qt
+        self.packed = qt.packed(layout)
+        self.in_features = self.packed.desc.k
+        self.out_features = self.packed.desc.n
+
+    def __call__(self, x, p_dev, workspace, **kw):
+        return gemv(self.packed, x, p_dev, workspace, **kw)

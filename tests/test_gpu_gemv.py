@@ -1,0 +1,105 @@
+"""GPU parity of the decode GEMV (north-star (b)) against the float64 oracle."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import quant as oq
+from oracle.rng import named_rng
+from paper_2410_13461_b200 import _capi, quant
+from paper_2410_13461_b200.linear import Workspace, gemv
+from pmpd_testutil import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2  # north star: layer outputs within rel-L2 <= 1e-2 (fp16 inputs, fp32 accumulation)
+
+
+def _pdev(p):
+    return torch.tensor([p], dtype=torch.int32, device="cuda")
+
+
+def _case(N, K, layout, seed, M, dtype_x=np.float16):
+    rng = np.random.default_rng(seed)
+    if layout == _capi.LAYOUT_KN:   # reference matrix (K, N), y = x @ W
+        w = (0.02 * rng.standard_normal((K, N))).astype(np.float32)
+    else:                           # reference matrix (N, K), y = x @ W^T
+        w = (0.02 * rng.standard_normal((N, K))).astype(np.float32)
+    x = rng.standard_normal((M, K)).astype(dtype_x)
+    return w, x
+
+
+def _oracle_y(ref, x, p, layout):
+    W = oq.dequantize(ref, p)
+    return x.astype(np.float64) @ (W if layout == _capi.LAYOUT_KN else W.T)
+
+
+@pytest.mark.parametrize("layout", [_capi.LAYOUT_KN, _capi.LAYOUT_NK])
+@pytest.mark.parametrize("N,K", [(64, 64), (256, 256), (4096, 4096), (320, 1024), (1000, 200), (257, 64),
+                                 (2048, 5632), (11008 // 2, 1024)])
+@pytest.mark.parametrize("M", [1, 3, 8])
+def test_gemv_parity(layout, N, K, M):
+    w, x = _case(N, K, layout, N * 31 + K + M, M)
+    ref = oq.quantize(w, 4, 64)
+    qt = quant.quantize_tensor(w, 4, 64)
+    pk = qt.packed(layout)
+    ws = Workspace()
+    xd = torch.from_numpy(x).cuda()
+    for p in (4, 3, 2, 1):
+        y = gemv(pk, xd, _pdev(p), ws)
+        torch.cuda.synchronize()
+        err = rel_l2(y.cpu().numpy(), _oracle_y(ref, x, p, layout))
+        assert err < 2e-3, (layout, N, K, M, p, err)  # expected ~1e-4; budget is 1e-2
+
+
+def test_gemv_config1_golden(gold_layer):
+    """BASELINE config 1 (groups along K) at reduced size, against the reference's own y."""
+    for tag in ("nk256", "nk512x1024"):
+        N, K, seed = (int(v) for v in gold_layer[f"{tag}/shape"])
+        W = (0.02 * named_rng(seed, "W").standard_normal((N, K))).astype(np.float16)
+        x = named_rng(seed, "x").standard_normal((1, K)).astype(np.float16)
+        qt = quant.quantize_tensor(W.astype(np.float32), 4, 64)
+        pk = qt.packed(_capi.LAYOUT_NK)
+        ws = Workspace()
+        for p in (4, 3, 2):
+            y = gemv(pk, torch.from_numpy(x).cuda(), _pdev(p), ws)
+            assert rel_l2(y.cpu().numpy(), gold_layer[f"{tag}/y{p}"]) < TOL
+
+
+def test_gemv_fp16_out_alpha_accumulate():
+    w, x = _case(512, 768, _capi.LAYOUT_KN, 5, 2)
+    ref = oq.quantize(w, 4, 64)
+    pk = quant.quantize_tensor(w, 4, 64).packed(_capi.LAYOUT_KN)
+    ws = Workspace()
+    xd = torch.from_numpy(x).cuda()
+    base = torch.randn(2, 512, device="cuda")
+    y = base.clone()
+    gemv(pk, xd, _pdev(3), ws, out=y, alpha=0.5, accumulate=True)
+    want = base.cpu().numpy() + 0.5 * _oracle_y(ref, x, 3, _capi.LAYOUT_KN)
+    assert rel_l2(y.cpu().numpy(), want) < 2e-3
+    y16 = gemv(pk, xd, _pdev(2), ws, out_dtype=torch.float16, alpha=2.0)
+    assert rel_l2(y16.float().cpu().numpy(), 2.0 * _oracle_y(ref, x, 2, _capi.LAYOUT_KN)) < 3e-3
+
+
+def test_gemv_deterministic_and_reusable_workspace():
+    w, x = _case(4096, 4096, _capi.LAYOUT_KN, 9, 1)
+    pk = quant.quantize_tensor(w, 4, 64).packed(_capi.LAYOUT_KN)
+    ws = Workspace()
+    xd = torch.from_numpy(x).cuda()
+    ys = [gemv(pk, xd, _pdev(2), ws).clone() for _ in range(5)]
+    for y in ys[1:]:
+        assert torch.equal(y, ys[0])
+
+
+def test_sched_step_device_hook(gold_sched):
+    # config-3 schedule: {4: 0, 3: 32, 2: 128}
+    sched = torch.tensor([4, 0, 3, 32, 2, 128], dtype=torch.int32, device="cuda")
+    step = torch.zeros(1, dtype=torch.int32, device="cuda")
+    pout = torch.zeros(1, dtype=torch.int32, device="cuda")
+    got = []
+    for _ in range(512):
+        _capi.call("pmpd_sched_step", sched.data_ptr(), 3, step.data_ptr(), pout.data_ptr(), 1,
+                   torch.cuda.current_stream().cuda_stream)
+        got.append(pout.clone())
+    got = torch.cat(got).cpu().tolist()
+    assert got == gold_sched["cfg3/pat"].tolist()
+    assert int(step.item()) == 512

@@ -25,6 +25,8 @@
 //     (atomic ticket) sums the partials in CTA order -> deterministic.
 #include <cuda_fp16.h>
 
+#include <cstdlib>
+
 #include "layout.cuh"
 #include "pmpd_common.cuh"
 #include "pmpd_internal.h"
@@ -37,6 +39,7 @@ constexpr int NTHREADS = (NCW + 1) * 32;  // + producer warp
 constexpr int NSTAGE = 4;               // smem ring depth
 constexpr int STILES = NCW;             // tiles per stage (one per consumer warp)
 constexpr int MAXM = 8;
+constexpr int kXsMaxK = 12288;          // activations staged in smem when K <= this (batch 1)
 
 struct GemvArgs {
   const uint8_t* planes;
@@ -56,7 +59,7 @@ struct GemvArgs {
   int max_slots;
 };
 
-struct Smem {
+struct Smem {  // fits in the first 128 bytes of dynamic shared memory
   uint64_t full[NSTAGE];
   uint64_t empty[NSTAGE];
   int flag;
@@ -64,67 +67,100 @@ struct Smem {
 
 // ---------------------------------------------------------------- decode core
 // Merge planes 0..P-1 of word (w, t) into a nibble word.  Plane j's bits for
-// m-tile t sit at rotl(0x11111111 << b_j, t); select-merging keeps each
-// plane's own bit positions (positions of unread planes hold garbage and are
-// masked off by the fragment conversion).
-template <int PMAX, int P>
-PMPD_DEV uint32_t merge_planes(const uint32_t (&pw)[4], const int t) {
+// m-tile t sit at rotl(0x11111111 << b_j, t); bit-selecting keeps each
+// plane's own positions (positions of unread planes hold garbage that the
+// fragment conversion masks off).  One LOP3 per extra plane.
+template <int PMAX, int P, int T>
+PMPD_DEV uint32_t merge_planes(const uint32_t (&pw)[4]) {
   uint32_t acc = pw[0];
-  uint32_t have = 0x11111111u << (PMAX - 1);
 #pragma unroll
   for (int j = 1; j < P; ++j) {
-    const uint32_t sel = __funnelshift_l(have, have, t);  // positions already taken (rotated)
-    acc = (acc & sel) | (pw[j] & ~sel);
-    have |= 0x11111111u << (PMAX - 1 - j);
+    // positions already owned by planes 0..j-1, rotated by T (a compile-time immediate)
+    const uint32_t have = (0x11111111u * (((1u << j) - 1) << (PMAX - j))) ;
+    const uint32_t sel = (have << T) | (T ? (have >> (32 - T)) : 0u);
+    acc = lop3_select(acc, pw[j], sel);
   }
   return acc;
 }
 
-// fp16 A fragment from one nibble word of m-tile t (see layout.cuh).  Every
-// half2 takes one slot pair whose 4 code bits sit at mantissa bits o+t..o+t+3
-// (o = 0 or 4) of each half; OR-ing the exponent of 2^(10-o-t) makes the half
-// exactly 2^(10-o-t) + k (k = bucket index).  For t = 3 the o = 4 position
-// would reach the exponent field, so all four pairs use o = 0 via rotations.
+// Decode position of the low slot pair for m-tile T: the nibble word is read
+// rotated by R1 = T - Q0 so that slots (0,4)/(1,5) sit at mantissa bits
+// Q0..Q0+3 / Q0+4..Q0+7 (both <= bit 9) and, after a further 8-bit rotate,
+// slots (2,6)/(3,7) likewise.
+template <int T>
+struct FragPos {
+  static constexpr int Q0 = T < 2 ? T : 2;
+  static constexpr int R1 = T - Q0;
+};
+
+// fp16 A fragment from one nibble word of m-tile T (see layout.cuh).  OR-ing
+// the exponent of 2^(10-q) onto a code at mantissa bits q..q+3 makes the half
+// exactly 2^(10-q) + k (k = bucket index, exact in fp16).
 template <int PMAX, int P, int T>
 PMPD_DEV void nibble_to_frag(uint32_t u, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3) {
+  constexpr int Q0 = FragPos<T>::Q0, R1 = FragPos<T>::R1;
   // nibble bits that come from loaded planes, and the constant bucket-centre bit
   constexpr uint32_t kLoaded = ((1u << PMAX) - 1) & ~((1u << (PMAX - P)) - 1);
   constexpr uint32_t kConst = (P < PMAX) ? (1u << (PMAX - P - 1)) : 0u;
-  constexpr uint32_t m0 = (kLoaded * 0x00010001u) << T;
-  constexpr uint32_t g0 = (((uint32_t)(25 - T) << 10) | (kConst << T)) * 0x00010001u;
-  const uint32_t u8 = rotr32(u, 8);
-  a0 = (u & m0) | g0;
-  a2 = (u8 & m0) | g0;
-  if constexpr (T < 3) {
-    constexpr uint32_t m4 = ((kLoaded << 4) * 0x00010001u) << T;
-    constexpr uint32_t g4 = (((uint32_t)(21 - T) << 10) | (kConst << (T + 4))) * 0x00010001u;
-    a1 = (u & m4) | g4;
-    a3 = (u8 & m4) | g4;
-  } else {
-    a1 = (rotr32(u, 4) & m0) | g0;
-    a3 = (rotr32(u, 12) & m0) | g0;
-  }
+  constexpr uint32_t m0 = (kLoaded * 0x00010001u) << Q0;
+  constexpr uint32_t m4 = (kLoaded * 0x00010001u) << (Q0 + 4);
+  constexpr uint32_t g0 = (((uint32_t)(25 - Q0) << 10) | (kConst << Q0)) * 0x00010001u;
+  constexpr uint32_t g4 = (((uint32_t)(21 - Q0) << 10) | (kConst << (Q0 + 4))) * 0x00010001u;
+  const uint32_t ua = R1 ? rotr32(u, R1) : u;
+  const uint32_t ub = rotr32(u, R1 + 8);
+  a0 = lop3_and_or(ua, m0, g0);
+  a1 = lop3_and_or(ua, m4, g4);
+  a2 = lop3_and_or(ub, m0, g0);
+  a3 = lop3_and_or(ub, m4, g4);
 }
 
-// fp16 value offset carried by each A row after the MMA: 2^(10-t) for rows
-// gq (a0/a2), 2^(6-t) for rows gq+8 (a1/a3) except t = 3 (2^7 for both).
-PMPD_DEV float row_offset(int t, int h) { return (h && t < 3) ? (float)(64 >> t) : (float)(1024 >> t); }
+// fp16 value offset carried by each A row after the MMA: 2^(10-Q0) for rows
+// gq (a0/a2), 2^(6-Q0) for rows gq+8 (a1/a3).
+PMPD_DEV float row_offset(int t, int h) {
+  const int q0 = t < 2 ? t : 2;
+  return (float)(1024 >> (q0 + 4 * h));
+}
+
+// ---------------------------------------------------------------- smem plan
+// [Smem | ring: NSTAGE x (PMAX planes + scales) x STILES tiles | xs: staged
+//  activations (XS) | bt: per-warp B~ fragments | red/redb: cross-warp sums]
+template <int PMAX, int MB, bool XS>
+struct Plan {
+  static constexpr int kStage = STILES * (PMAX + 1) * kTilePlaneBytes;
+  static constexpr int kRing = 128;
+  static constexpr int kXs = kRing + NSTAGE * kStage;
+  static constexpr int kXsBytes = XS ? MB * kXsMaxK * 2 : 0;
+  static constexpr int kBt = kXs + kXsBytes;
+  static constexpr int kBtRows = MB == 1 ? 1 : MAXM;
+  static constexpr int kRed = kBt + NCW * kBtRows * 64 * 2;
+  static constexpr int kRedb = kRed + NCW * 64 * MB * 4;
+  static constexpr int kBytes = kRedb + NCW * MB * 4;
+};
+
+// Tile iteration without integer division: stages never straddle an n-group.
+struct TileCursor {
+  int t, ng, kt;
+  PMPD_DEV int stage_end(int T1, int KT) const { return min(min(t + STILES, T1), t - kt + KT); }
+};
 
 // ---------------------------------------------------------------- consumer
 // State of one consumer warp; run() is instantiated per (layout, p_max, p) so
 // that the whole tile loop is specialised for the active precision.
-template <int LAYOUT, int PMAX>
+template <int LAYOUT, int PMAX, int MB, bool XS>
 struct Consumer {
+  using PL = Plan<PMAX, MB, XS>;
   const GemvArgs& a;
   Smem& sm;
-  uint8_t* ring;
-  __half* bt;
+  uint8_t* smem;
+  const __half* xs;  // staged activations [MB][kXsMaxK] (XS) or global x
+  int xld;           // leading dimension of xs
+  uint32_t* bt;      // this warp's B~ fragments, permuted for 2 x LDS.128 per lane
   float* red;
   float* redb;
-  int warp, lane, gq, tig, T0, T1, KT, NT, G, c, stage_bytes, M;
+  int warp, lane, gq, tig, T0, T1, KT, NT, G, c, M;
   float acc[4][4];
-  float aux[4];      // KN: ones-MMA column sums of B~ (cols 2tig, 2tig+1)
-  float bias[MAXM];  // KN: this lane's part of sum_k x*min
+  float aux[4];    // KN: ones-MMA column sums of B~ (cols 2tig, 2tig+1)
+  float bias[MB];  // KN: this lane's part of sum_k x*min
 
   PMPD_DEV void reset() {
 #pragma unroll
@@ -134,13 +170,33 @@ struct Consumer {
 #pragma unroll
     for (int e = 0; e < 4; ++e) aux[e] = 0.f;
 #pragma unroll
-    for (int b = 0; b < MAXM; ++b) bias[b] = 0.f;
+    for (int b = 0; b < MB; ++b) bias[b] = 0.f;
+  }
+
+  // x[b][k..k+1] as float2 (zero outside [0, k_real))
+  PMPD_DEV float2 xpair(int b, int k) const {
+    if constexpr (XS) {
+      return __half22float2(*reinterpret_cast<const __half2*>(xs + b * xld + k));
+    } else {
+      const __half* xr = xs + (int64_t)b * xld;
+      if (k + 1 < a.k_real) return __half22float2(*reinterpret_cast<const __half2*>(xr + k));
+      return make_float2(k < a.k_real ? __half2float(xr[k]) : 0.f, 0.f);
+    }
+  }
+  PMPD_DEV uint32_t xword(int b, int k) const {
+    if constexpr (XS) {
+      return *reinterpret_cast<const uint32_t*>(xs + b * xld + k);
+    } else {
+      const __half* xr = xs + (int64_t)b * xld;
+      if (k + 1 < a.k_real) return __ldg(reinterpret_cast<const unsigned int*>(xr + k));
+      return k < a.k_real ? (uint32_t)__half_as_ushort(xr[k]) : 0u;
+    }
   }
 
   template <int P>
-  PMPD_DEV void tile(const uint8_t* st, int wslot, int tile_idx) {
+  PMPD_DEV void tile(const uint8_t* st, int wslot, int kt) {
     constexpr uint32_t ONES = 0x3C003C00u;
-    const int k0 = (tile_idx % KT) * kTile;
+    const int k0 = kt * kTile;
     uint32_t pw[4][4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -159,47 +215,36 @@ struct Consumer {
         reinterpret_cast<const float*>(st + PMAX * STILES * kTilePlaneBytes + wslot * kTileScaleBytes);
     uint32_t bfr[4][2];
     if constexpr (LAYOUT == PMPD_LAYOUT_KN) {
-      // B~[b][k] = fp16(x[b][k] * step[k]); bias[b] += x[b][k] * min[k]; lane owns k = 2*lane, 2*lane+1
+      // B~[b][k] = fp16(x[b][k] * step[k]); bias[b] += x[b][k] * min[k].  Lane L owns the
+      // half2 word k = 2L, 2L+1 and stores it where reader tig = L&3 finds its 8 words
+      // contiguous: slot (L&3)*8 + (L>>3)*2 + ((L>>2)&1).
       const float2 dl = *reinterpret_cast<const float2*>(sc + 2 * lane);
       const float2 mn = *reinterpret_cast<const float2*>(sc + 64 + 2 * lane);
       const int kk = k0 + 2 * lane;
+      const int slot = (lane & 3) * 8 + (lane >> 3) * 2 + ((lane >> 2) & 1);
 #pragma unroll
-      for (int b = 0; b < MAXM; ++b) {
-        if (b < M) {
-          float2 xf = make_float2(0.f, 0.f);
-          const __half* xr = a.x + (int64_t)b * a.ldx;
-          if (kk + 1 < a.k_real) {
-            xf = __half22float2(*reinterpret_cast<const __half2*>(xr + kk));
-          } else if (kk < a.k_real) {
-            xf.x = __half2float(xr[kk]);
-          }
-          reinterpret_cast<__half2*>(bt + b * 64)[lane] = __floats2half2_rn(xf.x * dl.x, xf.y * dl.y);
+      for (int b = 0; b < MB; ++b) {
+        if (MB == 1 || b < M) {
+          const float2 xf = xpair(b, kk);
+          const __half2 h = __floats2half2_rn(xf.x * dl.x, xf.y * dl.y);
+          bt[b * 32 + slot] = *reinterpret_cast<const uint32_t*>(&h);
           bias[b] = fmaf(xf.x, mn.x, fmaf(xf.y, mn.y, bias[b]));
         }
       }
       __syncwarp();
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        bfr[w][0] = *reinterpret_cast<const uint32_t*>(bt + gq * 64 + 16 * w + 2 * tig);
-        bfr[w][1] = *reinterpret_cast<const uint32_t*>(bt + gq * 64 + 16 * w + 2 * tig + 8);
-      }
+      const int row = MB == 1 ? 0 : gq;
+      uint4 lo = *reinterpret_cast<const uint4*>(bt + row * 32 + tig * 8);
+      uint4 hi = *reinterpret_cast<const uint4*>(bt + row * 32 + tig * 8 + 4);
+      if (gq >= (MB == 1 ? 1 : M)) lo = hi = make_uint4(0u, 0u, 0u, 0u);
+      bfr[0][0] = lo.x; bfr[0][1] = lo.y; bfr[1][0] = lo.z; bfr[1][1] = lo.w;
+      bfr[2][0] = hi.x; bfr[2][1] = hi.y; bfr[3][0] = hi.z; bfr[3][1] = hi.w;
       __syncwarp();
     } else {
+      const bool live = gq < (MB == 1 ? 1 : M);
 #pragma unroll
       for (int w = 0; w < 4; ++w)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int kk = k0 + 16 * w + 2 * tig + 8 * h;
-          uint32_t v = 0;
-          if (gq < M) {
-            const __half* xr = a.x + (int64_t)gq * a.ldx;
-            if (kk + 1 < a.k_real)
-              v = __ldg(reinterpret_cast<const unsigned int*>(xr + kk));
-            else if (kk < a.k_real)
-              v = (uint32_t)__half_as_ushort(xr[kk]);
-          }
-          bfr[w][h] = v;
-        }
+        for (int h = 0; h < 2; ++h) bfr[w][h] = live ? xword(gq, k0 + 16 * w + 2 * tig + 8 * h) : 0u;
     }
 
     float cl[4][4];
@@ -219,7 +264,7 @@ struct Consumer {
       // m-tile t = 0..3 (compile-time t: masks and exponents are immediates)
 #define PMPD_MTILE(T)                                                            \
   {                                                                              \
-    const uint32_t u = merge_planes<PMAX, P>(pj, T);                             \
+    const uint32_t u = merge_planes<PMAX, P, T>(pj);                             \
     nibble_to_frag<PMAX, P, T>(u, a0, a1, a2, a3);                               \
     if constexpr (LAYOUT == PMPD_LAYOUT_KN)                                      \
       mma_f16_16816(acc[T], a0, a1, a2, a3, bfr[w][0], bfr[w][1]);               \
@@ -267,7 +312,8 @@ struct Consumer {
 
   // cross-warp, then (if the n-group is split across CTAs) cross-CTA reduction
   PMPD_DEV void flush(int ng) {
-    float* rw = red + warp * 64 * MAXM;
+    const int Me = MB == 1 ? 1 : M;
+    float* rw = red + warp * 64 * MB;
 #pragma unroll
     for (int t = 0; t < 4; ++t)
 #pragma unroll
@@ -275,53 +321,65 @@ struct Consumer {
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
           const int b = 2 * tig + cc;
-          if (b < M) {
+          if (b < Me) {
             float v = acc[t][2 * h + cc];
             if constexpr (LAYOUT == PMPD_LAYOUT_KN) v = fmaf(-row_offset(t, h), aux[cc], v);
-            rw[(16 * t + gq + 8 * h) * MAXM + b] = v;
+            rw[(16 * t + gq + 8 * h) * MB + b] = v;
           }
         }
     if constexpr (LAYOUT == PMPD_LAYOUT_KN) {
 #pragma unroll
-      for (int b = 0; b < MAXM; ++b)
-        if (b < M) {
+      for (int b = 0; b < MB; ++b)
+        if (MB == 1 || b < M) {
           const float s = warp_sum(bias[b]);
-          if (lane == 0) redb[warp * MAXM + b] = s;
+          if (lane == 0) redb[warp * MB + b] = s;
         }
     }
     named_bar_sync(1, NCW * 32);
     const int tid = threadIdx.x;
     float vals[2] = {0.f, 0.f};
-    int nv = 0;
-    for (int e = tid; e < 64 * M; e += NCW * 32, ++nv) {
-      const int nl = e / M, b = e % M;
-      float v = 0.f;
-      for (int w = 0; w < NCW; ++w) v += red[(w * 64 + nl) * MAXM + b];
-      if constexpr (LAYOUT == PMPD_LAYOUT_KN)
-        for (int w = 0; w < NCW; ++w) v += redb[w * MAXM + b];
-      vals[nv] = v;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int e = tid + r * NCW * 32;
+      if (e < 64 * Me) {
+        const int nl = e / Me, b = e - nl * Me;
+        float v = 0.f;
+#pragma unroll
+        for (int w = 0; w < NCW; ++w) v += red[(w * 64 + nl) * MB + b];
+        if constexpr (LAYOUT == PMPD_LAYOUT_KN) {
+#pragma unroll
+          for (int w = 0; w < NCW; ++w) v += redb[w * MB + b];
+        }
+        vals[r] = v;
+      }
     }
     const bool whole = (T0 <= ng * KT) && ((ng + 1) * KT <= T1);
     if (whole) {
-      nv = 0;
-      for (int e = tid; e < 64 * M; e += NCW * 32, ++nv) store(ng, e / M, e % M, vals[nv]);
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int e = tid + r * NCW * 32;
+        if (e < 64 * Me) store(ng, e / Me, e % Me, vals[r]);
+      }
     } else {
       const int tile_first = ng * KT, tile_last = min((ng + 1) * KT, NT) - 1;
       const int c_first = (int)(((int64_t)(tile_first + 1) * G + NT - 1) / NT) - 1;
       const int c_last = (int)(((int64_t)(tile_last + 1) * G + NT - 1) / NT) - 1;
-      float* part = a.partial + (int64_t)ng * a.max_slots * 64 * M;
-      nv = 0;
-      for (int e = tid; e < 64 * M; e += NCW * 32, ++nv) part[(int64_t)(c - c_first) * 64 * M + e] = vals[nv];
+      float* part = a.partial + (int64_t)ng * a.max_slots * 64 * Me;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int e = tid + r * NCW * 32;
+        if (e < 64 * Me) part[(int64_t)(c - c_first) * 64 * Me + e] = vals[r];
+      }
       __threadfence();
       named_bar_sync(1, NCW * 32);
       if (tid == 0) sm.flag = (atomicAdd(&a.counters[ng], 1) == c_last - c_first);
       named_bar_sync(1, NCW * 32);
       if (sm.flag) {
         __threadfence();
-        for (int e = tid; e < 64 * M; e += NCW * 32) {
+        for (int e = tid; e < 64 * Me; e += NCW * 32) {
           float v = 0.f;
-          for (int s2 = 0; s2 <= c_last - c_first; ++s2) v += __ldcg(part + (int64_t)s2 * 64 * M + e);
-          store(ng, e / M, e % M, v);
+          for (int s2 = 0; s2 <= c_last - c_first; ++s2) v += __ldcg(part + (int64_t)s2 * 64 * Me + e);
+          store(ng, e / Me, e % Me, v);
         }
         if (tid == 0) a.counters[ng] = 0;
       }
@@ -334,30 +392,33 @@ struct Consumer {
   PMPD_DEV void run() {
     reset();
     int si = 0;
-    for (int t = T0; t < T1; ++si) {
-      const int end = min(min(t + STILES, T1), (t / KT + 1) * KT);
+    TileCursor cur{T0, T0 / KT, T0 % KT};
+    while (cur.t < T1) {
+      const int end = cur.stage_end(T1, KT);
       const int slot = si % NSTAGE;
-      const int ng = t / KT;
       mbar_wait(&sm.full[slot], (si / NSTAGE) & 1);
-      if (warp < end - t) tile<P>(ring + slot * stage_bytes, warp, t + warp);
+      if (warp < end - cur.t) tile<P>(smem + PL::kRing + slot * PL::kStage, warp, cur.kt + warp);
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[slot]);
-      t = end;
-      if (t == T1 || t / KT != ng) flush(ng);
+      const int ng = cur.ng;
+      cur.kt += end - cur.t;
+      cur.t = end;
+      ++si;
+      if (cur.kt == KT || cur.t == T1) flush(ng);
+      if (cur.kt == KT) {
+        cur.kt = 0;
+        ++cur.ng;
+      }
     }
   }
 };
 
 // ---------------------------------------------------------------- kernel
-template <int LAYOUT, int PMAX>
+template <int LAYOUT, int PMAX, int MB, bool XS>
 __global__ void __launch_bounds__(NTHREADS, 2) qgemv_kernel(const GemvArgs a) {
+  using PL = Plan<PMAX, MB, XS>;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-  const int stage_bytes = STILES * (PMAX + 1) * kTilePlaneBytes;
-  uint8_t* ring = smem_raw + 128;
-  __half* bt_all = reinterpret_cast<__half*>(ring + NSTAGE * stage_bytes);  // KN: [NCW][MAXM][64]
-  float* red = reinterpret_cast<float*>(bt_all + NCW * MAXM * 64);          // [NCW][64][MAXM]
-  float* redb = red + NCW * 64 * MAXM;                                      // [NCW][MAXM]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int NT = a.n_tiles * a.k_tiles, KT = a.k_tiles;
@@ -386,26 +447,33 @@ __global__ void __launch_bounds__(NTHREADS, 2) qgemv_kernel(const GemvArgs a) {
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       int si = 0;
-      for (int t = T0; t < T1; ++si) {
-        const int end = min(min(t + STILES, T1), (t / KT + 1) * KT);
-        const int cnt = end - t, slot = si % NSTAGE;
+      TileCursor cur{T0, T0 / KT, T0 % KT};
+      while (cur.t < T1) {
+        const int end = cur.stage_end(T1, KT);
+        const int cnt = end - cur.t, slot = si % NSTAGE;
         if (si >= NSTAGE) mbar_wait(&sm.empty[slot], ((si / NSTAGE) & 1) ^ 1);
-        uint8_t* st = ring + slot * stage_bytes;
+        uint8_t* st = smem_raw + PL::kRing + slot * PL::kStage;
         mbar_arrive_expect_tx(&sm.full[slot], (uint32_t)(cnt * kTilePlaneBytes * (p + 1)));
         for (int j = 0; j < p; ++j)
           bulk_g2s_stream(st + j * STILES * kTilePlaneBytes,
-                          a.planes + j * a.plane_bytes + (int64_t)t * kTilePlaneBytes, cnt * kTilePlaneBytes,
+                          a.planes + j * a.plane_bytes + (int64_t)cur.t * kTilePlaneBytes, cnt * kTilePlaneBytes,
                           &sm.full[slot], pol);
-        bulk_g2s_stream(st + PMAX * STILES * kTilePlaneBytes, a.scales + (int64_t)t * kTileScaleBytes,
+        bulk_g2s_stream(st + PMAX * STILES * kTilePlaneBytes, a.scales + (int64_t)cur.t * kTileScaleBytes,
                         cnt * kTileScaleBytes, &sm.full[slot], pol);
-        t = end;
+        cur.kt += cnt;
+        cur.t = end;
+        if (cur.kt == KT) cur.kt = 0;
+        ++si;
       }
     }
     return;
   }
 
   // -------------------------------------------------------------- consumers
-  Consumer<LAYOUT, PMAX> cs{a, sm, ring, bt_all + warp * MAXM * 64, red, redb};
+  Consumer<LAYOUT, PMAX, MB, XS> cs{a, sm, smem_raw};
+  cs.bt = reinterpret_cast<uint32_t*>(smem_raw + PL::kBt) + warp * PL::kBtRows * 32;
+  cs.red = reinterpret_cast<float*>(smem_raw + PL::kRed);
+  cs.redb = reinterpret_cast<float*>(smem_raw + PL::kRedb);
   cs.warp = warp;
   cs.lane = lane;
   cs.gq = lane >> 2;
@@ -416,13 +484,33 @@ __global__ void __launch_bounds__(NTHREADS, 2) qgemv_kernel(const GemvArgs a) {
   cs.NT = NT;
   cs.G = G;
   cs.c = c;
-  cs.stage_bytes = stage_bytes;
   cs.M = a.m;
-  if constexpr (LAYOUT == PMPD_LAYOUT_KN) {
-    for (int i = lane; i < MAXM * 64; i += 32) cs.bt[i] = __float2half(0.f);
-    __syncwarp();
-  }
   pdl_wait();  // activations and the workspace belong to the predecessor until here
+  if constexpr (XS) {
+    // stage x (zero-padded to a multiple of 64) in shared memory once
+    __half* xs = reinterpret_cast<__half*>(smem_raw + PL::kXs);
+    const int kp = KT * kTile;
+    for (int b = 0; b < MB; ++b)
+      for (int k = threadIdx.x * 8; k < kp; k += NCW * 32 * 8) {
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        const __half* src = a.x + (int64_t)b * a.ldx + k;
+        if (k + 8 <= a.k_real && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+          v = __ldg(reinterpret_cast<const uint4*>(src));
+        } else {
+          __half tmp[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) tmp[i] = (k + i < a.k_real) ? src[i] : __float2half(0.f);
+          v = *reinterpret_cast<const uint4*>(tmp);
+        }
+        *reinterpret_cast<uint4*>(xs + b * kXsMaxK + k) = v;
+      }
+    named_bar_sync(1, NCW * 32);
+    cs.xs = xs;
+    cs.xld = kXsMaxK;
+  } else {
+    cs.xs = a.x;
+    cs.xld = a.ldx;
+  }
   switch (p) {
     case 4:
       if constexpr (PMAX >= 4) cs.template run<4>();
@@ -439,12 +527,11 @@ __global__ void __launch_bounds__(NTHREADS, 2) qgemv_kernel(const GemvArgs a) {
   }
 }
 
-template <int LAYOUT, int PMAX>
-int launch(const GemvArgs& a, int grid, cudaStream_t s) {
-  const int stage_bytes = STILES * (PMAX + 1) * kTilePlaneBytes;
-  const size_t smem = 128 + (size_t)NSTAGE * stage_bytes + NCW * MAXM * 64 * sizeof(__half) +
-                      (NCW * 64 * MAXM + NCW * MAXM) * sizeof(float);
-  auto kern = qgemv_kernel<LAYOUT, PMAX>;
+template <int LAYOUT, int PMAX, int MB, bool XS>
+int launch_m(const GemvArgs& a, int grid, cudaStream_t s) {
+  using PL = Plan<PMAX, MB, XS>;
+  const size_t smem = PL::kBytes;
+  auto kern = qgemv_kernel<LAYOUT, PMAX, MB, XS>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -465,9 +552,28 @@ int launch(const GemvArgs& a, int grid, cudaStream_t s) {
   return PMPD_OK;
 }
 
+template <int LAYOUT, int PMAX>
+int launch(const GemvArgs& a, int grid, cudaStream_t s) {
+  if (a.m == 1)
+    return a.k_tiles * kTile <= kXsMaxK ? launch_m<LAYOUT, PMAX, 1, true>(a, grid, s)
+                                        : launch_m<LAYOUT, PMAX, 1, false>(a, grid, s);
+  return launch_m<LAYOUT, PMAX, MAXM, false>(a, grid, s);
+}
+
+int ctas_per_sm() {
+  static int v = 0;
+  if (v == 0) {
+    const char* e = getenv("PMPD_GEMV_CTAS_PER_SM");
+    v = e ? atoi(e) : 1;
+    if (v < 1 || v > 4) v = 1;
+  }
+  return v;
+}
+
 int grid_for(const pmpd_qtensor* t) {
   const int nt = t->n_tiles * t->k_tiles;
-  return nt < num_sms() ? nt : num_sms();
+  const int g = num_sms() * ctas_per_sm();
+  return nt < g ? nt : g;
 }
 
 int slots_for(const pmpd_qtensor* t) {

@@ -94,6 +94,19 @@ PMPD_DEV void mma_f16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2
 }
 
 PMPD_DEV uint32_t rotr32(uint32_t x, int s) { return __funnelshift_r(x, x, s); }
+
+// Explicit 3-input LOP3s: the compiler otherwise splits (a & K1) | K2 and
+// bit-selects with constant masks into two instructions.
+PMPD_DEV uint32_t lop3_and_or(uint32_t a, uint32_t b, uint32_t c) {  // (a & b) | c
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+PMPD_DEV uint32_t lop3_select(uint32_t a, uint32_t b, uint32_t m) {  // (a & m) | (b & ~m)
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(d) : "r"(a), "r"(b), "r"(m));
+  return d;
+}
 PMPD_DEV uint32_t half2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 
 PMPD_DEV float warp_sum(float v) {

@@ -1,0 +1,167 @@
+"""The decode-token linear stack of a Llama-shaped model, B200-resident.
+
+This is the unit the headline metric is quoted on (BASELINE.json: "7B decode
+linear-layer µs/token & HBM GB/s at 2/3/4-bit, batch 1"): for every layer the
+fused q|k|v projection, o, the fused gate|up projection and down, then the
+vocabulary head — exactly the linear call sites of one reference decode step
+(pkg/src/pmpd/tinylm.py:341-343,359,362,364,368), each a GEMV over the nested
+bit-plane weights at the precision chosen on device by the schedule hook.
+
+The chain keeps the real data dependencies (each GEMV consumes the previous
+output; q|k|v of layer i+1 reads down of layer i) and scales every output by
+1/(std*sqrt(K)) so activations stay O(1) without the attention/norm glue.
+One token = one CUDA-graph replay; the precision of token i is
+``PrecisionSchedule.precision_at(i)`` evaluated by ``pmpd_sched_step``.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+import torch.nn.functional as F
+
+from . import _capi
+from .linear import Workspace, gemv, workspace_bytes
+from .quant import QuantizedTensor, quantize_tensor
+
+
+@dataclass(frozen=True)
+class StackShape:
+    n_layers: int
+    d_model: int
+    d_ff: int
+    vocab: int
+
+    @property
+    def weights_per_token(self) -> int:
+        d, f = self.d_model, self.d_ff
+        return self.n_layers * (4 * d * d + 3 * d * f) + d * self.vocab
+
+
+LLAMA2_7B = StackShape(32, 4096, 11008, 32000)
+MOBILELLAMA_1B4 = StackShape(24, 2048, 5632, 32000)
+
+
+def algorithmic_bytes(shape: StackShape, p: int, m: int = 1, group_size: int = 64) -> int:
+    """perf.py:96-101 accounting (p/8 bytes + 8 bytes of f32 min/step per group) plus activations."""
+    w = shape.weights_per_token
+    if p == 16:
+        wb = 2 * w
+    else:
+        wb = w * p // 8 + 8 * w // group_size
+    d, f, L = shape.d_model, shape.d_ff, shape.n_layers
+    act = L * 2 * m * ((d + 3 * d) + (d + d) + (d + 2 * f) + (f + d)) + 2 * m * d + 4 * m * shape.vocab
+    return wb + act
+
+
+def _rand_kn(K: int, N: int, std: float, gen: torch.Generator) -> torch.Tensor:
+    return torch.randn((K, N), generator=gen, device="cuda", dtype=torch.float32).mul_(std)
+
+
+class LinearStack:
+    """Quantized (nested 4/3/2-bit) weights of every decode linear layer, packed for the GEMV."""
+
+    def __init__(self, shape: StackShape, p_max: int = 4, group_size: int = 64, seed: int = 0, std: float = 0.02,
+                 m: int = 1, keep_fp16: bool = False):
+        self.shape, self.p_max, self.m, self.std = shape, p_max, m, std
+        d, f, V = shape.d_model, shape.d_ff, shape.vocab
+        gen = torch.Generator(device="cuda")
+        gen.manual_seed(seed)
+        self.layers = []
+        self.fp16 = [] if keep_fp16 else None
+
+        def make(K, N):
+            w = _rand_kn(K, N, std, gen)
+            qt = quantize_tensor(w, p_max, group_size)
+            pk = qt.packed(_capi.LAYOUT_KN)
+            qt.drop_reference_copy()
+            if keep_fp16:
+                alpha = 1.0 / (std * math.sqrt(K))
+                self.fp16.append((w.t().contiguous() * alpha).half())  # (N, K) for F.linear
+            del w
+            return qt, pk
+
+        for _ in range(shape.n_layers):
+            self.layers.append([make(d, 3 * d), make(d, d), make(d, 2 * f), make(f, d)])
+        self.head = make(d, V)
+        torch.cuda.synchronize()
+        ws = max(workspace_bytes(pk, m) for lay in self.layers + [[self.head]] for _, pk in lay)
+        self.ws = Workspace(ws)
+        self.x0 = torch.randn((m, d), device="cuda").half()
+        self.qkv = torch.empty((m, 3 * d), device="cuda", dtype=torch.float16)
+        self.o = torch.empty((m, d), device="cuda", dtype=torch.float16)
+        self.u = torch.empty((m, 2 * f), device="cuda", dtype=torch.float16)
+        self.h = torch.empty((m, d), device="cuda", dtype=torch.float16)
+        self.logits = torch.empty((m, V), device="cuda", dtype=torch.float32)
+        self.p_dev = torch.full((1,), p_max, dtype=torch.int32, device="cuda")
+        self.step = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.sched = torch.tensor([p_max, 0], dtype=torch.int32, device="cuda")
+        self.n_prec = 1
+
+    # -------------------------------------------------------------- schedule
+    def set_schedule(self, switch_points: dict) -> None:
+        """Device switch-point table {p: first token index}; the step counter restarts at 0."""
+        flat = []
+        for p, st in sorted(switch_points.items(), reverse=True):
+            flat += [int(p), int(st)]
+        self.sched = torch.tensor(flat, dtype=torch.int32, device="cuda")
+        self.n_prec = len(switch_points)
+        self.step.zero_()
+
+    def reset_step(self, value: int = 0) -> None:
+        self.step.fill_(value)
+
+    # -------------------------------------------------------------- one token
+    def token(self) -> None:
+        """Issue one decode token's linear stack on the current stream (graph-capturable)."""
+        s = torch.cuda.current_stream().cuda_stream
+        _capi.call("pmpd_sched_step", self.sched.data_ptr(), self.n_prec, self.step.data_ptr(),
+                   self.p_dev.data_ptr(), 1, s)
+        d, f = self.shape.d_model, self.shape.d_ff
+        a_d = 1.0 / (self.std * math.sqrt(d))
+        a_f = 1.0 / (self.std * math.sqrt(f))
+        inp = self.x0
+        for (_, wqkv), (_, wo), (_, wup), (_, wdn) in self.layers:
+            gemv(wqkv, inp, self.p_dev, self.ws, out=self.qkv, alpha=a_d)
+            gemv(wo, self.qkv[:, 2 * d:], self.p_dev, self.ws, out=self.o, alpha=a_d)
+            gemv(wup, self.o, self.p_dev, self.ws, out=self.u, alpha=a_d)
+            gemv(wdn, self.u[:, :f], self.p_dev, self.ws, out=self.h, alpha=a_f)
+            inp = self.h
+        gemv(self.head[1], inp, self.p_dev, self.ws, out=self.logits, alpha=a_d)
+
+    def token_fp16(self) -> None:
+        """fp16 baseline of the same chain through cuBLAS (precision 16, tinylm.py:204-213)."""
+        d, f = self.shape.d_model, self.shape.d_ff
+        inp = self.x0
+        L = self.shape.n_layers
+        for i in range(L):
+            wqkv, wo, wup, wdn = self.fp16[4 * i: 4 * i + 4]
+            torch.matmul(inp, wqkv.t(), out=self.qkv)
+            torch.matmul(self.qkv[:, 2 * d:], wo.t(), out=self.o)
+            torch.matmul(self.o, wup.t(), out=self.u)
+            torch.matmul(self.u[:, :f], wdn.t(), out=self.h)
+            inp = self.h
+        self.logits.copy_(F.linear(inp, self.fp16[-1]).float())
+
+    def capture(self, fn) -> torch.cuda.CUDAGraph:
+        """CUDA graph of one token (fn = self.token or self.token_fp16)."""
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            fn()  # warm-up (workspace sizing, cuBLAS handles)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        torch.cuda.synchronize()
+        return g
+
+    def stream_bytes(self, p: int) -> int:
+        """Bytes of packed weights the GEMVs actually fetch at precision p."""
+        tot = 0
+        for lay in self.layers + [[self.head]]:
+            for _, pk in lay:
+                tot += pk.stream_bytes(p)
+        return tot

@@ -143,7 +143,9 @@ int pmpd_gemv(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, int32_t m, 
 
 /* Per-token precision hook: replaces PrecisionSchedule.precision_at
  * (schedule.py:93-99) as called by generate (tinylm.py:512,518).
- * sched_dev: int32 [2*n_prec] = {p_0, st_0, p_1, st_1, ...} (any order);
+ * sched_dev: int32 [2*n_prec] = {p_0, st_0, p_1, st_1, ...} (any order; entries
+ * with p <= 0 are unused, so a fixed-capacity table can be rewritten in place
+ * without re-capturing a CUDA graph);
  * step_dev: int32 decode-step counter.  Writes the lowest precision whose
  * switch point is <= *step_dev to *p_out_dev, then (if advance) increments
  * *step_dev.  Entirely on device: no host sync inside a captured decode step. */

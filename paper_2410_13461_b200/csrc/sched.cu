@@ -17,6 +17,7 @@ __global__ void sched_step_kernel(const int32_t* __restrict__ sched, int n_prec,
   int best = -1, highest = -1;
   for (int q = 0; q < n_prec; ++q) {
     const int p = sched[2 * q], st = sched[2 * q + 1];
+    if (p <= 0) continue;  // unused entry of a fixed-capacity table
     if (p > highest) highest = p;
     if (st <= i && (best < 0 || p < best)) best = p;
   }

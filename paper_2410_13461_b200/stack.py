@@ -39,6 +39,8 @@ class StackShape:
         return self.n_layers * (4 * d * d + 3 * d * f) + d * self.vocab
 
 
+SCHED_CAPACITY = 8
+
 LLAMA2_7B = StackShape(32, 4096, 11008, 32000)
 MOBILELLAMA_1B4 = StackShape(24, 2048, 5632, 32000)
 
@@ -96,17 +98,18 @@ class LinearStack:
         self.logits = torch.empty((m, V), device="cuda", dtype=torch.float32)
         self.p_dev = torch.full((1,), p_max, dtype=torch.int32, device="cuda")
         self.step = torch.zeros(1, dtype=torch.int32, device="cuda")
-        self.sched = torch.tensor([p_max, 0], dtype=torch.int32, device="cuda")
-        self.n_prec = 1
+        # fixed-capacity device switch-point table (rewritten in place: graphs keep its address)
+        self.sched = torch.zeros(2 * SCHED_CAPACITY, dtype=torch.int32, device="cuda")
+        self.n_prec = SCHED_CAPACITY
+        self.set_schedule({p_max: 0})
 
     # -------------------------------------------------------------- schedule
     def set_schedule(self, switch_points: dict) -> None:
         """Device switch-point table {p: first token index}; the step counter restarts at 0."""
-        flat = []
-        for p, st in sorted(switch_points.items(), reverse=True):
-            flat += [int(p), int(st)]
-        self.sched = torch.tensor(flat, dtype=torch.int32, device="cuda")
-        self.n_prec = len(switch_points)
+        flat = [0] * (2 * SCHED_CAPACITY)
+        for i, (p, st) in enumerate(sorted(switch_points.items(), reverse=True)):
+            flat[2 * i], flat[2 * i + 1] = int(p), int(st)
+        self.sched.copy_(torch.tensor(flat, dtype=torch.int32))
         self.step.zero_()
 
     def reset_step(self, value: int = 0) -> None:

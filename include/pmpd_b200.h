@@ -152,6 +152,57 @@ int pmpd_gemv(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, int32_t m, 
 int pmpd_sched_step(const int32_t* sched_dev, int32_t n_prec, int32_t* step_dev, int32_t* p_out_dev, int32_t advance,
                     void* stream);
 
+/* ------------------------------------------------------------- decoder glue
+ * The non-linear parts of one forward step (tinylm.py:293-368); residual
+ * stream f32, GEMV inputs f16, KV cache f16 [max_ctx][d] per layer holding
+ * post-RoPE K and V rows (KVCache, tinylm.py:272-286).  *T_dev is the number
+ * of cached tokens before the step, read on device (graph-replayable). */
+
+/* out (f16, ldo) = x / sqrt(mean(x^2) + eps) * gain, per row (_rmsnorm, tinylm.py:293-295). */
+int pmpd_rmsnorm(const float* x_dev, int32_t ldx, const float* gain_dev, int32_t m, int32_t d, float eps, void* out_dev,
+                 int32_t ldo, void* stream);
+
+/* Rotate-half RoPE of q|k (tinylm.py:308-319,344-345) for m tokens at positions
+ * *T_dev + i; rotated q -> q_out (f32 [m][d]); rotated k and v -> cache rows
+ * (tinylm.py:346-347).  cos/sin: f32 [max_ctx][d_head/2] from float64 tables. */
+int pmpd_rope_kv(const float* qkv_dev, int32_t ldq, int32_t m, int32_t d, int32_t d_head, const float* cos_dev,
+                 const float* sin_dev, const int32_t* T_dev, int32_t max_ctx, float* q_out_dev, void* k_cache_dev,
+                 void* v_cache_dev, void* stream);
+
+/* Causal softmax attention of m queries over cache rows 0..T+i (tinylm.py:349-358) -> f16 [m][d]. */
+int pmpd_attention(const float* q_dev, int32_t m, int32_t d, int32_t d_head, const void* k_cache_dev,
+                   const void* v_cache_dev, const int32_t* T_dev, int32_t max_ctx, float scale, void* out_dev,
+                   void* stream);
+
+/* out (f16) = silu(u[:, :ff]) * u[:, ff:] (tinylm.py:362-364). */
+int pmpd_silu_mul(const float* u_dev, int32_t ldu, int32_t m, int32_t ff, void* out_dev, int32_t ldo, void* stream);
+
+/* Greedy sample: argmax per row, lowest index on ties (sample, tinylm.py:422-429);
+ * sets *bad_dev = 1 if a logit is non-finite (InputError in the reference). */
+int pmpd_argmax(const float* logits_dev, int32_t ld, int32_t m, int32_t vocab, int32_t* out_dev, int32_t* bad_dev,
+                void* stream);
+
+/* *p += v on device (cache-length and step counters). */
+int pmpd_add_i32(int32_t* p_dev, int32_t v, void* stream);
+
+/* dst[*idx_dev][0..n) = src[0..n) if *idx_dev < capacity (per-step logits history). */
+int pmpd_store_row(const float* src_dev, float* dst_dev, const int32_t* idx_dev, int32_t n, int32_t capacity,
+                   void* stream);
+
+/* Device bookkeeping of one generated token: tokens[*n] = *cur; *n += 1; *T += 1 (if T). */
+int pmpd_push_token(const int32_t* cur_dev, int32_t* tokens_dev, int32_t* n_dev, int32_t* T_dev, int32_t capacity,
+                    void* stream);
+
+/* Learned switch predictor on device (learnsched.py:118-125,151-160):
+ * attention-pool cache rows 0..T-1 of the feature block with query q, ReLU MLP,
+ * argmax (lowest on ties) -> grid point; writes the two-phase schedule
+ * {p_high: 0, p_low: grid[cls]} into the fixed-capacity table sched_dev
+ * (int32[16], the pmpd_sched_step format).  dbg_logits (optional, f32[ncls]). */
+int pmpd_learned_predict(const void* k_dev, const void* v_dev, int32_t ldkv, const int32_t* T_dev, int32_t max_T,
+                         int32_t dk, int32_t dv, int32_t hidden, int32_t ncls, const float* q_dev, const float* w1_dev,
+                         const float* b1_dev, const float* w2_dev, const float* b2_dev, const int32_t* grid_dev,
+                         int32_t p_high, int32_t p_low, int32_t* sched_dev, float* dbg_logits_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

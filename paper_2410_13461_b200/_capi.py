@@ -59,6 +59,15 @@ SIGNATURES = {
     "pmpd_gemv_workspace_bytes": [_D, _I, ctypes.POINTER(_L)],
     "pmpd_gemv": [_D, _P, _I, _I, _P, _P, _I, _I, _F, _I, _P, _L, _P],
     "pmpd_sched_step": [_P, _I, _P, _P, _I, _P],
+    "pmpd_rmsnorm": [_P, _I, _P, _I, _I, _F, _P, _I, _P],
+    "pmpd_rope_kv": [_P, _I, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P],
+    "pmpd_attention": [_P, _I, _I, _I, _P, _P, _P, _I, _F, _P, _P],
+    "pmpd_silu_mul": [_P, _I, _I, _I, _P, _I, _P],
+    "pmpd_argmax": [_P, _I, _I, _I, _P, _P, _P],
+    "pmpd_add_i32": [_P, _I, _P],
+    "pmpd_push_token": [_P, _P, _P, _P, _I, _P],
+    "pmpd_store_row": [_P, _P, _P, _I, _I, _P],
+    "pmpd_learned_predict": [_P, _P, _I, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P],
 }
 _RESTYPES = {"pmpd_last_error": ctypes.c_char_p}
 

@@ -1,0 +1,175 @@
+"""GPU parity of the device model (prefill / decode / generate, schedulers) against the
+reference golden vectors and the float64 oracle."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import learnsched as olearn
+from oracle import model as om
+from oracle import schedule as osched
+from paper_2410_13461_b200 import learnsched, quant, tinylm
+from paper_2410_13461_b200.errors import ConfigError, ContractViolation, InputError
+from paper_2410_13461_b200.schedule import FixedScheduler, PrecisionSchedule, StaticScheduler, SwitchGrid
+from pmpd_testutil import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2  # north star: logits within rel-L2 <= 1e-2
+
+
+@pytest.fixture(scope="module")
+def small():
+    cfg = tinylm.ModelConfig(n_layers=2, n_heads=2, d_model=64, d_ff=128, max_context=128)
+    return tinylm.ModelVariants.from_random(cfg, quant.PrecisionSet((4, 3, 2)), seed=7)
+
+
+@pytest.fixture(scope="module")
+def toy():
+    cfg = tinylm.ModelConfig(n_layers=4, n_heads=4, d_model=128, d_ff=256, max_context=256)
+    return tinylm.ModelVariants.from_random(cfg, quant.PrecisionSet((4, 3, 2)), seed=11)
+
+
+def host(t):
+    return t.double().cpu().numpy()
+
+
+def test_weights_bit_identical_to_reference(small, gold_model):
+    import hashlib
+
+    def sha(a):
+        return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+    for name, t in small.tensors.items():
+        got = sha(t.store.planes.cpu().numpy()) + sha(t.mins.cpu().numpy()) + sha(t.deltas.cpu().numpy())
+        assert got == str(gold_model[f"small/sha/{name}"]), name
+
+
+def test_forward_full_all_precisions(small, gold_model):
+    toks = [int(t) for t in gold_model["small/tokens"]]
+    for p in (2, 3, 4, 16):
+        got = host(tinylm.forward_full(small, p, toks))
+        err = rel_l2(got, gold_model[f"small/full{p}"])
+        assert err < TOL, (p, err)
+
+
+def test_toy_model_criterion6_incremental_equals_full(toy, gold_model):
+    toks = [int(t) for t in gold_model["toy/tokens"]]
+    for p in (2, 3, 4, 16):
+        full = host(tinylm.forward_full(toy, p, toks))
+        assert rel_l2(full, gold_model[f"toy/full{p}"]) < TOL, p
+        _, cache = tinylm.prefill(toy, p, toks[:1])
+        got = [host(tinylm.forward_full(toy, p, toks[:1])[0])]
+        for t in toks[1:]:
+            lg, cache = tinylm.decode_step(toy, p, t, cache)
+            got.append(host(lg))
+        # device incremental vs device full: same arithmetic up to f16 KV rounding
+        assert rel_l2(np.array(got), full) < 2e-3, p
+
+
+def test_progressive_decode_logits(small, gold_model):
+    prompt = [int(t) for t in gold_model["small/prompt"]]
+    lg, cache = tinylm.prefill(small, 4, prompt)
+    assert rel_l2(host(lg), gold_model["small/prefill4"]) < TOL
+    sched = PrecisionSchedule((4, 3, 2), 4, {4: 0, 3: 4, 2: 9}, 24)
+    tok = int(np.argmax(gold_model["small/prefill4"]))
+    for i, ref in enumerate(gold_model["small/decode_logits"]):
+        lg, cache = tinylm.decode_step(small, sched.precision_at(i), tok, cache)
+        assert rel_l2(host(lg), ref) < TOL, i
+        tok = int(np.argmax(ref))  # teacher-forced on the reference tokens
+
+
+def test_generate_traces_match_reference(small, gold_model):
+    prompt = [int(t) for t in gold_model["small/prompt"]]
+    runs = {
+        "fixed4": (FixedScheduler(4), None, 10, prompt),
+        "two_phase": (StaticScheduler(PrecisionSchedule.two_phase(3, 2, 3, 16, p_prefill=4)), None, 8, prompt),
+        "prog432": (StaticScheduler(PrecisionSchedule((4, 3, 2), 4, {4: 0, 3: 4, 2: 9}, 24)), -1, 24, prompt),
+        "fp16": (FixedScheduler(16), None, 6, prompt),
+    }
+    net = learnsched.SchedulerNet.init(64, 64, 8, SwitchGrid(5, 16), 3, 2, seed=0)
+    runs["learned"] = (learnsched.LearnedScheduler(net, p_prefill=4), None, 12, list(b"A lantern in the window"))
+    for k, (sch, eos, mx, pr) in runs.items():
+        tr = tinylm.generate(small, pr, sch, eos_id=eos, max_new=mx, record_logits=True)
+        assert tr.output_tokens == gold_model[f"small/trace/{k}/tokens"].tolist(), k
+        assert tr.precisions == gold_model[f"small/trace/{k}/precisions"].tolist(), k
+        assert sorted(tr.schedule.switch_points.items()) == [tuple(r) for r in gold_model[f"small/trace/{k}/st"].tolist()]
+        assert tr.termination == str(gold_model[f"small/trace/{k}/term"]), k
+
+
+def test_generate_logits_track_oracle_teacher_forced(small, gold_model):
+    """Per-step logits of the device generation vs the oracle fed the same tokens."""
+    prompt = [int(t) for t in gold_model["small/prompt"]]
+    sch = StaticScheduler(PrecisionSchedule((4, 3, 2), 4, {4: 0, 3: 4, 2: 9}, 24))
+    tr = tinylm.generate(small, prompt, sch, eos_id=-1, max_new=24, record_logits=True)
+    cfg = om.Config(n_layers=2, n_heads=2, d_model=64, d_ff=128, max_context=128)
+    m = om.Model.from_random(cfg, (4, 3, 2), seed=7)
+    lg, cache = om.prefill(m, 4, prompt)
+    refs = [lg]
+    osc = osched.Schedule((4, 3, 2), 4, {4: 0, 3: 4, 2: 9}, 24)
+    for i, tok in enumerate(tr.output_tokens[:-1]):
+        lg, cache = om.decode_step(m, osc.precision_at(i), tok, cache)
+        refs.append(lg)
+    got = host(tr.logits)
+    for i, ref in enumerate(refs):
+        assert rel_l2(got[i], ref) < TOL, i
+
+
+def test_learned_predictor_device(gold_learn):
+    net = learnsched.SchedulerNet.init(16, 16, 8, SwitchGrid(5, 16), 3, 2, seed=3)
+    for t in (1, 7, 40):
+        K, V = gold_learn[f"T{t}/K"], gold_learn[f"T{t}/V"]
+        lg = learnsched.class_logits(net, K, V)
+        ref = gold_learn[f"T{t}/logits"]
+        assert np.max(np.abs(lg - ref)) < 5e-3 * max(1.0, np.max(np.abs(ref)))
+
+        class C:
+            def layer_kv(self, layer, K=K, V=V):
+                return K, V
+        s = learnsched.predict_schedule(net, C(), 4)
+        assert sorted(s.switch_points.items()) == [tuple(r) for r in gold_learn[f"T{t}/st"].tolist()]
+
+
+def test_contracts_and_errors(small):
+    prompt = list(b"The river")
+    with pytest.raises(ContractViolation):
+        tinylm.generate(small, prompt, StaticScheduler(PrecisionSchedule.two_phase(6, 2, 3, 16)), max_new=8)
+    with pytest.raises(ContractViolation):
+        tinylm.generate(small, prompt, StaticScheduler(PrecisionSchedule((4, 3), 4, {4: 5, 3: 1}, 16)), max_new=8)
+    with pytest.raises(InputError):
+        tinylm.generate(small, prompt, StaticScheduler(PrecisionSchedule.two_phase(3, 2, 2, 8)), max_new=9)
+    with pytest.raises(InputError):
+        tinylm.prefill(small, 4, [])
+    with pytest.raises(InputError):
+        tinylm.prefill(small, 4, [999])
+    with pytest.raises(InputError):
+        tinylm.prefill(small, 4, [1] * 128)
+    with pytest.raises(ContractViolation):
+        tinylm.prefill(small, 5, prompt)
+    with pytest.raises(ContractViolation):
+        small.weights("embed", 5)
+    cfg = tinylm.ModelConfig(n_layers=1, n_heads=2, d_model=64, d_ff=64, max_context=8)
+    m = tinylm.ModelVariants.from_random(cfg, quant.PrecisionSet((3,)), seed=1)
+    _, cache = tinylm.prefill(m, 3, [1] * 7)
+    tinylm.decode_step(m, 3, 1, cache)
+    with pytest.raises(InputError):
+        tinylm.decode_step(m, 3, 1, cache)
+
+
+def test_eos_termination(small):
+    prompt = list(b"The river finds its way")
+    lg, _ = tinylm.prefill(small, 4, prompt)
+    eos = int(torch.argmax(lg).item())
+    tr = tinylm.generate(small, prompt, FixedScheduler(4), eos_id=eos, max_new=10)
+    assert tr.termination == "eos" and tr.output_tokens == [eos]
+
+
+def test_save_load_round_trip(tmp_path, small):
+    path = tmp_path / "model.pmpd"
+    small.save(path)
+    loaded = tinylm.ModelVariants.load(path)
+    assert loaded.config == small.config
+    for name, qt in small.tensors.items():
+        assert torch.equal(qt.store.planes, loaded.tensors[name].store.planes)
+    prompt = list(b"The river finds its way")
+    a = tinylm.generate(small, prompt, FixedScheduler(16), max_new=8)
+    b = tinylm.generate(loaded, prompt, FixedScheduler(16), max_new=8)
+    assert a.output_tokens == b.output_tokens

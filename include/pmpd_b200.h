@@ -52,7 +52,8 @@ extern "C" {
  * plane (reading precision p touches exactly planes 0..p-1, the reference's
  * memory-prefix property, quant.py:5-8), bits permuted inside each tile into
  * the tensor-core fragment order of the decode GEMV, plus a per-tile f32
- * scale block.  They require group_size % 64 == 0 and p_max <= 4. */
+ * scale block (and, for KN, a per-n-tile 1/max(step) used to scale the GEMV's
+ * integer activation operand).  They require group_size % 64 == 0 and p_max <= 4. */
 #define PMPD_LAYOUT_REF 0
 #define PMPD_LAYOUT_KN 1
 #define PMPD_LAYOUT_NK 2
@@ -71,7 +72,8 @@ typedef struct pmpd_qtensor {
   int32_t groups;            /* groups per reference row: ceil(cols/group_size) */
   int64_t plane_bytes;       /* bytes of ONE plane region */
   int64_t scale_bytes;       /* bytes of the scale region (after the planes) */
-  int64_t total_bytes;       /* p_max * plane_bytes + scale_bytes */
+  int64_t aux_bytes;         /* KN: per n-tile 1/max(step) (after the scales); else 0 */
+  int64_t total_bytes;       /* p_max * plane_bytes + scale_bytes + aux_bytes */
   void* data;                /* device base pointer, caller-owned */
 } pmpd_qtensor;
 
@@ -151,6 +153,33 @@ int pmpd_gemv(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, int32_t m, 
  * *step_dev.  Entirely on device: no host sync inside a captured decode step. */
 int pmpd_sched_step(const int32_t* sched_dev, int32_t n_prec, int32_t* step_dev, int32_t* p_out_dev, int32_t advance,
                     void* stream);
+
+/* ------------------------------------------------------------- decode engine
+ * All quantized linear layers of one batch-1 decode token in ONE cooperative
+ * persistent kernel (replaces the per-layer h @ weights(name, p) calls of a
+ * reference decode step, tinylm.py:341-368).  A program is a device array of
+ * opaque op records (pmpd_engine_op_bytes() each) built with
+ * pmpd_engine_make_op; op i reads the f16 vector in_alpha * (output of op src)
+ * [src_col ...] (act 0) or silu(g)*u (act 1), or x_in for src = -1, and
+ * writes split-K partials to part_dev ([n_tiles][max_slots][64] f32); the last
+ * op's output is reduced into y_out (f32) scaled by y_alpha.  bar_dev: two
+ * zero-initialised uint32 (self-resetting).  Weights are streamed at the
+ * precision *p_dev (planes 0..p-1 only). */
+int pmpd_engine_op_bytes(void);
+int pmpd_engine_grid(void);
+int pmpd_engine_max_slots(const pmpd_qtensor* t);
+/* Contributing CTAs per n-group of t's output under the engine grid (host array, n_tiles bytes). */
+int pmpd_engine_nslots(const pmpd_qtensor* t, uint8_t* out_host);
+int pmpd_engine_make_op(const pmpd_qtensor* t, int32_t src, int32_t src_col, int32_t act, int32_t act_off,
+                        float in_alpha, float* part_dev, int32_t max_slots, const uint8_t* nslots_dev,
+                        void* op_host);
+int pmpd_engine_run(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const void* x_in_dev, float* y_out_dev,
+                    float y_alpha, uint32_t* bar_dev, int32_t* status_dev, void* stream);
+/* Same, recording a per-CTA per-op timeline (globaltimer ns) into trace_dev [grid][n_ops][4]:
+ * {input ready, input staged, tiles done, op published}. */
+int pmpd_engine_run_traced(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const void* x_in_dev,
+                           float* y_out_dev, float y_alpha, uint32_t* bar_dev, int32_t* status_dev, int64_t* trace_dev,
+                           void* stream);
 
 /* ------------------------------------------------------------- decoder glue
  * The non-linear parts of one forward step (tinylm.py:293-368); residual

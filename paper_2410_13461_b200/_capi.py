@@ -13,7 +13,7 @@ import threading
 from .errors import ConfigError, ContractViolation, FormatError, InputError, PmpdError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libpmpd_b200.so")
+LIB_PATH = os.environ.get("PMPD_LIB") or os.path.join(_HERE, "lib", "libpmpd_b200.so")
 
 OK, ERR_CONFIG, ERR_INPUT, ERR_CONTRACT, ERR_FORMAT, ERR_CUDA = 0, 1, 2, 3, 4, 5
 LAYOUT_REF, LAYOUT_KN, LAYOUT_NK = 0, 1, 2
@@ -35,7 +35,7 @@ class QTensorDesc(ctypes.Structure):
                 ("layout", ctypes.c_int32), ("n", ctypes.c_int32), ("k", ctypes.c_int32),
                 ("n_tiles", ctypes.c_int32), ("k_tiles", ctypes.c_int32), ("groups", ctypes.c_int32),
                 ("plane_bytes", ctypes.c_int64), ("scale_bytes", ctypes.c_int64),
-                ("total_bytes", ctypes.c_int64), ("data", ctypes.c_void_p)]
+                ("aux_bytes", ctypes.c_int64), ("total_bytes", ctypes.c_int64), ("data", ctypes.c_void_p)]
 
 
 _P = ctypes.c_void_p
@@ -67,6 +67,13 @@ SIGNATURES = {
     "pmpd_add_i32": [_P, _I, _P],
     "pmpd_push_token": [_P, _P, _P, _P, _I, _P],
     "pmpd_store_row": [_P, _P, _P, _I, _I, _P],
+    "pmpd_engine_op_bytes": [],
+    "pmpd_engine_grid": [],
+    "pmpd_engine_max_slots": [_D],
+    "pmpd_engine_nslots": [_D, _P],
+    "pmpd_engine_make_op": [_D, _I, _I, _I, _I, _F, _P, _I, _P, _P],
+    "pmpd_engine_run": [_P, _I, _P, _P, _P, _F, _P, _P, _P],
+    "pmpd_engine_run_traced": [_P, _I, _P, _P, _P, _F, _P, _P, _P, _P],
     "pmpd_learned_predict": [_P, _P, _I, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P],
 }
 _RESTYPES = {"pmpd_last_error": ctypes.c_char_p}

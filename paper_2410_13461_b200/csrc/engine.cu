@@ -1,0 +1,659 @@
+// Persistent decode engine: every quantized linear layer of one decode token
+// in ONE cooperative kernel.
+//
+// Replaces the per-layer `h @ model.weights(name, p)` calls of one reference
+// decode step (pkg/src/pmpd/tinylm.py:341-368, weights() 201-231) for the
+// batch-1 decode path.  Why one kernel: at batch 1 every GEMV is a few
+// microseconds of HBM traffic, so per-launch setup, pipeline ramp-up and the
+// cross-CTA reduction dominate a per-op kernel.  Here
+//   * a producer warp per SM streams the CTA's weight tiles of op 0, 1, 2, ...
+//     through a shared-memory ring with 1-D TMA bulk copies, never waiting
+//     for activations (weights do not depend on them) — only planes 0..p-1;
+//   * consumer warps decode bit planes into u8 tensor-core fragments and run
+//     mma.sync m16n8k32 (u8 x {s8,u8}) against an int16 two-digit activation
+//     operand, int32 accumulation (see gemv.cu for the arithmetic);
+//   * an epilogue warp reduces the consumer warps' per-n-group partials and
+//     writes one partial per (n-group, CTA) to global memory, then publishes
+//     the op's completion on a grid-wide counter;
+//   * the next op's consumers wait on that counter (acquire), sum the few
+//     partial slots of the columns they need (deferred split-K reduction,
+//     deterministic order) into an f16 activation vector in shared memory.
+// Co-residency of all CTAs is guaranteed by a cooperative launch.
+#include <cuda_fp16.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "decode_core.cuh"
+#include "layout.cuh"
+#include "pmpd_common.cuh"
+#include "pmpd_internal.h"
+
+namespace pmpd {
+namespace {
+
+#ifndef PMPD_ENGINE_NCW
+#define PMPD_ENGINE_NCW 8
+#endif
+#ifndef PMPD_ENGINE_TPW
+#define PMPD_ENGINE_TPW 2
+#endif
+constexpr int E_NCW = PMPD_ENGINE_NCW;      // consumer warps
+constexpr int E_TPW = PMPD_ENGINE_TPW;      // tiles per consumer warp per stage
+constexpr int E_STILES = E_NCW * E_TPW;     // tiles per stage
+constexpr int E_PROD = E_NCW;               // producer warp
+constexpr int E_EPI = E_NCW + 1;            // epilogue warp
+constexpr int E_THREADS = (E_NCW + 2) * 32;
+constexpr int E_MAXSTAGE = 12;
+constexpr int E_XMAX = 12288;               // max K of a staged activation vector
+constexpr int kMaxSlotsFast = 4;            // partial slots summed with independent loads
+
+struct EngineOp {
+  const uint8_t* planes;
+  const uint8_t* scales;
+  const float* aux;
+  long long plane_bytes;
+  int n_tiles, k_tiles, n_real, k_real;
+  int src;        // -1: external input; else index of the op whose output feeds this one
+  int src_col;    // first column of src's output used as input element 0
+  int act;        // 0: identity; 1: silu(g) * u with u at column src_col + act_off
+  int act_off;
+  float in_alpha; // scale applied to the reduced source before the activation
+  int max_slots;  // partial slots per n-group of THIS op's output
+  float* part;    // this op's output partials [n_tiles][max_slots][64]
+  const unsigned char* nslots;  // contributing CTAs per n-group of THIS op's output
+};
+
+struct EngineArgs {
+  const EngineOp* ops;
+  int n_ops;
+  const int32_t* p_dev;
+  const __half* x_in;  // input of op 0 (f16)
+  float* y_out;        // output of the last op (f32), y_alpha * reduced partials
+  float y_alpha;
+  unsigned* bar;       // [0]: op-completion tickets, [1]: CTAs done (self-resetting)
+  int* status;
+  long long* trace;    // optional timeline [G][n_ops][4] (globaltimer ns), null = off
+};
+
+PMPD_DEV long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// shared-memory plan (byte offsets)
+constexpr int kSmBar = 0;                            // mbarriers
+constexpr int kSmMisc = 256;                         // mx, flags
+constexpr int kSmNs = 512;                           // per-source-n-group slot counts: [2][512] B
+constexpr int kSmX = 1536;                           // f16 activations
+constexpr int kSmXq = kSmX + E_XMAX * 2;             // per-warp int8 activation fragments
+constexpr int kSmRed = kSmXq + E_NCW * E_TPW * 128;  // [2][E_NCW][64] f32
+constexpr int kSmRedb = kSmRed + 2 * E_NCW * 64 * 4; // [2][E_NCW] f32
+constexpr int kSmRing = (kSmRedb + 2 * E_NCW * 4 + 127) / 128 * 128;
+
+struct Bars {
+  uint64_t full[E_MAXSTAGE];
+  uint64_t empty[E_MAXSTAGE];
+  uint64_t red_full[2];
+  uint64_t red_empty[2];
+};
+
+PMPD_DEV int cta_of_tile(int t, int G, int NT) { return (int)(((int64_t)(t + 1) * G + NT - 1) / NT) - 1; }
+
+PMPD_DEV unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+struct Range {
+  int T0, T1, KT, NT;
+};
+PMPD_DEV Range range_of(const EngineOp& op, int c, int G) {
+  Range r;
+  r.NT = op.n_tiles * op.k_tiles;
+  r.KT = op.k_tiles;
+  r.T0 = (int)((int64_t)c * r.NT / G);
+  r.T1 = (int)((int64_t)(c + 1) * r.NT / G);
+  return r;
+}
+
+// ------------------------------------------------------------------ consumer tile
+template <int P>
+PMPD_DEV void engine_tile(const uint8_t* st, int stiles_cnt, int wslot, int kt, int lane, const __half* xs,
+                          uint8_t* xq, float qs, int (&dhi)[4][4], int (&dlo)[4][4], float& bias) {
+  const int gq = lane >> 2, tig = lane & 3;
+  uint32_t pw[E_TPW][4][4];
+  float2 dl[E_TPW], mn[E_TPW];
+  bool live[E_TPW];
+#pragma unroll
+  for (int q = 0; q < E_TPW; ++q) {
+    const int sl = wslot + q * E_NCW;
+    live[q] = sl < stiles_cnt;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (j < P && live[q]) {
+        const uint4 v = *reinterpret_cast<const uint4*>(st + j * E_STILES * kTilePlaneBytes + sl * kTilePlaneBytes +
+                                                        lane * 16);
+        pw[q][j][0] = v.x;
+        pw[q][j][1] = v.y;
+        pw[q][j][2] = v.z;
+        pw[q][j][3] = v.w;
+      } else {
+        pw[q][j][0] = pw[q][j][1] = pw[q][j][2] = pw[q][j][3] = 0u;
+      }
+    }
+    if (live[q]) {
+      const float* sc = reinterpret_cast<const float*>(st + P * E_STILES * kTilePlaneBytes + sl * kTileScaleBytes);
+      dl[q] = *reinterpret_cast<const float2*>(sc + 2 * lane);
+      mn[q] = *reinterpret_cast<const float2*>(sc + 64 + 2 * lane);
+    } else {
+      dl[q] = mn[q] = make_float2(0.f, 0.f);
+    }
+  }
+  const int wi = lane >> 1;
+  const int pos = (((wi & 3) << 2) | (wi >> 2)) * 4 + 2 * (lane & 1);
+#pragma unroll
+  for (int q = 0; q < E_TPW; ++q) {
+    if (!live[q]) continue;
+    const int kk = (kt + q * E_NCW) * kTile + 2 * lane;
+    const float2 xf = __half22float2(*reinterpret_cast<const __half2*>(xs + kk));
+    bias = fmaf(xf.x, mn[q].x, fmaf(xf.y, mn[q].y, bias));
+    const float f0 = fmaf(xf.x * dl[q].x, qs, 12582912.f);
+    const float f1 = fmaf(xf.y * dl[q].y, qs, 12582912.f);
+    const uint32_t u0 = __float_as_uint(f0), u1 = __float_as_uint(f1);
+    uint8_t* row = xq + q * 128;
+    *reinterpret_cast<uint16_t*>(row + pos) = (uint16_t)__byte_perm(u0, u1, 0x0040);
+    *reinterpret_cast<uint16_t*>(row + 64 + pos) = (uint16_t)__byte_perm(u0, u1, 0x0051);
+  }
+  __syncwarp();
+  uint32_t bl[E_TPW][4], bh[E_TPW][4];
+#pragma unroll
+  for (int q = 0; q < E_TPW; ++q) {
+    uint4 lo4 = make_uint4(0u, 0u, 0u, 0u), hi4 = lo4;
+    if (live[q] && gq == 0) {
+      lo4 = *reinterpret_cast<const uint4*>(xq + q * 128 + tig * 16);
+      hi4 = *reinterpret_cast<const uint4*>(xq + q * 128 + 64 + tig * 16);
+    }
+    bl[q][0] = lo4.x; bl[q][1] = lo4.y; bl[q][2] = lo4.z; bl[q][3] = lo4.w;
+    bh[q][0] = hi4.x; bh[q][1] = hi4.y; bh[q][2] = hi4.z; bh[q][3] = hi4.w;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < E_TPW; ++q) {
+    if (!live[q]) continue;
+#pragma unroll
+    for (int cch = 0; cch < 2; ++cch) {
+      const uint32_t pe[4] = {pw[q][0][2 * cch], pw[q][1][2 * cch], pw[q][2][2 * cch], pw[q][3][2 * cch]};
+      const uint32_t po[4] = {pw[q][0][2 * cch + 1], pw[q][1][2 * cch + 1], pw[q][2][2 * cch + 1],
+                              pw[q][3][2 * cch + 1]};
+#define PMPD_E_MTILE(T)                                                             \
+  {                                                                                 \
+    uint32_t a0, a1, a2, a3;                                                        \
+    nibble_to_u8<4, P, T>(merge_planes<4, P, T>(pe), a0, a1);                       \
+    nibble_to_u8<4, P, T>(merge_planes<4, P, T>(po), a2, a3);                       \
+    mma_u8s8_16832(dhi[T], a0, a1, a2, a3, bh[q][2 * cch], bh[q][2 * cch + 1]);     \
+    mma_u8u8_16832(dlo[T], a0, a1, a2, a3, bl[q][2 * cch], bl[q][2 * cch + 1]);     \
+  }
+      PMPD_E_MTILE(0)
+      PMPD_E_MTILE(1)
+      PMPD_E_MTILE(2)
+      PMPD_E_MTILE(3)
+#undef PMPD_E_MTILE
+    }
+  }
+}
+
+// ------------------------------------------------------------------ kernel
+template <int P>
+PMPD_DEV void consumer_loop(const EngineArgs& a, uint8_t* smem, Bars& bars, int G, int c, int stage_bytes,
+                            int nstage) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tig = lane & 3;
+  __half* xs = reinterpret_cast<__half*>(smem + kSmX);
+  uint8_t* xq = smem + kSmXq + warp * E_TPW * 128;
+  float* misc = reinterpret_cast<float*>(smem + kSmMisc);
+  float* red = reinterpret_cast<float*>(smem + kSmRed);
+  float* redb = reinterpret_cast<float*>(smem + kSmRedb);
+  int slot = 0;     // ring slot (continues across ops)
+  uint32_t phase = 0;
+  int seg = 0;      // n-group segment counter (red double buffer)
+  uint8_t* ns_s = smem + kSmNs;
+  for (int oi = 0; oi < a.n_ops; ++oi) {
+    const EngineOp& op = a.ops[oi];
+    const Range r = range_of(op, c, G);
+    // ---------------------------------------------------------- stage the input vector
+    // k-tiles this CTA touches
+    int lo0 = 0, hi0 = r.KT, lo1 = 0, hi1 = 0;
+    if (r.T1 - r.T0 < r.KT && r.T1 > r.T0) {
+      const int a0 = r.T0 % r.KT, b0 = (r.T1 - 1) % r.KT;
+      if (a0 <= b0) {
+        lo0 = a0;
+        hi0 = b0 + 1;
+      } else {
+        lo0 = a0;
+        hi0 = r.KT;
+        lo1 = 0;
+        hi1 = b0 + 1;
+      }
+    } else if (r.T1 <= r.T0) {
+      hi0 = 0;
+    }
+    // slot counts of the source n-groups this CTA reads (static table: safe before the wait)
+    if (op.src >= 0) {
+      const EngineOp& sop = a.ops[op.src];
+      for (int seg2 = 0; seg2 < 2; ++seg2) {
+        const int klo = (seg2 ? lo1 : lo0) * kTile, khi = (seg2 ? hi1 : hi0) * kTile;
+        for (int g = klo / 64 + threadIdx.x; g < (khi + 63) / 64; g += E_NCW * 32) {
+          const int n0 = op.src_col + g * 64;  // src_col % 64 may be != 0: two source groups per k-tile
+          ns_s[2 * g] = sop.nslots[n0 >> 6];
+          const int n1 = min(n0 + 63, sop.n_tiles * 64 - 1);
+          ns_s[2 * g + 1] = sop.nslots[n1 >> 6];
+          if (op.act == 1) {
+            ns_s[512 + 2 * g] = sop.nslots[(n0 + op.act_off) >> 6];
+            ns_s[512 + 2 * g + 1] = sop.nslots[min(n0 + op.act_off + 63, sop.n_tiles * 64 - 1) >> 6];
+          }
+        }
+      }
+    }
+    if (oi > 0) {
+      // every op starts after ALL CTAs published ALL earlier ops (the ticket count is only a
+      // safe completion test for a strict op-by-op order)
+      if (threadIdx.x == 0)
+        while (ld_acquire(a.bar) < (unsigned)(oi * G)) __nanosleep(32);
+      named_bar_sync(1, E_NCW * 32);
+    }
+    if (a.trace && threadIdx.x == 0) a.trace[((int64_t)c * a.n_ops + oi) * 4 + 0] = gtimer();
+    float mx = 0.f;
+    const EngineOp* src = op.src >= 0 ? &a.ops[op.src] : nullptr;
+    // Each thread stages 4 consecutive elements: all partial-slot loads of a group are
+    // issued before the sums (one L2 round trip), slot counts come from a host table.
+    for (int seg2 = 0; seg2 < 2; ++seg2) {
+      const int klo = (seg2 ? lo1 : lo0) * kTile, khi = (seg2 ? hi1 : hi0) * kTile;
+      for (int k = klo + 4 * threadIdx.x; k < khi; k += 4 * E_NCW * 32) {
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        if (!src) {
+          if (k + 4 <= op.k_real) {
+            const uint2 raw = __ldg(reinterpret_cast<const uint2*>(a.x_in + k));
+            const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
+            const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
+            v[0] = f0.x; v[1] = f0.y; v[2] = f1.x; v[3] = f1.y;
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[i] = (k + i < op.k_real) ? __half2float(a.x_in[k + i]) : 0.f;
+          }
+        } else {
+          auto reduced4 = [&](int n, int ksel, int which, float (&o)[4]) {  // 4 elements of one n-group
+            const int ng = n >> 6;
+            const int ns = ns_s[which * 512 + 2 * (ksel >> 6) + (((n & 63) < ((op.src_col + which * op.act_off) & 63)) ? 1 : 0)];
+            const float4* pp = reinterpret_cast<const float4*>(src->part + ((int64_t)ng * src->max_slots) * 64 +
+                                                               (n & 63));
+            float4 acc[kMaxSlotsFast];
+#pragma unroll
+            for (int q = 0; q < kMaxSlotsFast; ++q)
+              acc[q] = q < ns ? __ldcg(pp + q * 16) : make_float4(0.f, 0.f, 0.f, 0.f);
+            float4 s4 = acc[0];
+#pragma unroll
+            for (int q = 1; q < kMaxSlotsFast; ++q) {
+              s4.x += acc[q].x;
+              s4.y += acc[q].y;
+              s4.z += acc[q].z;
+              s4.w += acc[q].w;
+            }
+            for (int q = kMaxSlotsFast; q < ns; ++q) {  // rare: more contributors than the fast path holds
+              const float4 e = __ldcg(pp + q * 16);
+              s4.x += e.x;
+              s4.y += e.y;
+              s4.z += e.z;
+              s4.w += e.w;
+            }
+            o[0] = s4.x * op.in_alpha;
+            o[1] = s4.y * op.in_alpha;
+            o[2] = s4.z * op.in_alpha;
+            o[3] = s4.w * op.in_alpha;
+          };
+          float g[4];
+          reduced4(op.src_col + k, k, 0, g);
+          if (op.act == 1) {
+            float u[4];
+            reduced4(op.src_col + op.act_off + k, k, 1, u);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[i] = g[i] / (1.f + __expf(-g[i])) * u[i];
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[i] = g[i];
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            if (k + i >= op.k_real) v[i] = 0.f;
+        }
+        __half2 h01 = __floats2half2_rn(v[0], v[1]), h23 = __floats2half2_rn(v[2], v[3]);
+        *reinterpret_cast<__half2*>(xs + k) = h01;
+        *reinterpret_cast<__half2*>(xs + k + 2) = h23;
+        const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(f01.x), fabsf(f01.y)), fmaxf(fabsf(f23.x), fabsf(f23.y))));
+      }
+    }
+    mx = warp_max(mx);
+    if (lane == 0) misc[8 + warp] = mx;
+    named_bar_sync(1, E_NCW * 32);
+    mx = 0.f;
+#pragma unroll
+    for (int w = 0; w < E_NCW; ++w) mx = fmaxf(mx, misc[8 + w]);
+    if (a.trace && threadIdx.x == 0) a.trace[((int64_t)c * a.n_ops + oi) * 4 + 1] = gtimer();
+    // ---------------------------------------------------------- tiles of this op
+    int t = r.T0, ng = r.T0 / r.KT, kt = r.T0 % r.KT;
+    int dhi[4][4], dlo[4][4];
+    float bias = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) dhi[i][e] = dlo[i][e] = 0;
+    float qs = 0.f;
+    if (t < r.T1) {
+      const float idm = __ldg(op.aux + ng);
+      qs = (mx > 0.f && idm > 0.f) ? 32767.f * idm / mx : 0.f;
+    }
+    while (t < r.T1) {
+      const int end = min(min(t + E_STILES, r.T1), t - kt + r.KT);
+      mbar_wait(&bars.full[slot], phase);
+      if (warp < end - t) {
+        engine_tile<P>(smem + kSmRing + slot * stage_bytes, end - t, warp, kt + warp, lane, xs, xq, qs, dhi, dlo,
+                       bias);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars.empty[slot]);
+      if (++slot == nstage) {
+        slot = 0;
+        phase ^= 1u;
+      }
+      kt += end - t;
+      t = end;
+      if (kt == r.KT || t == r.T1) {
+        // hand the n-group partial to the epilogue warp (double-buffered)
+        const int buf = seg & 1;
+        if (seg >= 2) mbar_wait(&bars.red_empty[buf], ((seg >> 1) & 1) ^ 1);
+        float* rw = red + (buf * E_NCW + warp) * 64;
+        const float ds = qs > 0.f ? 1.f / qs : 0.f;
+        if (tig == 0) {
+#pragma unroll
+          for (int tt = 0; tt < 4; ++tt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              rw[16 * tt + gq + 8 * h] = fmaf(256.f, (float)dhi[tt][2 * h], (float)dlo[tt][2 * h]) *
+                                         (ds * (1.f / (float)(1 << tt)));
+        }
+        const float bs = warp_sum(bias);
+        if (lane == 0) redb[buf * E_NCW + warp] = bs;
+        __syncwarp();  // order every lane's partial stores before lane 0's release-arrive
+        if (lane == 0) mbar_arrive(&bars.red_full[buf]);
+        ++seg;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) dhi[i][e] = dlo[i][e] = 0;
+        bias = 0.f;
+        if (kt == r.KT) {
+          kt = 0;
+          ++ng;
+          if (t < r.T1) {
+            const float idm = __ldg(op.aux + ng);
+            qs = (mx > 0.f && idm > 0.f) ? 32767.f * idm / mx : 0.f;
+          }
+        }
+      }
+    }
+    if (a.trace && threadIdx.x == 0) a.trace[((int64_t)c * a.n_ops + oi) * 4 + 2] = gtimer();
+  }
+}
+
+__global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  Bars& bars = *reinterpret_cast<Bars*>(smem + kSmBar);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x, c = blockIdx.x;
+  int p = *a.p_dev;
+  if (p < 1 || p > 4) {
+    if (threadIdx.x == 0 && c == 0) atomicExch(a.status, PMPD_ERR_CONTRACT);
+    p = p < 1 ? 1 : 4;
+  }
+  const int stage_bytes = E_STILES * (p + 1) * kTilePlaneBytes;
+  uint32_t dyn_bytes;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn_bytes));
+  int nstage = (int)((dyn_bytes - kSmRing) / stage_bytes);
+  nstage = nstage > E_MAXSTAGE ? E_MAXSTAGE : nstage;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nstage; ++i) {
+      mbar_init(&bars.full[i], 1);
+      mbar_init(&bars.empty[i], E_NCW);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars.red_full[i], E_NCW);
+      mbar_init(&bars.red_empty[i], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == E_PROD) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int slot = 0, used = 0;
+      uint32_t phase = 0;
+      for (int oi = 0; oi < a.n_ops; ++oi) {
+        const EngineOp& op = a.ops[oi];
+        const Range r = range_of(op, c, G);
+        int t = r.T0, kt = r.T0 % r.KT;
+        while (t < r.T1) {
+          const int end = min(min(t + E_STILES, r.T1), t - kt + r.KT);
+          const int cnt = end - t;
+          if (used) mbar_wait(&bars.empty[slot], phase ^ 1u);
+          uint8_t* st = smem + kSmRing + slot * stage_bytes;
+          mbar_arrive_expect_tx(&bars.full[slot], (uint32_t)(cnt * kTilePlaneBytes * (p + 1)));
+          for (int j = 0; j < p; ++j)
+            bulk_g2s_stream(st + j * E_STILES * kTilePlaneBytes,
+                            op.planes + j * op.plane_bytes + (int64_t)t * kTilePlaneBytes, cnt * kTilePlaneBytes,
+                            &bars.full[slot], pol);
+          bulk_g2s_stream(st + p * E_STILES * kTilePlaneBytes, op.scales + (int64_t)t * kTileScaleBytes,
+                          cnt * kTileScaleBytes, &bars.full[slot], pol);
+          kt += cnt;
+          if (kt == r.KT) kt = 0;
+          t = end;
+          if (++slot == nstage) {
+            slot = 0;
+            phase ^= 1u;
+            used = 1;
+          }
+        }
+      }
+    }
+  } else if (warp == E_EPI) {
+    // ------------------------------------------------------------ epilogue
+    float* red = reinterpret_cast<float*>(smem + kSmRed);
+    float* redb = reinterpret_cast<float*>(smem + kSmRedb);
+    int seg = 0;
+    for (int oi = 0; oi < a.n_ops; ++oi) {
+      const EngineOp& op = a.ops[oi];
+      const Range r = range_of(op, c, G);
+      int t = r.T0, ng = r.T0 / r.KT, kt = r.T0 % r.KT;
+      while (t < r.T1) {
+        const int seg_end = min(r.T1, t - kt + r.KT);
+        const int buf = seg & 1;
+        mbar_wait(&bars.red_full[buf], (seg >> 1) & 1);
+        float bsum = 0.f;
+#pragma unroll
+        for (int w = 0; w < E_NCW; ++w) bsum += redb[buf * E_NCW + w];
+        const int cf = cta_of_tile(ng * r.KT, G, r.NT);
+        float* dst = op.part + ((int64_t)ng * op.max_slots + (c - cf)) * 64;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int nl = lane + 32 * h;
+          float v = bsum;
+#pragma unroll
+          for (int w = 0; w < E_NCW; ++w) v += red[(buf * E_NCW + w) * 64 + nl];
+          dst[nl] = v;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars.red_empty[buf]);
+        ++seg;
+        kt += seg_end - t;
+        t = seg_end;
+        if (kt == r.KT) {
+          kt = 0;
+          ++ng;
+        }
+      }
+      __syncwarp();  // lane 0's release covers the warp's partial stores (cumulativity)
+      if (lane == 0) {
+        // A CTA with no tiles in op oi must not publish it before every CTA has
+        // published ops < oi: the ticket count is a completion test only if tickets
+        // of op oi never precede the completion of op oi-1.
+        if (oi > 0)
+          while (ld_acquire(a.bar) < (unsigned)(oi * G)) __nanosleep(32);
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar) : "memory");
+        if (a.trace) a.trace[((int64_t)c * a.n_ops + oi) * 4 + 3] = gtimer();
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ consumers
+    switch (p) {
+      case 4: consumer_loop<4>(a, smem, bars, G, c, stage_bytes, nstage); break;
+      case 3: consumer_loop<3>(a, smem, bars, G, c, stage_bytes, nstage); break;
+      case 2: consumer_loop<2>(a, smem, bars, G, c, stage_bytes, nstage); break;
+      default: consumer_loop<1>(a, smem, bars, G, c, stage_bytes, nstage); break;
+    }
+  }
+  // ---------------------------------------------------------------- final output
+  __syncthreads();
+  const EngineOp& last = a.ops[a.n_ops - 1];
+  if (threadIdx.x == 0)
+    while (ld_acquire(a.bar) < (unsigned)(a.n_ops * G)) __nanosleep(64);
+  __syncthreads();
+  const int NT = last.n_tiles * last.k_tiles, KT = last.k_tiles;
+  for (int ng = c; ng < last.n_tiles; ng += G) {
+    const int cf = cta_of_tile(ng * KT, G, NT), cl = cta_of_tile(min((ng + 1) * KT, NT) - 1, G, NT);
+    for (int nl = threadIdx.x; nl < 64; nl += blockDim.x) {
+      const int n = ng * 64 + nl;
+      if (n >= last.n_real) continue;
+      float s = 0.f;
+      const float* pp = last.part + (int64_t)ng * last.max_slots * 64 + nl;
+      for (int q = 0; q <= cl - cf; ++q) s += __ldcg(pp + q * 64);
+      a.y_out[n] = a.y_alpha * s;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(a.bar + 1, 1u) == (unsigned)(G - 1)) {
+      a.bar[0] = 0;
+      a.bar[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+}  // namespace
+}  // namespace pmpd
+
+using namespace pmpd;
+
+extern "C" {
+
+int pmpd_engine_op_bytes(void) { return (int)sizeof(EngineOp); }
+
+int pmpd_engine_grid(void) { return num_sms(); }
+
+// partial slots per n-group of an op's output for the engine's grid
+int pmpd_engine_max_slots(const pmpd_qtensor* t) {
+  const int nt = t->n_tiles * t->k_tiles, g = num_sms();
+  const int per = nt / g;
+  return per >= 1 ? t->k_tiles / per + 2 : g;
+}
+
+int pmpd_engine_nslots(const pmpd_qtensor* t, uint8_t* out_host) {
+  const int nt = t->n_tiles * t->k_tiles, g = num_sms(), kt = t->k_tiles;
+  auto cta = [&](int tile) { return (int)(((int64_t)(tile + 1) * g + nt - 1) / nt) - 1; };
+  for (int ng = 0; ng < t->n_tiles; ++ng) {
+    const int n = cta(std::min((ng + 1) * kt, nt) - 1) - cta(ng * kt) + 1;
+    if (n > 255) return fail(PMPD_ERR_CONFIG, "too many contributors per n-group");
+    out_host[ng] = (uint8_t)n;
+  }
+  return PMPD_OK;
+}
+
+int pmpd_engine_make_op(const pmpd_qtensor* t, int32_t src, int32_t src_col, int32_t act, int32_t act_off,
+                        float in_alpha, float* part_dev, int32_t max_slots, const uint8_t* nslots_dev,
+                        void* op_host) {
+  if (!t || !t->data || !op_host) return fail(PMPD_ERR_CONFIG, "null argument");
+  if (t->layout != PMPD_LAYOUT_KN || t->p_max != 4)
+    return fail(PMPD_ERR_CONFIG, "the decode engine needs KN tiles with p_max 4");
+  if (t->k_tiles * kTile > E_XMAX) return fail(PMPD_ERR_CONFIG, "engine input width above %d", E_XMAX);
+  EngineOp op{};
+  op.planes = static_cast<const uint8_t*>(t->data);
+  op.scales = op.planes + (int64_t)t->p_max * t->plane_bytes;
+  op.aux = reinterpret_cast<const float*>(op.scales + t->scale_bytes);
+  op.plane_bytes = t->plane_bytes;
+  op.n_tiles = t->n_tiles;
+  op.k_tiles = t->k_tiles;
+  op.n_real = t->n;
+  op.k_real = t->k;
+  op.src = src;
+  op.src_col = src_col;
+  op.act = act;
+  op.act_off = act_off;
+  op.in_alpha = in_alpha;
+  op.max_slots = max_slots;
+  op.part = part_dev;
+  op.nslots = nslots_dev;
+  if ((src_col & 3) || (act_off & 3)) return fail(PMPD_ERR_CONFIG, "engine input offsets must be multiples of 4");
+  *static_cast<EngineOp*>(op_host) = op;
+  return PMPD_OK;
+}
+
+int pmpd_engine_run_traced(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const void* x_in, float* y_out,
+                           float y_alpha, uint32_t* bar_dev, int32_t* status_dev, int64_t* trace_dev, void* stream);
+
+int pmpd_engine_run(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const void* x_in, float* y_out,
+                    float y_alpha, uint32_t* bar_dev, int32_t* status_dev, void* stream) {
+  return pmpd_engine_run_traced(ops_dev, n_ops, p_dev, x_in, y_out, y_alpha, bar_dev, status_dev, nullptr, stream);
+}
+
+int pmpd_engine_run_traced(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const void* x_in, float* y_out,
+                           float y_alpha, uint32_t* bar_dev, int32_t* status_dev, int64_t* trace_dev, void* stream) {
+  if (n_ops < 1) return fail(PMPD_ERR_CONFIG, "engine program is empty");
+  EngineArgs a;
+  a.ops = static_cast<const EngineOp*>(ops_dev);
+  a.n_ops = n_ops;
+  a.p_dev = p_dev;
+  a.x_in = static_cast<const __half*>(x_in);
+  a.y_out = y_out;
+  a.y_alpha = y_alpha;
+  a.bar = bar_dev;
+  a.status = status_dev;
+  a.trace = reinterpret_cast<long long*>(trace_dev);
+  static int smem = 0;
+  if (smem == 0) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    smem = optin;
+    if (const char* e = getenv("PMPD_ENGINE_SMEM")) smem = atoi(e) < optin ? atoi(e) : optin;
+    cudaFuncSetAttribute(engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(num_sms());
+  cfg.blockDim = dim3(E_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = as_stream(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, engine_kernel, a);
+  if (e != cudaSuccess) return fail(PMPD_ERR_CUDA, "engine launch: %s", cudaGetErrorString(e));
+  return PMPD_OK;
+}
+
+}  // extern "C"

@@ -27,6 +27,7 @@
 
 #include <cstdlib>
 
+#include "decode_core.cuh"
 #include "layout.cuh"
 #include "pmpd_common.cuh"
 #include "pmpd_internal.h"
@@ -34,11 +35,26 @@
 namespace pmpd {
 namespace {
 
-constexpr int NCW = 8;                  // consumer warps
+#ifndef PMPD_GEMV_NCW
+#define PMPD_GEMV_NCW 8
+#endif
+#ifndef PMPD_GEMV_NSTAGE
+#define PMPD_GEMV_NSTAGE 4
+#endif
+constexpr int NCW = PMPD_GEMV_NCW;      // consumer warps
 constexpr int NTHREADS = (NCW + 1) * 32;  // + producer warp
-constexpr int NSTAGE = 4;               // smem ring depth
-constexpr int STILES = NCW;             // tiles per stage (one per consumer warp)
+constexpr int NSTAGE = PMPD_GEMV_NSTAGE;  // smem ring depth
+#ifndef PMPD_GEMV_TPW
+#define PMPD_GEMV_TPW 2
+#endif
+constexpr int TPW = PMPD_GEMV_TPW;       // tiles per consumer warp per stage (ILP)
+constexpr int STILES = NCW * TPW;        // tiles per stage
 constexpr int MAXM = 8;
+// Workspace: a FIXED-size counter region (so GEMVs of different widths sharing one
+// workspace never see another shape's partials where they expect zeroed counters),
+// one status word, then the split-K partials.
+constexpr int kWsCounters = 16384;
+constexpr int64_t kWsHead = (int64_t)kWsCounters * 4 + 256;
 constexpr int kXsMaxK = 12288;          // activations staged in smem when K <= this (batch 1)
 
 struct GemvArgs {
@@ -53,6 +69,7 @@ struct GemvArgs {
   int y_dtype, ldy;
   float alpha;
   int accumulate;
+  const float* aux;  // KN: per n-tile 1 / max(step)
   int* counters;   // [n_tiles]
   int* status;     // [1]
   float* partial;  // [n_tiles][max_slots][64][m]
@@ -65,76 +82,23 @@ struct Smem {  // fits in the first 128 bytes of dynamic shared memory
   int flag;
 };
 
-// ---------------------------------------------------------------- decode core
-// Merge planes 0..P-1 of word (w, t) into a nibble word.  Plane j's bits for
-// m-tile t sit at rotl(0x11111111 << b_j, t); bit-selecting keeps each
-// plane's own positions (positions of unread planes hold garbage that the
-// fragment conversion masks off).  One LOP3 per extra plane.
-template <int PMAX, int P, int T>
-PMPD_DEV uint32_t merge_planes(const uint32_t (&pw)[4]) {
-  uint32_t acc = pw[0];
-#pragma unroll
-  for (int j = 1; j < P; ++j) {
-    // positions already owned by planes 0..j-1, rotated by T (a compile-time immediate)
-    const uint32_t have = (0x11111111u * (((1u << j) - 1) << (PMAX - j))) ;
-    const uint32_t sel = (have << T) | (T ? (have >> (32 - T)) : 0u);
-    acc = lop3_select(acc, pw[j], sel);
-  }
-  return acc;
-}
-
-// Decode position of the low slot pair for m-tile T: the nibble word is read
-// rotated by R1 = T - Q0 so that slots (0,4)/(1,5) sit at mantissa bits
-// Q0..Q0+3 / Q0+4..Q0+7 (both <= bit 9) and, after a further 8-bit rotate,
-// slots (2,6)/(3,7) likewise.
-template <int T>
-struct FragPos {
-  static constexpr int Q0 = T < 2 ? T : 2;
-  static constexpr int R1 = T - Q0;
-};
-
-// fp16 A fragment from one nibble word of m-tile T (see layout.cuh).  OR-ing
-// the exponent of 2^(10-q) onto a code at mantissa bits q..q+3 makes the half
-// exactly 2^(10-q) + k (k = bucket index, exact in fp16).
-template <int PMAX, int P, int T>
-PMPD_DEV void nibble_to_frag(uint32_t u, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3) {
-  constexpr int Q0 = FragPos<T>::Q0, R1 = FragPos<T>::R1;
-  // nibble bits that come from loaded planes, and the constant bucket-centre bit
-  constexpr uint32_t kLoaded = ((1u << PMAX) - 1) & ~((1u << (PMAX - P)) - 1);
-  constexpr uint32_t kConst = (P < PMAX) ? (1u << (PMAX - P - 1)) : 0u;
-  constexpr uint32_t m0 = (kLoaded * 0x00010001u) << Q0;
-  constexpr uint32_t m4 = (kLoaded * 0x00010001u) << (Q0 + 4);
-  constexpr uint32_t g0 = (((uint32_t)(25 - Q0) << 10) | (kConst << Q0)) * 0x00010001u;
-  constexpr uint32_t g4 = (((uint32_t)(21 - Q0) << 10) | (kConst << (Q0 + 4))) * 0x00010001u;
-  const uint32_t ua = R1 ? rotr32(u, R1) : u;
-  const uint32_t ub = rotr32(u, R1 + 8);
-  a0 = lop3_and_or(ua, m0, g0);
-  a1 = lop3_and_or(ua, m4, g4);
-  a2 = lop3_and_or(ub, m0, g0);
-  a3 = lop3_and_or(ub, m4, g4);
-}
-
-// fp16 value offset carried by each A row after the MMA: 2^(10-Q0) for rows
-// gq (a0/a2), 2^(6-Q0) for rows gq+8 (a1/a3).
-PMPD_DEV float row_offset(int t, int h) {
-  const int q0 = t < 2 ? t : 2;
-  return (float)(1024 >> (q0 + 4 * h));
-}
-
 // ---------------------------------------------------------------- smem plan
 // [Smem | ring: NSTAGE x (PMAX planes + scales) x STILES tiles | xs: staged
-//  activations (XS) | bt: per-warp B~ fragments | red/redb: cross-warp sums]
+//  activations (XS) | xq: per-warp int8 activation fragments (KN) |
+//  red/redb: cross-warp sums | qsc: per-n-group activation scales (KN)]
 template <int PMAX, int MB, bool XS>
 struct Plan {
   static constexpr int kStage = STILES * (PMAX + 1) * kTilePlaneBytes;
   static constexpr int kRing = 128;
   static constexpr int kXs = kRing + NSTAGE * kStage;
   static constexpr int kXsBytes = XS ? MB * kXsMaxK * 2 : 0;
-  static constexpr int kBt = kXs + kXsBytes;
-  static constexpr int kBtRows = MB == 1 ? 1 : MAXM;
-  static constexpr int kRed = kBt + NCW * kBtRows * 64 * 2;
+  static constexpr int kXq = kXs + kXsBytes;
+  static constexpr int kXqRows = MB == 1 ? 1 : MAXM;
+  static constexpr int kXqWarp = TPW * kXqRows * 2 * 64;  // lo + hi bytes per row and tile
+  static constexpr int kRed = kXq + NCW * kXqWarp;
   static constexpr int kRedb = kRed + NCW * 64 * MB * 4;
-  static constexpr int kBytes = kRedb + NCW * MB * 4;
+  static constexpr int kMx = kRedb + NCW * MB * 4;  // per-row max |x| (KN)
+  static constexpr int kBytes = kMx + MAXM * 4 + 32 * 4;
 };
 
 // Tile iteration without integer division: stages never straddle an n-group.
@@ -149,28 +113,46 @@ struct TileCursor {
 template <int LAYOUT, int PMAX, int MB, bool XS>
 struct Consumer {
   using PL = Plan<PMAX, MB, XS>;
+  static constexpr bool KN = LAYOUT == PMPD_LAYOUT_KN;
   const GemvArgs& a;
   Smem& sm;
   uint8_t* smem;
   const __half* xs;  // staged activations [MB][kXsMaxK] (XS) or global x
   int xld;           // leading dimension of xs
-  uint32_t* bt;      // this warp's B~ fragments, permuted for 2 x LDS.128 per lane
+  uint8_t* xq;       // KN: this warp's int8 activation fragments [rows][lo 64 | hi 64]
   float* red;
   float* redb;
+  const float* mx;   // KN: per-row max |x| (smem)
   int warp, lane, gq, tig, T0, T1, KT, NT, G, c, M;
+  // NK: f32 accumulators of the current n-group; KN: int32 hi/lo digit accumulators
   float acc[4][4];
-  float aux[4];    // KN: ones-MMA column sums of B~ (cols 2tig, 2tig+1)
+  int dhi[4][4], dlo[4][4];
   float bias[MB];  // KN: this lane's part of sum_k x*min
+  float qs[MB];    // KN: activation quantisation scale 32767 / (max|x_b| * max step_g)
 
   PMPD_DEV void reset() {
 #pragma unroll
     for (int t = 0; t < 4; ++t)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) acc[t][e] = 0.f;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) aux[e] = 0.f;
+      for (int e = 0; e < 4; ++e) {
+        acc[t][e] = 0.f;
+        dhi[t][e] = 0;
+        dlo[t][e] = 0;
+      }
 #pragma unroll
     for (int b = 0; b < MB; ++b) bias[b] = 0.f;
+  }
+
+  // set the KN activation scale for n-group ng
+  PMPD_DEV void enter_group(int ng) {
+    if constexpr (KN) {
+      const float idm = __ldg(a.aux + ng);
+#pragma unroll
+      for (int b = 0; b < MB; ++b) {
+        const float m = mx[b];
+        qs[b] = (m > 0.f && idm > 0.f) ? 32767.f * idm / m : 0.f;
+      }
+    }
   }
 
   // x[b][k..k+1] as float2 (zero outside [0, k_real))
@@ -194,10 +176,7 @@ struct Consumer {
   }
 
   template <int P>
-  PMPD_DEV void tile(const uint8_t* st, int wslot, int kt) {
-    constexpr uint32_t ONES = 0x3C003C00u;
-    const int k0 = kt * kTile;
-    uint32_t pw[4][4];
+  PMPD_DEV void load_planes(const uint8_t* st, int wslot, uint32_t (&pw)[4][4]) const {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       if (j < P) {
@@ -211,42 +190,104 @@ struct Consumer {
         pw[j][0] = pw[j][1] = pw[j][2] = pw[j][3] = 0u;
       }
     }
-    const float* sc =
-        reinterpret_cast<const float*>(st + PMAX * STILES * kTilePlaneBytes + wslot * kTileScaleBytes);
-    uint32_t bfr[4][2];
-    if constexpr (LAYOUT == PMPD_LAYOUT_KN) {
-      // B~[b][k] = fp16(x[b][k] * step[k]); bias[b] += x[b][k] * min[k].  Lane L owns the
-      // half2 word k = 2L, 2L+1 and stores it where reader tig = L&3 finds its 8 words
-      // contiguous: slot (L&3)*8 + (L>>3)*2 + ((L>>2)&1).
-      const float2 dl = *reinterpret_cast<const float2*>(sc + 2 * lane);
-      const float2 mn = *reinterpret_cast<const float2*>(sc + 64 + 2 * lane);
-      const int kk = k0 + 2 * lane;
-      const int slot = (lane & 3) * 8 + (lane >> 3) * 2 + ((lane >> 2) & 1);
+  }
+
+  // ------------------------------------------------------------- KN tiles (IMMA)
+  // Processes the TPW tiles {wslot + q*NCW} of one stage (all in the same n-group)
+  // phase by phase so their dependency chains interleave.
+  template <int P>
+  PMPD_DEV void tile_kn(const uint8_t* st, int wslot, int kt, int cnt) {
+    uint32_t pw[TPW][4][4];
+    float2 dl[TPW], mn[TPW];
+    bool live[TPW];
+#pragma unroll
+    for (int q = 0; q < TPW; ++q) {
+      const int sl = wslot + q * NCW;
+      live[q] = sl < cnt;
+      if (live[q]) {
+        load_planes<P>(st, sl, pw[q]);
+        const float* sc = reinterpret_cast<const float*>(st + PMAX * STILES * kTilePlaneBytes + sl * kTileScaleBytes);
+        dl[q] = *reinterpret_cast<const float2*>(sc + 2 * lane);
+        mn[q] = *reinterpret_cast<const float2*>(sc + 64 + 2 * lane);
+      }
+    }
+    // Activation operand: xq[b][k] = rint(x[b][k] * step[k] * qs[b]) as int16 (|.| <= 32767),
+    // split into a u8 low digit and an s8 high digit.  Lane L owns k = 2L, 2L+1 (u16 stores);
+    // storage is permuted so reader tig fetches {b0,b1} of both 32-k chunks with one LDS.128.
+    const int wi = lane >> 1;
+    const int pos = (((wi & 3) << 2) | (wi >> 2)) * 4 + 2 * (lane & 1);
+#pragma unroll
+    for (int q = 0; q < TPW; ++q) {
+      if (!live[q]) continue;
+      const int kk = (kt + q * NCW) * kTile + 2 * lane;
 #pragma unroll
       for (int b = 0; b < MB; ++b) {
         if (MB == 1 || b < M) {
           const float2 xf = xpair(b, kk);
-          const __half2 h = __floats2half2_rn(xf.x * dl.x, xf.y * dl.y);
-          bt[b * 32 + slot] = *reinterpret_cast<const uint32_t*>(&h);
-          bias[b] = fmaf(xf.x, mn.x, fmaf(xf.y, mn.y, bias[b]));
+          bias[b] = fmaf(xf.x, mn[q].x, fmaf(xf.y, mn[q].y, bias[b]));
+          const float f0 = fmaf(xf.x * dl[q].x, qs[b], 12582912.f);  // 1.5 * 2^23: round-to-nearest-even
+          const float f1 = fmaf(xf.y * dl[q].y, qs[b], 12582912.f);
+          const uint32_t u0 = __float_as_uint(f0), u1 = __float_as_uint(f1);
+          uint8_t* row = xq + (q * PL::kXqRows + b) * 128;
+          *reinterpret_cast<uint16_t*>(row + pos) = (uint16_t)__byte_perm(u0, u1, 0x0040);
+          *reinterpret_cast<uint16_t*>(row + 64 + pos) = (uint16_t)__byte_perm(u0, u1, 0x0051);
         }
       }
-      __syncwarp();
-      const int row = MB == 1 ? 0 : gq;
-      uint4 lo = *reinterpret_cast<const uint4*>(bt + row * 32 + tig * 8);
-      uint4 hi = *reinterpret_cast<const uint4*>(bt + row * 32 + tig * 8 + 4);
-      if (gq >= (MB == 1 ? 1 : M)) lo = hi = make_uint4(0u, 0u, 0u, 0u);
-      bfr[0][0] = lo.x; bfr[0][1] = lo.y; bfr[1][0] = lo.z; bfr[1][1] = lo.w;
-      bfr[2][0] = hi.x; bfr[2][1] = hi.y; bfr[3][0] = hi.z; bfr[3][1] = hi.w;
-      __syncwarp();
-    } else {
-      const bool live = gq < (MB == 1 ? 1 : M);
-#pragma unroll
-      for (int w = 0; w < 4; ++w)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) bfr[w][h] = live ? xword(gq, k0 + 16 * w + 2 * tig + 8 * h) : 0u;
     }
+    __syncwarp();
+    uint32_t bl[TPW][2][2], bh[TPW][2][2];
+#pragma unroll
+    for (int q = 0; q < TPW; ++q) {
+      uint4 lo4 = make_uint4(0u, 0u, 0u, 0u), hi4 = lo4;
+      if (live[q] && gq < (MB == 1 ? 1 : M)) {
+        const uint8_t* row = xq + (q * PL::kXqRows + (MB == 1 ? 0 : gq)) * 128;
+        lo4 = *reinterpret_cast<const uint4*>(row + tig * 16);
+        hi4 = *reinterpret_cast<const uint4*>(row + 64 + tig * 16);
+      }
+      bl[q][0][0] = lo4.x; bl[q][0][1] = lo4.y; bl[q][1][0] = lo4.z; bl[q][1][1] = lo4.w;
+      bh[q][0][0] = hi4.x; bh[q][0][1] = hi4.y; bh[q][1][0] = hi4.z; bh[q][1][1] = hi4.w;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < TPW; ++q) {
+      if (!live[q]) continue;
+#pragma unroll
+      for (int cch = 0; cch < 2; ++cch) {
+        const uint32_t pe[4] = {pw[q][0][2 * cch], pw[q][1][2 * cch], pw[q][2][2 * cch], pw[q][3][2 * cch]};
+        const uint32_t po[4] = {pw[q][0][2 * cch + 1], pw[q][1][2 * cch + 1], pw[q][2][2 * cch + 1],
+                                pw[q][3][2 * cch + 1]};
+#define PMPD_KN_MTILE(T)                                                     \
+  {                                                                          \
+    uint32_t a0, a1, a2, a3;                                                 \
+    nibble_to_u8<PMAX, P, T>(merge_planes<PMAX, P, T>(pe), a0, a1);          \
+    nibble_to_u8<PMAX, P, T>(merge_planes<PMAX, P, T>(po), a2, a3);          \
+    mma_u8s8_16832(dhi[T], a0, a1, a2, a3, bh[q][cch][0], bh[q][cch][1]);    \
+    mma_u8u8_16832(dlo[T], a0, a1, a2, a3, bl[q][cch][0], bl[q][cch][1]);    \
+  }
+        PMPD_KN_MTILE(0)
+        PMPD_KN_MTILE(1)
+        PMPD_KN_MTILE(2)
+        PMPD_KN_MTILE(3)
+#undef PMPD_KN_MTILE
+      }
+    }
+  }
 
+  // ------------------------------------------------------------- NK tile (HMMA)
+  template <int P>
+  PMPD_DEV void tile_nk(const uint8_t* st, int wslot, int kt) {
+    constexpr uint32_t ONES = 0x3C003C00u;
+    const int k0 = kt * kTile;
+    uint32_t pw[4][4];
+    load_planes<P>(st, wslot, pw);
+    const float* sc =
+        reinterpret_cast<const float*>(st + PMAX * STILES * kTilePlaneBytes + wslot * kTileScaleBytes);
+    uint32_t bfr[4][2];
+    const bool live = gq < (MB == 1 ? 1 : M);
+#pragma unroll
+    for (int w = 0; w < 4; ++w)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) bfr[w][h] = live ? xword(gq, k0 + 16 * w + 2 * tig + 8 * h) : 0u;
     float cl[4][4];
     float sx[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -255,46 +296,36 @@ struct Consumer {
       for (int e = 0; e < 4; ++e) cl[t][e] = 0.f;
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
-      if constexpr (LAYOUT == PMPD_LAYOUT_KN)
-        mma_f16_16816(aux, ONES, ONES, ONES, ONES, bfr[w][0], bfr[w][1]);
-      else
-        mma_f16_16816(sx, ONES, ONES, ONES, ONES, bfr[w][0], bfr[w][1]);
+      mma_f16_16816(sx, ONES, ONES, ONES, ONES, bfr[w][0], bfr[w][1]);
       const uint32_t pj[4] = {pw[0][w], pw[1][w], pw[2][w], pw[3][w]};
-      uint32_t a0, a1, a2, a3;
-      // m-tile t = 0..3 (compile-time t: masks and exponents are immediates)
-#define PMPD_MTILE(T)                                                            \
-  {                                                                              \
-    const uint32_t u = merge_planes<PMAX, P, T>(pj);                             \
-    nibble_to_frag<PMAX, P, T>(u, a0, a1, a2, a3);                               \
-    if constexpr (LAYOUT == PMPD_LAYOUT_KN)                                      \
-      mma_f16_16816(acc[T], a0, a1, a2, a3, bfr[w][0], bfr[w][1]);               \
-    else                                                                         \
-      mma_f16_16816(cl[T], a0, a1, a2, a3, bfr[w][0], bfr[w][1]);                \
+#define PMPD_NK_MTILE(T)                                                   \
+  {                                                                        \
+    uint32_t a0, a1, a2, a3;                                               \
+    nibble_to_frag<PMAX, P, T>(merge_planes<PMAX, P, T>(pj), a0, a1, a2, a3); \
+    mma_f16_16816(cl[T], a0, a1, a2, a3, bfr[w][0], bfr[w][1]);            \
   }
-      PMPD_MTILE(0)
-      PMPD_MTILE(1)
-      PMPD_MTILE(2)
-      PMPD_MTILE(3)
-#undef PMPD_MTILE
+      PMPD_NK_MTILE(0)
+      PMPD_NK_MTILE(1)
+      PMPD_NK_MTILE(2)
+      PMPD_NK_MTILE(3)
+#undef PMPD_NK_MTILE
     }
-    if constexpr (LAYOUT == PMPD_LAYOUT_NK) {
-      // rows of this lane: n_l = 16t + gq + 8h -> scale slot gq*8 + 2t + h
-      const float4 d0 = *reinterpret_cast<const float4*>(sc + gq * 8);
-      const float4 d1 = *reinterpret_cast<const float4*>(sc + gq * 8 + 4);
-      const float4 m0 = *reinterpret_cast<const float4*>(sc + 64 + gq * 8);
-      const float4 m1 = *reinterpret_cast<const float4*>(sc + 64 + gq * 8 + 4);
-      const float dd[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
-      const float mm[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+    // rows of this lane: n_l = 16t + gq + 8h -> scale slot gq*8 + 2t + h
+    const float4 d0 = *reinterpret_cast<const float4*>(sc + gq * 8);
+    const float4 d1 = *reinterpret_cast<const float4*>(sc + gq * 8 + 4);
+    const float4 m0 = *reinterpret_cast<const float4*>(sc + 64 + gq * 8);
+    const float4 m1 = *reinterpret_cast<const float4*>(sc + 64 + gq * 8 + 4);
+    const float dd[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+    const float mm[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
+    for (int t = 0; t < 4; ++t)
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
+      for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int cc = 0; cc < 2; ++cc) {
-            const float d = fmaf(-row_offset(t, h), sx[cc], cl[t][2 * h + cc]);
-            acc[t][2 * h + cc] = fmaf(dd[2 * t + h], d, fmaf(mm[2 * t + h], sx[cc], acc[t][2 * h + cc]));
-          }
-    }
+        for (int cc = 0; cc < 2; ++cc) {
+          const float d = fmaf(-row_offset(t, h), sx[cc], cl[t][2 * h + cc]);
+          acc[t][2 * h + cc] = fmaf(dd[2 * t + h], d, fmaf(mm[2 * t + h], sx[cc], acc[t][2 * h + cc]));
+        }
   }
 
   PMPD_DEV void store(int ng, int nl, int b, float v) {
@@ -322,12 +353,19 @@ struct Consumer {
         for (int cc = 0; cc < 2; ++cc) {
           const int b = 2 * tig + cc;
           if (b < Me) {
-            float v = acc[t][2 * h + cc];
-            if constexpr (LAYOUT == PMPD_LAYOUT_KN) v = fmaf(-row_offset(t, h), aux[cc], v);
+            float v;
+            if constexpr (KN) {
+              // y = (256*hi + lo) * 2^-t / qs[b]
+              const float q = qs[MB == 1 ? 0 : b];
+              const float ds = q > 0.f ? __fdividef(1.f, q) * (1.f / (float)(1 << t)) : 0.f;
+              v = fmaf(256.f, (float)dhi[t][2 * h + cc], (float)dlo[t][2 * h + cc]) * ds;
+            } else {
+              v = acc[t][2 * h + cc];
+            }
             rw[(16 * t + gq + 8 * h) * MB + b] = v;
           }
         }
-    if constexpr (LAYOUT == PMPD_LAYOUT_KN) {
+    if constexpr (KN) {
 #pragma unroll
       for (int b = 0; b < MB; ++b)
         if (MB == 1 || b < M) {
@@ -346,7 +384,7 @@ struct Consumer {
         float v = 0.f;
 #pragma unroll
         for (int w = 0; w < NCW; ++w) v += red[(w * 64 + nl) * MB + b];
-        if constexpr (LAYOUT == PMPD_LAYOUT_KN) {
+        if constexpr (KN) {
 #pragma unroll
           for (int w = 0; w < NCW; ++w) v += redb[w * MB + b];
         }
@@ -370,9 +408,11 @@ struct Consumer {
         const int e = tid + r * NCW * 32;
         if (e < 64 * Me) part[(int64_t)(c - c_first) * 64 * Me + e] = vals[r];
       }
-      __threadfence();
       named_bar_sync(1, NCW * 32);
-      if (tid == 0) sm.flag = (atomicAdd(&a.counters[ng], 1) == c_last - c_first);
+      if (tid == 0) {
+        __threadfence();  // cumulative: orders the CTA's partial stores (bar.sync) before the ticket
+        sm.flag = (atomicAdd(&a.counters[ng], 1) == c_last - c_first);
+      }
       named_bar_sync(1, NCW * 32);
       if (sm.flag) {
         __threadfence();
@@ -393,13 +433,31 @@ struct Consumer {
     reset();
     int si = 0;
     TileCursor cur{T0, T0 / KT, T0 % KT};
+    enter_group(cur.ng);
     while (cur.t < T1) {
       const int end = cur.stage_end(T1, KT);
       const int slot = si % NSTAGE;
+#ifndef PMPD_GEMV_SKIP_MEMORY
       mbar_wait(&sm.full[slot], (si / NSTAGE) & 1);
-      if (warp < end - cur.t) tile<P>(smem + PL::kRing + slot * PL::kStage, warp, cur.kt + warp);
+#endif
+#ifdef PMPD_GEMV_SKIP_COMPUTE
+      if (false) {
+#else
+      if (warp < end - cur.t) {
+#endif
+        if constexpr (KN) {
+          tile_kn<P>(smem + PL::kRing + slot * PL::kStage, warp, cur.kt + warp, end - cur.t);
+        } else {
+#pragma unroll
+          for (int q = 0; q < TPW; ++q)
+            if (warp + q * NCW < end - cur.t)
+              tile_nk<P>(smem + PL::kRing + slot * PL::kStage, warp + q * NCW, cur.kt + warp + q * NCW);
+        }
+      }
       __syncwarp();
+#ifndef PMPD_GEMV_SKIP_MEMORY
       if (lane == 0) mbar_arrive(&sm.empty[slot]);
+#endif
       const int ng = cur.ng;
       cur.kt += end - cur.t;
       cur.t = end;
@@ -408,6 +466,7 @@ struct Consumer {
       if (cur.kt == KT) {
         cur.kt = 0;
         ++cur.ng;
+        if (cur.t < T1) enter_group(cur.ng);
       }
     }
   }
@@ -415,7 +474,7 @@ struct Consumer {
 
 // ---------------------------------------------------------------- kernel
 template <int LAYOUT, int PMAX, int MB, bool XS>
-__global__ void __launch_bounds__(NTHREADS, 2) qgemv_kernel(const GemvArgs a) {
+__global__ void __launch_bounds__(NTHREADS, 1) qgemv_kernel(const GemvArgs a) {
   using PL = Plan<PMAX, MB, XS>;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -444,7 +503,11 @@ __global__ void __launch_bounds__(NTHREADS, 2) qgemv_kernel(const GemvArgs a) {
 
   if (warp == NCW) {
     // ------------------------------------------------------------ producer
+#ifdef PMPD_GEMV_SKIP_MEMORY
+    if (false) {
+#else
     if (lane == 0) {
+#endif
       const uint64_t pol = policy_evict_first();
       int si = 0;
       TileCursor cur{T0, T0 / KT, T0 % KT};
@@ -471,9 +534,11 @@ __global__ void __launch_bounds__(NTHREADS, 2) qgemv_kernel(const GemvArgs a) {
 
   // -------------------------------------------------------------- consumers
   Consumer<LAYOUT, PMAX, MB, XS> cs{a, sm, smem_raw};
-  cs.bt = reinterpret_cast<uint32_t*>(smem_raw + PL::kBt) + warp * PL::kBtRows * 32;
+  cs.xq = smem_raw + PL::kXq + warp * PL::kXqWarp;
   cs.red = reinterpret_cast<float*>(smem_raw + PL::kRed);
   cs.redb = reinterpret_cast<float*>(smem_raw + PL::kRedb);
+  float* mxs = reinterpret_cast<float*>(smem_raw + PL::kMx);
+  cs.mx = mxs;
   cs.warp = warp;
   cs.lane = lane;
   cs.gq = lane >> 2;
@@ -485,12 +550,19 @@ __global__ void __launch_bounds__(NTHREADS, 2) qgemv_kernel(const GemvArgs a) {
   cs.G = G;
   cs.c = c;
   cs.M = a.m;
+  if constexpr (LAYOUT == PMPD_LAYOUT_KN) {
+    // zero the int8 activation rows that stay unused (b >= M)
+    for (int i = lane; i < PL::kXqWarp / 4; i += 32) reinterpret_cast<uint32_t*>(cs.xq)[i] = 0u;
+  }
   pdl_wait();  // activations and the workspace belong to the predecessor until here
-  if constexpr (XS) {
-    // stage x (zero-padded to a multiple of 64) in shared memory once
-    __half* xs = reinterpret_cast<__half*>(smem_raw + PL::kXs);
-    const int kp = KT * kTile;
-    for (int b = 0; b < MB; ++b)
+  const int Me = MB == 1 ? 1 : a.m;
+  float* red32 = reinterpret_cast<float*>(smem_raw + PL::kMx) + MAXM;  // 32 floats of scratch
+  for (int b = 0; b < Me; ++b) {
+    float m = 0.f;
+    if constexpr (XS) {
+      // stage x (zero-padded to a multiple of 64) in shared memory once, tracking max |x|
+      __half* xs = reinterpret_cast<__half*>(smem_raw + PL::kXs);
+      const int kp = KT * kTile;
       for (int k = threadIdx.x * 8; k < kp; k += NCW * 32 * 8) {
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
         const __half* src = a.x + (int64_t)b * a.ldx + k;
@@ -502,10 +574,33 @@ __global__ void __launch_bounds__(NTHREADS, 2) qgemv_kernel(const GemvArgs a) {
           for (int i = 0; i < 8; ++i) tmp[i] = (k + i < a.k_real) ? src[i] : __float2half(0.f);
           v = *reinterpret_cast<const uint4*>(tmp);
         }
+        const __half2* h2 = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __half22float2(h2[i]);
+          m = fmaxf(m, fmaxf(fabsf(f.x), fabsf(f.y)));
+        }
         *reinterpret_cast<uint4*>(xs + b * kXsMaxK + k) = v;
       }
-    named_bar_sync(1, NCW * 32);
-    cs.xs = xs;
+    } else if constexpr (LAYOUT == PMPD_LAYOUT_KN) {
+      for (int k = threadIdx.x; k < a.k_real; k += NCW * 32)
+        m = fmaxf(m, fabsf(__half2float(a.x[(int64_t)b * a.ldx + k])));
+    }
+    if constexpr (LAYOUT == PMPD_LAYOUT_KN) {
+      m = warp_max(m);
+      if (lane == 0) red32[warp] = m;
+      named_bar_sync(1, NCW * 32);
+      if (threadIdx.x == 0) {
+        float r = 0.f;
+        for (int w = 0; w < NCW; ++w) r = fmaxf(r, red32[w]);
+        mxs[b] = r;
+      }
+      named_bar_sync(1, NCW * 32);
+    }
+  }
+  named_bar_sync(1, NCW * 32);
+  if constexpr (XS) {
+    cs.xs = reinterpret_cast<__half*>(smem_raw + PL::kXs);
     cs.xld = kXsMaxK;
   } else {
     cs.xs = a.x;
@@ -593,7 +688,8 @@ int pmpd_gemv_workspace_bytes(const pmpd_qtensor* t, int32_t m, int64_t* bytes) 
   if (!t || !bytes) return fail(PMPD_ERR_CONFIG, "null argument");
   if (m < 1 || m > MAXM) return fail(PMPD_ERR_INPUT, "decode GEMV batch must be in [1, %d], got %d", MAXM, m);
   if (!is_tiled(t->layout)) return fail(PMPD_ERR_CONFIG, "GEMV needs a tiled layout (KN or NK)");
-  const int64_t head = ((int64_t)t->n_tiles * 4 + 4 + 255) / 256 * 256;
+  if (t->n_tiles > kWsCounters) return fail(PMPD_ERR_CONFIG, "GEMV output too wide (%d n-tiles)", t->n_tiles);
+  const int64_t head = kWsHead;
   *bytes = head + (int64_t)t->n_tiles * slots_for(t) * 64 * m * 4;
   return PMPD_OK;
 }
@@ -613,6 +709,7 @@ int pmpd_gemv(const pmpd_qtensor* t, const void* x, int32_t ldx, int32_t m, cons
   GemvArgs a;
   a.planes = static_cast<const uint8_t*>(t->data);
   a.scales = a.planes + (int64_t)t->p_max * t->plane_bytes;
+  a.aux = reinterpret_cast<const float*>(a.scales + t->scale_bytes);
   a.plane_bytes = t->plane_bytes;
   a.n_tiles = t->n_tiles;
   a.k_tiles = t->k_tiles;
@@ -630,8 +727,8 @@ int pmpd_gemv(const pmpd_qtensor* t, const void* x, int32_t ldx, int32_t m, cons
   a.accumulate = accumulate;
   uint8_t* w8 = static_cast<uint8_t*>(ws);
   a.counters = reinterpret_cast<int*>(w8);
-  a.status = reinterpret_cast<int*>(w8) + t->n_tiles;
-  a.partial = reinterpret_cast<float*>(w8 + ((int64_t)t->n_tiles * 4 + 4 + 255) / 256 * 256);
+  a.status = reinterpret_cast<int*>(w8) + kWsCounters;
+  a.partial = reinterpret_cast<float*>(w8 + kWsHead);
   a.max_slots = slots_for(t);
   const int grid = grid_for(t);
   cudaStream_t s = as_stream(stream);

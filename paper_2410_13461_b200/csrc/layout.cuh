@@ -15,9 +15,10 @@
 // a0..a3, with no shifts beyond one 8-bit rotate per word.  The per-row
 // offsets are removed exactly after the MMA.
 //
-// Slot -> fragment element (PTX ISA mma.m16n8k16 A layout):
-//   row  = gq + 8*(s & 1)                     (a0/a2: row gq, a1/a3: row gq+8)
-//   kk   = 2*tig + 8*((s >> 1) & 1) + (s >> 2) (a0/a1: k 2tig(+1), a2/a3: +8)
+// The slot -> (row, k) map differs per layout (see nk_/kn_tile_coord below):
+// NK tiles feed fp16 A fragments of mma.m16n8k16 (per-row f32 scales need
+// f32 accumulators per tile); KN tiles feed u8 A fragments of mma.m16n8k32
+// whose bytes are the bucket indices themselves (int32 accumulation).
 #pragma once
 #include <stdint.h>
 
@@ -33,8 +34,9 @@ struct TileCoord {
   int lane, w, t, s;
 };
 
-// tile-local (n_l, k_l) in [0,64)^2 -> (lane, word, m-tile, slot)
-PMPD_HD TileCoord tile_coord(int n_l, int k_l) {
+// ---- NK tiles: fragment order of mma.m16n8k16 (fp16 A, HMMA decode path) ----
+// slot s: row = gq + 8*(s&1), k = 16w + 2*tig + 8*((s>>1)&1) + (s>>2)
+PMPD_HD TileCoord nk_tile_coord(int n_l, int k_l) {
   TileCoord c;
   c.t = n_l >> 4;
   const int r = n_l & 15;
@@ -46,15 +48,43 @@ PMPD_HD TileCoord tile_coord(int n_l, int k_l) {
   c.lane = gq * 4 + tig;
   return c;
 }
-
-// inverse: (lane, w, t, s) -> tile-local (n_l, k_l)
-PMPD_HD void tile_inverse(int lane, int w, int t, int s, int* n_l, int* k_l) {
+PMPD_HD void nk_tile_inverse(int lane, int w, int t, int s, int* n_l, int* k_l) {
   const int gq = lane >> 2, tig = lane & 3;
   *n_l = 16 * t + gq + 8 * (s & 1);
   *k_l = 16 * w + 2 * tig + 8 * ((s >> 1) & 1) + (s >> 2);
 }
 
-// bit position inside the plane word
+// ---- KN tiles: fragment order of mma.m16n8k32 (u8 A, IMMA decode path) ----
+// A fragment (m-tile t, 32-k chunk c): a0/a1 = even/odd slots of word w = 2c,
+// a2/a3 = even/odd slots of word w = 2c+1; a register holds 4 consecutive k.
+// slot s: row = gq + 8*(s&1), k = 32*(w>>1) + 16*(w&1) + 4*tig + (s>>1)
+PMPD_HD TileCoord kn_tile_coord(int n_l, int k_l) {
+  TileCoord c;
+  c.t = n_l >> 4;
+  const int r = n_l & 15;
+  const int gq = r & 7, h = r >> 3;
+  c.w = ((k_l >> 5) << 1) | ((k_l >> 4) & 1);
+  const int kk = k_l & 15;
+  const int tig = kk >> 2, j = kk & 3;
+  c.s = h + 2 * j;
+  c.lane = gq * 4 + tig;
+  return c;
+}
+PMPD_HD void kn_tile_inverse(int lane, int w, int t, int s, int* n_l, int* k_l) {
+  const int gq = lane >> 2, tig = lane & 3;
+  *n_l = 16 * t + gq + 8 * (s & 1);
+  *k_l = 32 * (w >> 1) + 16 * (w & 1) + 4 * tig + (s >> 1);
+}
+
+PMPD_HD TileCoord tile_coord(bool kn, int n_l, int k_l) { return kn ? kn_tile_coord(n_l, k_l) : nk_tile_coord(n_l, k_l); }
+PMPD_HD void tile_inverse(bool kn, int lane, int w, int t, int s, int* n_l, int* k_l) {
+  if (kn)
+    kn_tile_inverse(lane, w, t, s, n_l, k_l);
+  else
+    nk_tile_inverse(lane, w, t, s, n_l, k_l);
+}
+
+// bit position inside the plane word: nibble slot s of m-tile t, code bit b_j
 PMPD_HD int tile_bitpos(int t, int s, int bj) { return (4 * s + t + bj) & 31; }
 
 // u32 word index of (lane, w) inside a tile's 512-byte plane chunk

@@ -143,7 +143,7 @@ __global__ void pack_planes_kernel(Geo g, const uint8_t* __restrict__ ref, int64
   for (int t = 0; t < 4; ++t)
     for (int s = 0; s < 8; ++s) {
       int nl, kl;
-      tile_inverse(lane, w, t, s, &nl, &kl);
+      tile_inverse(g.layout == PMPD_LAYOUT_KN, lane, w, t, s, &nl, &kl);
       const int n = ng * kTile + nl, k = kt * kTile + kl;
       if (n >= g.n || k >= g.k) continue;
       int r, c;
@@ -174,6 +174,24 @@ __global__ void pack_scales_kernel(Geo g, const float* __restrict__ mins, const 
   out[id] = v;
 }
 
+// KN aux block: 1 / max_k step[k][group(n-tile)] per n-tile (0 if all steps are 0).
+// The decode GEMV scales its integer activations by it so that the int16
+// operand x*step*32767/(max|x| * max step) never overflows.
+__global__ void pack_aux_kernel(Geo g, const float* __restrict__ deltas, float* __restrict__ aux) {
+  const int ng = blockIdx.x;
+  const int grp = ng * kTile / g.gs;
+  float mx = 0.f;
+  for (int k = threadIdx.x; k < g.k; k += blockDim.x) mx = fmaxf(mx, deltas[(int64_t)k * g.groups + grp]);
+  mx = warp_max(mx);
+  __shared__ float sh[32];
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) mx = fmaxf(mx, sh[i]);
+    aux[ng] = mx > 0.f ? 1.f / mx : 0.f;
+  }
+}
+
 // code of reference element (r, c) read from the top p planes of any layout
 __device__ __forceinline__ uint32_t load_code(const Geo& g, const uint8_t* base, int r, int c, int p) {
   uint32_t code = 0;
@@ -191,7 +209,7 @@ __device__ __forceinline__ uint32_t load_code(const Geo& g, const uint8_t* base,
     k = c;
   }
   const int ng = n >> 6, kt = k >> 6;
-  const TileCoord tc = tile_coord(n & 63, k & 63);
+  const TileCoord tc = tile_coord(g.layout == PMPD_LAYOUT_KN, n & 63, k & 63);
   const int64_t word = ((int64_t)ng * g.kt + kt) * 128 + tile_word(tc.lane, tc.w);
   const uint32_t* pl = reinterpret_cast<const uint32_t*>(base);
   for (int j = 0; j < p; ++j) {
@@ -248,7 +266,7 @@ __global__ void unpack_planes_kernel(Geo g, const uint8_t* __restrict__ base, in
     const int r = (int)(flat / g.cols), c = (int)(flat % g.cols);
     const int n = (g.layout == PMPD_LAYOUT_KN) ? c : r;
     const int k = (g.layout == PMPD_LAYOUT_KN) ? r : c;
-    const TileCoord tc = tile_coord(n & 63, k & 63);
+    const TileCoord tc = tile_coord(g.layout == PMPD_LAYOUT_KN, n & 63, k & 63);
     const int64_t word = ((int64_t)(n >> 6) * g.kt + (k >> 6)) * 128 + tile_word(tc.lane, tc.w);
     out |= ((pl[word] >> tile_bitpos(tc.t, tc.s, g.p_max - 1 - j)) & 1u) << b;
   }
@@ -363,13 +381,14 @@ int pmpd_qtensor_describe(int32_t rows, int32_t cols, int32_t group_size, int32_
     t.k_tiles = (t.k + kTile - 1) / kTile;
     t.plane_bytes = (int64_t)t.n_tiles * t.k_tiles * kTilePlaneBytes;
     t.scale_bytes = (int64_t)t.n_tiles * t.k_tiles * kTileScaleBytes;
+    t.aux_bytes = layout == PMPD_LAYOUT_KN ? ((int64_t)t.n_tiles * 4 + 255) / 256 * 256 : 0;
   } else {
     t.n_tiles = t.k_tiles = 0;
     t.plane_bytes = ((int64_t)rows * cols + 7) / 8;
     t.plane_bytes = (t.plane_bytes + 15) / 16 * 16;  // keep the scale region 16-byte aligned
     t.scale_bytes = 2LL * rows * t.groups * 4;
   }
-  t.total_bytes = (int64_t)p_max * t.plane_bytes + t.scale_bytes;
+  t.total_bytes = (int64_t)p_max * t.plane_bytes + t.scale_bytes + t.aux_bytes;
   t.data = out->data;
   *out = t;
   return PMPD_OK;
@@ -430,6 +449,9 @@ int pmpd_pack(const pmpd_qtensor* t, const uint8_t* ref_planes, const float* min
   const int64_t nsc = (int64_t)t->n_tiles * t->k_tiles * 128;
   pack_scales_kernel<<<blocks_for(nsc), kThreads, 0, s>>>(
       g, mins, deltas, reinterpret_cast<float*>(base + (int64_t)t->p_max * t->plane_bytes));
+  if (t->layout == PMPD_LAYOUT_KN)
+    pack_aux_kernel<<<t->n_tiles, kThreads, 0, s>>>(
+        g, deltas, reinterpret_cast<float*>(base + (int64_t)t->p_max * t->plane_bytes + t->scale_bytes));
   return check_launch("pmpd_pack");
 }
 

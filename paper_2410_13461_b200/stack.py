@@ -22,6 +22,7 @@ import torch
 import torch.nn.functional as F
 
 from . import _capi
+from .engine import OpSpec, Program
 from .linear import Workspace, gemv, workspace_bytes
 from .quant import QuantizedTensor, quantize_tensor
 
@@ -132,6 +133,29 @@ class LinearStack:
             gemv(wdn, self.u[:, :f], self.p_dev, self.ws, out=self.h, alpha=a_f)
             inp = self.h
         gemv(self.head[1], inp, self.p_dev, self.ws, out=self.logits, alpha=a_d)
+
+    def build_engine(self) -> Program:
+        """The same chain as ``token`` as one persistent-engine program."""
+        d, f = self.shape.d_model, self.shape.d_ff
+        a_d = 1.0 / (self.std * math.sqrt(d))
+        a_f = 1.0 / (self.std * math.sqrt(f))
+        ops = []
+        for i, ((_, wqkv), (_, wo), (_, wup), (_, wdn)) in enumerate(self.layers):
+            base = 4 * i
+            ops.append(OpSpec(wqkv, src=base - 1, src_col=0, in_alpha=a_f if i else 1.0))
+            ops.append(OpSpec(wo, src=base, src_col=2 * d, in_alpha=a_d))
+            ops.append(OpSpec(wup, src=base + 1, src_col=0, in_alpha=a_d))
+            ops.append(OpSpec(wdn, src=base + 2, src_col=0, in_alpha=a_d))
+        ops.append(OpSpec(self.head[1], src=len(ops) - 1, src_col=0, in_alpha=a_f))
+        self.program = Program(ops, y_alpha=a_d)
+        return self.program
+
+    def token_engine(self) -> None:
+        """One decode token's linear stack through the persistent engine (graph-capturable)."""
+        s = torch.cuda.current_stream().cuda_stream
+        _capi.call("pmpd_sched_step", self.sched.data_ptr(), self.n_prec, self.step.data_ptr(),
+                   self.p_dev.data_ptr(), 1, s)
+        self.program.run(self.x0, self.p_dev, self.logits)
 
     def token_fp16(self) -> None:
         """fp16 baseline of the same chain through cuBLAS (precision 16, tinylm.py:204-213)."""

@@ -1,0 +1,77 @@
+"""GPU parity of the persistent decode engine: the whole chained linear stack in one kernel
+vs the per-op GEMV chain and vs the float64 oracle."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import quant as oq
+from paper_2410_13461_b200 import _capi
+from paper_2410_13461_b200.engine import OpSpec, Program
+from paper_2410_13461_b200.quant import quantize_tensor
+from paper_2410_13461_b200.stack import LinearStack, StackShape
+from pmpd_testutil import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def _pdev(p):
+    return torch.tensor([p], dtype=torch.int32, device="cuda")
+
+
+@pytest.mark.parametrize("shape", [StackShape(2, 256, 512, 1000), StackShape(3, 512, 1376, 2048),
+                                   StackShape(1, 4096, 11008, 32000)])
+def test_engine_matches_per_op_chain(shape):
+    st = LinearStack(shape, seed=3)
+    st.build_engine()
+    for p in (4, 3, 2):
+        st.set_schedule({p: 0})
+        st.token()
+        ref = st.logits.clone()
+        st.set_schedule({p: 0})
+        st.logits.zero_()
+        st.token_engine()
+        torch.cuda.synchronize()
+        err = rel_l2(st.logits.cpu().numpy(), ref.cpu().numpy())
+        assert err < 3e-3, (shape, p, err)
+        assert int(st.program.bar.sum().item()) == 0  # counters self-reset
+
+
+def test_engine_two_layer_chain_vs_oracle():
+    rng = np.random.default_rng(0)
+    K, N1, N2 = 320, 384, 200
+    w1 = (0.02 * rng.standard_normal((K, N1))).astype(np.float32)
+    w2 = (0.02 * rng.standard_normal((N1 - 64, N2))).astype(np.float32)
+    x = rng.standard_normal((1, K)).astype(np.float16)
+    q1, q2 = quantize_tensor(w1, 4, 64), quantize_tensor(w2, 4, 64)
+    a1 = 1.0 / (0.02 * math.sqrt(K))
+    prog = Program([OpSpec(q1.packed(_capi.LAYOUT_KN)),
+                    OpSpec(q2.packed(_capi.LAYOUT_KN), src=0, src_col=64, in_alpha=a1)], y_alpha=0.5)
+    y = torch.zeros(N2, device="cuda")
+    xd = torch.from_numpy(x).cuda()
+    r1, r2 = oq.quantize(w1, 4, 64), oq.quantize(w2, 4, 64)
+    for p in (4, 3, 2):
+        prog.run(xd, _pdev(p), y)
+        h = a1 * (x.astype(np.float64) @ oq.dequantize(r1, p))
+        h16 = h[:, 64:].astype(np.float16).astype(np.float64)
+        want = 0.5 * (h16 @ oq.dequantize(r2, p))
+        assert rel_l2(y.cpu().numpy(), want[0]) < 3e-3, p
+
+
+def test_engine_silu_input_transform():
+    rng = np.random.default_rng(1)
+    K, F, N = 256, 192, 128
+    wu = (0.05 * rng.standard_normal((K, 2 * F))).astype(np.float32)
+    wd = (0.05 * rng.standard_normal((F, N))).astype(np.float32)
+    x = rng.standard_normal((1, K)).astype(np.float16)
+    qu, qd = quantize_tensor(wu, 4, 64), quantize_tensor(wd, 4, 64)
+    prog = Program([OpSpec(qu.packed(_capi.LAYOUT_KN)),
+                    OpSpec(qd.packed(_capi.LAYOUT_KN), src=0, src_col=0, act=1, act_off=F, in_alpha=1.0)])
+    y = torch.zeros(N, device="cuda")
+    prog.run(torch.from_numpy(x).cuda(), _pdev(4), y)
+    u = x.astype(np.float64) @ oq.dequantize(oq.quantize(wu, 4, 64), 4)
+    g, up = u[:, :F], u[:, F:]
+    a = (g / (1 + np.exp(-g)) * up).astype(np.float16).astype(np.float64)
+    want = a @ oq.dequantize(oq.quantize(wd, 4, 64), 4)
+    assert rel_l2(y.cpu().numpy(), want[0]) < 3e-3

@@ -103,3 +103,21 @@ def test_sched_step_device_hook(gold_sched):
     got = torch.cat(got).cpu().tolist()
     assert got == gold_sched["cfg3/pat"].tolist()
     assert int(step.item()) == 512
+
+
+def test_shared_workspace_across_shapes():
+    """One workspace serves GEMVs of different widths back to back (counters must stay zeroed)."""
+    ws = Workspace()
+    outs = []
+    for (K, N) in [(4096, 4096), (4096, 22016), (11008, 4096), (4096, 32000), (4096, 12288)]:
+        w, x = _case(N, K, _capi.LAYOUT_KN, N + K, 1)
+        ref = oq.quantize(w, 4, 64)
+        pk = quantize_tensor_cached(w)
+        y = gemv(pk, torch.from_numpy(x).cuda(), _pdev(2), ws)
+        outs.append((y, ref, x))
+    for y, ref, x in outs:
+        assert rel_l2(y.cpu().numpy(), _oracle_y(ref, x, 2, _capi.LAYOUT_KN)) < 2e-3
+
+
+def quantize_tensor_cached(w):
+    return quant.quantize_tensor(w, 4, 64).packed(_capi.LAYOUT_KN)

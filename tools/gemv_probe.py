@@ -17,6 +17,7 @@ ap.add_argument("--iters", type=int, default=50)
 ap.add_argument("--m", type=int, default=1)
 ap.add_argument("--layout", default="kn")
 ap.add_argument("--graph", action="store_true")
+ap.add_argument("--p", default="4,3,2")
 args = ap.parse_args()
 lay = _capi.LAYOUT_KN if args.layout == "kn" else _capi.LAYOUT_NK
 torch.manual_seed(0)
@@ -36,7 +37,7 @@ for spec in args.shapes.split(","):
     ws = Workspace(workspace_bytes(pks[0], args.m))
     x = torch.randn(args.m, K, device="cuda").half()
     y = torch.empty(args.m, N, device="cuda")
-    for p in (4, 3, 2):
+    for p in [int(v) for v in args.p.split(",")]:
         pd = torch.tensor([p], dtype=torch.int32, device="cuda")
         for i in range(3):
             gemv(pks[i % copies], x, pd, ws, out=y)

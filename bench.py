@@ -178,7 +178,9 @@ def main():
     assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
 
     st = LinearStack(shape, seed=1234 + rank, keep_fp16=not args.no_fp16)
-    g = st.capture(st.token)
+    st.build_engine()
+    g = st.capture(st.token_engine)          # headline: persistent decode engine, one launch per token
+    g_ops = st.capture(st.token)             # per-op decode-GEMV chain (129 PDL launches per token)
 
     def barrier():
         torch.cuda.synchronize()
@@ -204,8 +206,12 @@ def main():
         for _ in range(3):
             g.replay()
         us = time_tokens(g, 64)
+        for _ in range(3):
+            g_ops.replay()
+        us_ops = time_tokens(g_ops, 32)
         per_p[p] = {"us_per_token": us, "GBps": algorithmic_bytes(shape, p) / us * 1e-3,
-                    "stream_GBps": st.stream_bytes(p) / us * 1e-3}
+                    "stream_GBps": st.stream_bytes(p) / us * 1e-3,
+                    "per_op_chain_us_per_token": us_ops}
     if st.fp16 is not None:
         gf = st.capture(st.token_fp16)
         for _ in range(3):
@@ -213,6 +219,9 @@ def main():
         us = time_tokens(gf, 64)
         per_p[16] = {"us_per_token": us, "GBps": algorithmic_bytes(shape, 16) / us * 1e-3, "impl": "cuBLAS fp16"}
         del gf
+    if st.fp16 is not None:
+        st.fp16 = None
+        torch.cuda.empty_cache()
 
     # ---- headline: progressive 4->3->2 over 512 tokens per step
     st.set_schedule(SCHED)
@@ -285,12 +294,13 @@ def main():
         "weighted_gpu_latency_us": weighted_kernel,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None, "peak_source": peak_src,
-                     "note": "algorithmic bytes (perf.py:101 + activations) per token / µs per token; the qgemv "
-                             "kernel is 129 of the 130 launches per token"},
+                     "note": "algorithmic bytes (perf.py:101 + activations) per token / µs per token; one "
+                             "persistent engine kernel carries all 129 linear layers of a token (plus 1 tiny "
+                             "precision-hook launch)"},
         "clocks": clk.summary(),
         "e2e": {"value": e2e_us, "unit": "us/token", "h2d_bytes_per_step": HORIZON * st.x0.numel() * 2,
                 "d2h_bytes_per_step": HORIZON * st.logits.numel() * 4},
-        "gpu_launches": args.steps * HORIZON * (1 + 4 * shape.n_layers + 1),
+        "gpu_launches": args.steps * HORIZON * 2,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         us, cores, cpu_pp, sample = cpu_sample(shape)

@@ -175,8 +175,9 @@ int pmpd_engine_make_op(const pmpd_qtensor* t, int32_t src, int32_t src_col, int
                         void* op_host);
 int pmpd_engine_run(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const void* x_in_dev, float* y_out_dev,
                     float y_alpha, uint32_t* bar_dev, int32_t* status_dev, void* stream);
-/* Same, recording a per-CTA per-op timeline (globaltimer ns) into trace_dev [grid][n_ops][4]:
- * {input ready, input staged, tiles done, op published}. */
+/* Same, recording a per-CTA per-op timeline (globaltimer ns):
+ * {input ready, input staged, tiles done, op published, warp-0 cycles in tiles, tile calls, loop cycles, 0}
+ * (trace_dev is [grid][n_ops][8]). */
 int pmpd_engine_run_traced(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const void* x_in_dev,
                            float* y_out_dev, float y_alpha, uint32_t* bar_dev, int32_t* status_dev, int64_t* trace_dev,
                            void* stream);

@@ -206,9 +206,20 @@ PMPD_DEV void engine_tile(const uint8_t* st, int stiles_cnt, int wslot, int kt, 
 }
 
 // ------------------------------------------------------------------ kernel
-template <int P>
-PMPD_DEV void consumer_loop(const EngineArgs& a, uint8_t* smem, Bars& bars, int G, int c, int stage_bytes,
-                            int nstage) {
+// Only the tile function is specialised per precision (keeps the kernel's code size,
+// and so instruction-cache pressure, small).
+PMPD_DEV void tile_dispatch(int p, const uint8_t* st, int cnt, int wslot, int kt, int lane, const __half* xs, uint8_t* xq,
+                            float qs, int (&dhi)[4][4], int (&dlo)[4][4], float& bias) {
+  switch (p) {
+    case 4: engine_tile<4>(st, cnt, wslot, kt, lane, xs, xq, qs, dhi, dlo, bias); break;
+    case 3: engine_tile<3>(st, cnt, wslot, kt, lane, xs, xq, qs, dhi, dlo, bias); break;
+    case 2: engine_tile<2>(st, cnt, wslot, kt, lane, xs, xq, qs, dhi, dlo, bias); break;
+    default: engine_tile<1>(st, cnt, wslot, kt, lane, xs, xq, qs, dhi, dlo, bias); break;
+  }
+}
+
+PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bars& bars, int G, int c,
+                            int stage_bytes, int nstage) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tig = lane & 3;
   __half* xs = reinterpret_cast<__half*>(smem + kSmX);
   uint8_t* xq = smem + kSmXq + warp * E_TPW * 128;
@@ -239,6 +250,13 @@ PMPD_DEV void consumer_loop(const EngineArgs& a, uint8_t* smem, Bars& bars, int 
     } else if (r.T1 <= r.T0) {
       hi0 = 0;
     }
+    // per-n-group step normalisers of this op (static: prefetched before the grid wait)
+    float idm_pre[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int ngp = r.T0 / r.KT + i;
+      idm_pre[i] = (r.T1 > r.T0 && ngp < op.n_tiles) ? __ldg(op.aux + ngp) : 0.f;
+    }
     // slot counts of the source n-groups this CTA reads (static table: safe before the wait)
     if (op.src >= 0) {
       const EngineOp& sop = a.ops[op.src];
@@ -263,75 +281,101 @@ PMPD_DEV void consumer_loop(const EngineArgs& a, uint8_t* smem, Bars& bars, int 
         while (ld_acquire(a.bar) < (unsigned)(oi * G)) __nanosleep(32);
       named_bar_sync(1, E_NCW * 32);
     }
-    if (a.trace && threadIdx.x == 0) a.trace[((int64_t)c * a.n_ops + oi) * 4 + 0] = gtimer();
+    if (a.trace && threadIdx.x == 0) a.trace[((int64_t)c * a.n_ops + oi) * 8 + 0] = gtimer();
     float mx = 0.f;
     const EngineOp* src = op.src >= 0 ? &a.ops[op.src] : nullptr;
-    // Each thread stages 4 consecutive elements: all partial-slot loads of a group are
-    // issued before the sums (one L2 round trip), slot counts come from a host table.
+    // Each thread stages groups of 4 consecutive elements, SB groups per batch: all
+    // partial-slot loads of a batch are issued before any sum (one L2 round trip per batch).
+    constexpr int SB = 2;
     for (int seg2 = 0; seg2 < 2; ++seg2) {
       const int klo = (seg2 ? lo1 : lo0) * kTile, khi = (seg2 ? hi1 : hi0) * kTile;
-      for (int k = klo + 4 * threadIdx.x; k < khi; k += 4 * E_NCW * 32) {
-        float v[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int kb = klo + 4 * threadIdx.x; kb < khi; kb += 4 * SB * E_NCW * 32) {
+        float v[SB][4];
         if (!src) {
-          if (k + 4 <= op.k_real) {
-            const uint2 raw = __ldg(reinterpret_cast<const uint2*>(a.x_in + k));
-            const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
-            const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
-            v[0] = f0.x; v[1] = f0.y; v[2] = f1.x; v[3] = f1.y;
-          } else {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) v[i] = (k + i < op.k_real) ? __half2float(a.x_in[k + i]) : 0.f;
+          for (int bi = 0; bi < SB; ++bi) {
+            const int k = kb + bi * 4 * E_NCW * 32;
+            if (k + 4 <= op.k_real) {
+              const uint2 raw = __ldg(reinterpret_cast<const uint2*>(a.x_in + k));
+              const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
+              const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
+              v[bi][0] = f0.x; v[bi][1] = f0.y; v[bi][2] = f1.x; v[bi][3] = f1.y;
+            } else {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) v[bi][i] = (k + i < op.k_real) ? __half2float(a.x_in[k + i]) : 0.f;
+            }
           }
         } else {
-          auto reduced4 = [&](int n, int ksel, int which, float (&o)[4]) {  // 4 elements of one n-group
-            const int ng = n >> 6;
-            const int ns = ns_s[which * 512 + 2 * (ksel >> 6) + (((n & 63) < ((op.src_col + which * op.act_off) & 63)) ? 1 : 0)];
-            const float4* pp = reinterpret_cast<const float4*>(src->part + ((int64_t)ng * src->max_slots) * 64 +
-                                                               (n & 63));
-            float4 acc[kMaxSlotsFast];
+          const int nsrc = op.act == 1 ? 2 : 1;
+          float4 acc[2][SB][kMaxSlotsFast];
+          int nsv[2][SB];
 #pragma unroll
-            for (int q = 0; q < kMaxSlotsFast; ++q)
-              acc[q] = q < ns ? __ldcg(pp + q * 16) : make_float4(0.f, 0.f, 0.f, 0.f);
-            float4 s4 = acc[0];
+          for (int which = 0; which < 2; ++which) {
+            if (which >= nsrc) break;
 #pragma unroll
-            for (int q = 1; q < kMaxSlotsFast; ++q) {
-              s4.x += acc[q].x;
-              s4.y += acc[q].y;
-              s4.z += acc[q].z;
-              s4.w += acc[q].w;
+            for (int bi = 0; bi < SB; ++bi) {
+              const int k = kb + bi * 4 * E_NCW * 32;
+              const int n = op.src_col + which * op.act_off + k;
+              const int ng = n >> 6;
+              const int ns = (k < khi) ? ns_s[which * 512 + 2 * (k >> 6) +
+                                              (((n & 63) < ((op.src_col + which * op.act_off) & 63)) ? 1 : 0)]
+                                       : 0;
+              nsv[which][bi] = ns;
+              const float4* pp = reinterpret_cast<const float4*>(src->part + ((int64_t)ng * src->max_slots) * 64 +
+                                                                 (n & 63));
+#pragma unroll
+              for (int q = 0; q < kMaxSlotsFast; ++q)
+                acc[which][bi][q] = q < ns ? __ldcg(pp + q * 16) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            for (int q = kMaxSlotsFast; q < ns; ++q) {  // rare: more contributors than the fast path holds
-              const float4 e = __ldcg(pp + q * 16);
-              s4.x += e.x;
-              s4.y += e.y;
-              s4.z += e.z;
-              s4.w += e.w;
-            }
-            o[0] = s4.x * op.in_alpha;
-            o[1] = s4.y * op.in_alpha;
-            o[2] = s4.z * op.in_alpha;
-            o[3] = s4.w * op.in_alpha;
-          };
-          float g[4];
-          reduced4(op.src_col + k, k, 0, g);
-          if (op.act == 1) {
-            float u[4];
-            reduced4(op.src_col + op.act_off + k, k, 1, u);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) v[i] = g[i] / (1.f + __expf(-g[i])) * u[i];
-          } else {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) v[i] = g[i];
           }
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            if (k + i >= op.k_real) v[i] = 0.f;
+          for (int bi = 0; bi < SB; ++bi) {
+            const int k = kb + bi * 4 * E_NCW * 32;
+            float r[2][4];
+#pragma unroll
+            for (int which = 0; which < 2; ++which) {
+              if (which >= nsrc) break;
+              float4 s4 = acc[which][bi][0];
+#pragma unroll
+              for (int q = 1; q < kMaxSlotsFast; ++q) {
+                s4.x += acc[which][bi][q].x;
+                s4.y += acc[which][bi][q].y;
+                s4.z += acc[which][bi][q].z;
+                s4.w += acc[which][bi][q].w;
+              }
+              const int n = op.src_col + which * op.act_off + k;
+              const float4* pp = reinterpret_cast<const float4*>(src->part +
+                                                                 ((int64_t)(n >> 6) * src->max_slots) * 64 + (n & 63));
+              for (int q = kMaxSlotsFast; q < nsv[which][bi]; ++q) {  // rare: many contributors
+                const float4 e = __ldcg(pp + q * 16);
+                s4.x += e.x;
+                s4.y += e.y;
+                s4.z += e.z;
+                s4.w += e.w;
+              }
+              r[which][0] = s4.x * op.in_alpha;
+              r[which][1] = s4.y * op.in_alpha;
+              r[which][2] = s4.z * op.in_alpha;
+              r[which][3] = s4.w * op.in_alpha;
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              float g = r[0][i];
+              if (op.act == 1) g = g / (1.f + __expf(-g)) * r[1][i];
+              v[bi][i] = (k + i < op.k_real) ? g : 0.f;
+            }
+          }
         }
-        __half2 h01 = __floats2half2_rn(v[0], v[1]), h23 = __floats2half2_rn(v[2], v[3]);
-        *reinterpret_cast<__half2*>(xs + k) = h01;
-        *reinterpret_cast<__half2*>(xs + k + 2) = h23;
-        const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
-        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(f01.x), fabsf(f01.y)), fmaxf(fabsf(f23.x), fabsf(f23.y))));
+#pragma unroll
+        for (int bi = 0; bi < SB; ++bi) {
+          const int k = kb + bi * 4 * E_NCW * 32;
+          if (k >= khi) break;
+          const __half2 h01 = __floats2half2_rn(v[bi][0], v[bi][1]), h23 = __floats2half2_rn(v[bi][2], v[bi][3]);
+          *reinterpret_cast<__half2*>(xs + k) = h01;
+          *reinterpret_cast<__half2*>(xs + k + 2) = h23;
+          const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+          mx = fmaxf(mx, fmaxf(fmaxf(fabsf(f01.x), fabsf(f01.y)), fmaxf(fabsf(f23.x), fabsf(f23.y))));
+        }
       }
     }
     mx = warp_max(mx);
@@ -340,7 +384,7 @@ PMPD_DEV void consumer_loop(const EngineArgs& a, uint8_t* smem, Bars& bars, int 
     mx = 0.f;
 #pragma unroll
     for (int w = 0; w < E_NCW; ++w) mx = fmaxf(mx, misc[8 + w]);
-    if (a.trace && threadIdx.x == 0) a.trace[((int64_t)c * a.n_ops + oi) * 4 + 1] = gtimer();
+    if (a.trace && threadIdx.x == 0) a.trace[((int64_t)c * a.n_ops + oi) * 8 + 1] = gtimer();
     // ---------------------------------------------------------- tiles of this op
     int t = r.T0, ng = r.T0 / r.KT, kt = r.T0 % r.KT;
     int dhi[4][4], dlo[4][4];
@@ -350,19 +394,34 @@ PMPD_DEV void consumer_loop(const EngineArgs& a, uint8_t* smem, Bars& bars, int 
 #pragma unroll
       for (int e = 0; e < 4; ++e) dhi[i][e] = dlo[i][e] = 0;
     float qs = 0.f;
+    long long tcyc = 0, tcalls = 0, scyc0 = clock64();
+    int ngi = 0;
     if (t < r.T1) {
-      const float idm = __ldg(op.aux + ng);
+      const float idm = idm_pre[0];
       qs = (mx > 0.f && idm > 0.f) ? 32767.f * idm / mx : 0.f;
     }
     while (t < r.T1) {
       const int end = min(min(t + E_STILES, r.T1), t - kt + r.KT);
+#ifndef PMPD_ENGINE_SKIP_MEMORY
       mbar_wait(&bars.full[slot], phase);
+#endif
+#ifdef PMPD_ENGINE_SKIP_COMPUTE
+      if (false) {
+#else
       if (warp < end - t) {
-        engine_tile<P>(smem + kSmRing + slot * stage_bytes, end - t, warp, kt + warp, lane, xs, xq, qs, dhi, dlo,
-                       bias);
+#endif
+        const long long c0 = clock64();
+        tile_dispatch(P, smem + kSmRing + slot * stage_bytes, end - t, warp, kt + warp, lane, xs, xq, qs, dhi, dlo,
+                      bias);
+        if (a.trace) {
+          tcyc += clock64() - c0;
+          ++tcalls;
+        }
       }
       __syncwarp();
+#ifndef PMPD_ENGINE_SKIP_MEMORY
       if (lane == 0) mbar_arrive(&bars.empty[slot]);
+#endif
       if (++slot == nstage) {
         slot = 0;
         phase ^= 1u;
@@ -397,13 +456,19 @@ PMPD_DEV void consumer_loop(const EngineArgs& a, uint8_t* smem, Bars& bars, int 
           kt = 0;
           ++ng;
           if (t < r.T1) {
-            const float idm = __ldg(op.aux + ng);
+            ++ngi;
+            const float idm = ngi < 4 ? idm_pre[ngi] : __ldg(op.aux + ng);
             qs = (mx > 0.f && idm > 0.f) ? 32767.f * idm / mx : 0.f;
           }
         }
       }
     }
-    if (a.trace && threadIdx.x == 0) a.trace[((int64_t)c * a.n_ops + oi) * 4 + 2] = gtimer();
+    if (a.trace && threadIdx.x == 0) {
+      a.trace[((int64_t)c * a.n_ops + oi) * 8 + 2] = gtimer();
+      a.trace[((int64_t)c * a.n_ops + oi) * 8 + 4] = tcyc;
+      a.trace[((int64_t)c * a.n_ops + oi) * 8 + 5] = tcalls;
+      a.trace[((int64_t)c * a.n_ops + oi) * 8 + 6] = clock64() - scyc0;
+    }
   }
 }
 
@@ -437,7 +502,11 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
 
   if (warp == E_PROD) {
     // ------------------------------------------------------------ producer
+#ifdef PMPD_ENGINE_SKIP_MEMORY
+    if (false) {
+#else
     if (lane == 0) {
+#endif
       const uint64_t pol = policy_evict_first();
       int slot = 0, used = 0;
       uint32_t phase = 0;
@@ -509,20 +578,15 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
         // A CTA with no tiles in op oi must not publish it before every CTA has
         // published ops < oi: the ticket count is a completion test only if tickets
         // of op oi never precede the completion of op oi-1.
-        if (oi > 0)
+        if (oi > 0 && r.T1 <= r.T0)
           while (ld_acquire(a.bar) < (unsigned)(oi * G)) __nanosleep(32);
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar) : "memory");
-        if (a.trace) a.trace[((int64_t)c * a.n_ops + oi) * 4 + 3] = gtimer();
+        if (a.trace) a.trace[((int64_t)c * a.n_ops + oi) * 8 + 3] = gtimer();
       }
     }
   } else {
     // ------------------------------------------------------------ consumers
-    switch (p) {
-      case 4: consumer_loop<4>(a, smem, bars, G, c, stage_bytes, nstage); break;
-      case 3: consumer_loop<3>(a, smem, bars, G, c, stage_bytes, nstage); break;
-      case 2: consumer_loop<2>(a, smem, bars, G, c, stage_bytes, nstage); break;
-      default: consumer_loop<1>(a, smem, bars, G, c, stage_bytes, nstage); break;
-    }
+    consumer_loop(p, a, smem, bars, G, c, stage_bytes, nstage);
   }
   // ---------------------------------------------------------------- final output
   __syncthreads();

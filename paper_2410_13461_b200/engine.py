@@ -62,9 +62,9 @@ class Program:
         self.n_out = ops[-1].packed.desc.n
 
     def run_traced(self, x_in, p_dev, y_out):
-        """One pass recording the per-CTA per-op timeline; returns int64 [grid, n_ops, 4] (ns)."""
+        """One pass recording the per-CTA per-op timeline; returns int64 [grid, n_ops, 8]: 4 timestamps (ns), warp-0 tile cycles, tile calls, loop cycles."""
         g = _capi.lib().pmpd_engine_grid()
-        tr = torch.zeros((g, len(self.ops), 4), dtype=torch.int64, device="cuda")
+        tr = torch.zeros((g, len(self.ops), 8), dtype=torch.int64, device="cuda")
         _capi.call("pmpd_engine_run_traced", self.table.data_ptr(), len(self.ops), p_dev.data_ptr(),
                    x_in.data_ptr(), y_out.data_ptr(), self.y_alpha, self.bar.data_ptr(), self.status.data_ptr(),
                    tr.data_ptr(), torch.cuda.current_stream().cuda_stream)

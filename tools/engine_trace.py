@@ -15,11 +15,18 @@ for name, ops in (("o x4", [OpSpec(o)] + [OpSpec(o, src=i) for i in range(3)]), 
     y = torch.zeros(ops[-1].packed.desc.n, device="cuda")
     for _ in range(3):
         tr = prog.run_traced(x, pd, y)
-    t0 = tr[tr > 0].min()
-    tr = (tr - t0).float() / 1000.0  # us
+    cyc = tr[:, :, 4:7].clone()
+    tt = tr[:, :, :4]
+    t0 = tt[tt > 0].min()
+    tr = (tt - t0).float() / 1000.0  # us
     print(f"== {name}")
     for oi in range(len(ops)):
         col = tr[:, oi, :]
         valid = col[:, 3] > 0
         print(f" op{oi}: ready med {col[:,0].median():6.2f} max {col[:,0].max():6.2f} | staged med {col[:,1].median():6.2f} max {col[:,1].max():6.2f}"
               f" | tiles med {col[:,2].median():6.2f} max {col[:,2].max():6.2f} | publish med {col[valid,3].median():6.2f} max {col[:,3].max():6.2f}")
+        cc = cyc[:, oi, :].float()
+        m = cc[:, 1] > 0
+        if m.any():
+            print(f"       warp0: tile calls {cc[m,1].median():.0f}, cycles/call {float((cc[m,0]/cc[m,1]).median()):.0f}, "
+                  f"tile share of loop {float((cc[m,0]/cc[m,2]).median()):.2f}")

@@ -192,3 +192,86 @@ class LinearStack:
             for _, pk in lay:
                 tot += pk.stream_bytes(p)
         return tot
+
+
+class TPLinearStack:
+    """The decode linear stack tensor-parallel over ``world`` GPUs (one process per GPU, NCCL).
+
+    Column-parallel q|k|v (by heads), gate|up (same offsets) and head (by vocabulary);
+    row-parallel o and down, each followed by an NCCL all-reduce of the batch x d
+    partial sums; the vocabulary shards are all-gathered.  All ranks draw the same
+    full weights from the same seed, quantize them bit-exactly and keep their
+    group-aligned sub-blocks (paper_2410_13461_b200.tp), so TP computes the same
+    function as the 1-GPU stack.
+    """
+
+    def __init__(self, shape: StackShape, n_heads: int, rank: int, world: int, group, p_max: int = 4,
+                 group_size: int = 64, seed: int = 0, std: float = 0.02, m: int = 1):
+        from . import tp
+        self.shape, self.rank, self.world, self.group, self.m, self.std = shape, rank, world, group, m, std
+        d, f, V = shape.d_model, shape.d_ff, shape.vocab
+        gen = torch.Generator(device="cuda")
+        gen.manual_seed(seed)
+        self.plan = tp.plan_layer(d, n_heads, f, world, rank, group_size)
+        self.head_cols = tp.plan_head(V, world, rank, group_size)
+        self.head_sizes = [tp.plan_head(V, world, r, group_size).size for r in range(world)]
+
+        def make(K, N, cols=None, rows=None):
+            w = _rand_kn(K, N, std, gen)
+            qt = quantize_tensor(w, p_max, group_size)
+            del w
+            qt = tp.shard_columns(qt, cols) if cols is not None else tp.shard_rows(qt, rows)
+            pk = qt.packed(_capi.LAYOUT_KN)
+            qt.drop_reference_copy()
+            return pk
+
+        P = self.plan
+        self.layers = []
+        for _ in range(shape.n_layers):
+            self.layers.append([make(d, 3 * d, cols=P.qkv_cols), make(d, d, rows=P.o_rows),
+                                make(d, 2 * f, cols=P.up_cols), make(f, d, rows=P.down_rows)])
+        self.head = make(d, V, cols=[self.head_cols])
+        torch.cuda.synchronize()
+        self.ws = Workspace(max(workspace_bytes(pk, m) for lay in self.layers for pk in lay))
+        self.ws.ensure(workspace_bytes(self.head, m))
+        hq = P.o_rows.size
+        self.x16 = torch.randn((m, d), device="cuda", generator=gen).half()
+        self.qkv = torch.empty((m, 3 * hq), device="cuda", dtype=torch.float16)
+        self.part = torch.empty((m, d), device="cuda", dtype=torch.float32)
+        self.u = torch.empty((m, 2 * P.ff.size), device="cuda", dtype=torch.float16)
+        self.logits_loc = torch.zeros((m, max(self.head_sizes)), device="cuda", dtype=torch.float32)
+        self.logits_all = torch.zeros((world, m, max(self.head_sizes)), device="cuda", dtype=torch.float32)
+        self.p_dev = torch.full((1,), p_max, dtype=torch.int32, device="cuda")
+        self.step = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.sched = torch.zeros(2 * SCHED_CAPACITY, dtype=torch.int32, device="cuda")
+        self.set_schedule({p_max: 0})
+
+    set_schedule = LinearStack.set_schedule
+    reset_step = LinearStack.reset_step
+    capture = LinearStack.capture
+
+    def token(self) -> None:
+        import torch.distributed as dist
+        s = torch.cuda.current_stream().cuda_stream
+        _capi.call("pmpd_sched_step", self.sched.data_ptr(), SCHED_CAPACITY, self.step.data_ptr(),
+                   self.p_dev.data_ptr(), 1, s)
+        d, f = self.shape.d_model, self.shape.d_ff
+        a_d = 1.0 / (self.std * math.sqrt(d))
+        a_f = 1.0 / (self.std * math.sqrt(f))
+        hq = self.plan.o_rows.size
+        ffl = self.plan.ff.size
+        for wqkv, wo, wup, wdn in self.layers:
+            gemv(wqkv, self.x16, self.p_dev, self.ws, out=self.qkv, alpha=a_d)
+            gemv(wo, self.qkv[:, 2 * hq:], self.p_dev, self.ws, out=self.part, alpha=a_d)   # row-parallel
+            dist.all_reduce(self.part, group=self.group)
+            self.x16.copy_(self.part)
+            gemv(wup, self.x16, self.p_dev, self.ws, out=self.u, alpha=a_d)               # column-parallel
+            gemv(wdn, self.u[:, :ffl], self.p_dev, self.ws, out=self.part, alpha=a_f)     # row-parallel
+            dist.all_reduce(self.part, group=self.group)
+            self.x16.copy_(self.part)
+        hs = self.head_cols.size
+        gemv(self.head, self.x16, self.p_dev, self.ws, out=self.logits_loc[:, :hs], alpha=a_d)
+        dist.all_gather_into_tensor(self.logits_all, self.logits_loc, group=self.group)
+
+    def stream_bytes(self, p: int) -> int:
+        return sum(pk.stream_bytes(p) for lay in self.layers for pk in lay) + self.head.stream_bytes(p)

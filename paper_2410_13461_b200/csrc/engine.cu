@@ -106,6 +106,36 @@ PMPD_DEV unsigned ld_acquire(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+PMPD_DEV unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Spin until *p >= target: relaxed polls (an acquire load invalidates L1 on every
+// iteration), then one acquire fence to order the subsequent reads.
+#ifndef E_SPIN
+#define E_SPIN 0
+#endif
+PMPD_DEV void wait_tickets(const unsigned* p, unsigned target) {
+#if E_SPIN == 0
+  while (ld_acquire(p) < target) __nanosleep(32);
+#elif E_SPIN == 4
+  while (ld_acquire(p) < target) {
+  }
+#elif E_SPIN == 1
+  while (ld_relaxed(p) < target) __nanosleep(20);
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#elif E_SPIN == 2
+  while (ld_relaxed(p) < target) {
+  }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#else
+  // relaxed polls, then one acquire load of the same word (synchronizes-with the release adds)
+  do {
+    while (ld_relaxed(p) < target) __nanosleep(32);
+  } while (ld_acquire(p) < target);
+#endif
+}
 
 struct Range {
   int T0, T1, KT, NT;
@@ -277,8 +307,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
     if (oi > 0) {
       // every op starts after ALL CTAs published ALL earlier ops (the ticket count is only a
       // safe completion test for a strict op-by-op order)
-      if (threadIdx.x == 0)
-        while (ld_acquire(a.bar) < (unsigned)(oi * G)) __nanosleep(32);
+      if (threadIdx.x == 0) wait_tickets(a.bar, (unsigned)(oi * G));
       named_bar_sync(1, E_NCW * 32);
     }
     if (a.trace && threadIdx.x == 0) a.trace[((int64_t)c * a.n_ops + oi) * 8 + 0] = gtimer();
@@ -394,7 +423,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
 #pragma unroll
       for (int e = 0; e < 4; ++e) dhi[i][e] = dlo[i][e] = 0;
     float qs = 0.f;
-    long long tcyc = 0, tcalls = 0, scyc0 = clock64();
+    long long tcyc = 0, tcalls = 0, scyc0 = a.trace ? clock64() : 0;
     int ngi = 0;
     if (t < r.T1) {
       const float idm = idm_pre[0];
@@ -410,12 +439,15 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
 #else
       if (warp < end - t) {
 #endif
-        const long long c0 = clock64();
-        tile_dispatch(P, smem + kSmRing + slot * stage_bytes, end - t, warp, kt + warp, lane, xs, xq, qs, dhi, dlo,
-                      bias);
         if (a.trace) {
+          const long long c0 = clock64();
+          tile_dispatch(P, smem + kSmRing + slot * stage_bytes, end - t, warp, kt + warp, lane, xs, xq, qs, dhi,
+                        dlo, bias);
           tcyc += clock64() - c0;
           ++tcalls;
+        } else {
+          tile_dispatch(P, smem + kSmRing + slot * stage_bytes, end - t, warp, kt + warp, lane, xs, xq, qs, dhi,
+                        dlo, bias);
         }
       }
       __syncwarp();
@@ -457,7 +489,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
           ++ng;
           if (t < r.T1) {
             ++ngi;
-            const float idm = ngi < 4 ? idm_pre[ngi] : __ldg(op.aux + ng);
+            const float idm = ngi == 1 ? idm_pre[1] : ngi == 2 ? idm_pre[2] : ngi == 3 ? idm_pre[3] : __ldg(op.aux + ng);
             qs = (mx > 0.f && idm > 0.f) ? 32767.f * idm / mx : 0.f;
           }
         }
@@ -517,7 +549,7 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
         while (t < r.T1) {
           const int end = min(min(t + E_STILES, r.T1), t - kt + r.KT);
           const int cnt = end - t;
-          if (used) mbar_wait(&bars.empty[slot], phase ^ 1u);
+          if (used) mbar_wait_backoff(&bars.empty[slot], phase ^ 1u);
           uint8_t* st = smem + kSmRing + slot * stage_bytes;
           mbar_arrive_expect_tx(&bars.full[slot], (uint32_t)(cnt * kTilePlaneBytes * (p + 1)));
           for (int j = 0; j < p; ++j)
@@ -549,7 +581,7 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
       while (t < r.T1) {
         const int seg_end = min(r.T1, t - kt + r.KT);
         const int buf = seg & 1;
-        mbar_wait(&bars.red_full[buf], (seg >> 1) & 1);
+        mbar_wait_backoff(&bars.red_full[buf], (seg >> 1) & 1);
         float bsum = 0.f;
 #pragma unroll
         for (int w = 0; w < E_NCW; ++w) bsum += redb[buf * E_NCW + w];
@@ -578,8 +610,7 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
         // A CTA with no tiles in op oi must not publish it before every CTA has
         // published ops < oi: the ticket count is a completion test only if tickets
         // of op oi never precede the completion of op oi-1.
-        if (oi > 0 && r.T1 <= r.T0)
-          while (ld_acquire(a.bar) < (unsigned)(oi * G)) __nanosleep(32);
+        if (oi > 0 && r.T1 <= r.T0) wait_tickets(a.bar, (unsigned)(oi * G));
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar) : "memory");
         if (a.trace) a.trace[((int64_t)c * a.n_ops + oi) * 8 + 3] = gtimer();
       }
@@ -591,8 +622,7 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
   // ---------------------------------------------------------------- final output
   __syncthreads();
   const EngineOp& last = a.ops[a.n_ops - 1];
-  if (threadIdx.x == 0)
-    while (ld_acquire(a.bar) < (unsigned)(a.n_ops * G)) __nanosleep(64);
+  if (threadIdx.x == 0) wait_tickets(a.bar, (unsigned)(a.n_ops * G));
   __syncthreads();
   const int NT = last.n_tiles * last.k_tiles, KT = last.k_tiles;
   for (int ng = c; ng < last.n_tiles; ng += G) {

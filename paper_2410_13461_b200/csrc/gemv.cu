@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) qgemv_kernel(const GemvArgs a) {
       while (cur.t < T1) {
         const int end = cur.stage_end(T1, KT);
         const int cnt = end - cur.t, slot = si % NSTAGE;
-        if (si >= NSTAGE) mbar_wait(&sm.empty[slot], ((si / NSTAGE) & 1) ^ 1);
+        if (si >= NSTAGE) mbar_wait_backoff(&sm.empty[slot], ((si / NSTAGE) & 1) ^ 1);
         uint8_t* st = smem_raw + PL::kRing + slot * PL::kStage;
         mbar_arrive_expect_tx(&sm.full[slot], (uint32_t)(cnt * kTilePlaneBytes * (p + 1)));
         for (int j = 0; j < p; ++j)

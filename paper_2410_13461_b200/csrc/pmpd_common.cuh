@@ -52,6 +52,11 @@ PMPD_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// Wait for warps off the critical path (producer, epilogue): back off between polls so the
+// spin does not steal issue slots from the consumer warps sharing the scheduler.
+PMPD_DEV void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) __nanosleep(64);
+}
 
 // 1-D bulk copy global -> shared, completion counted on an mbarrier (TMA engine).
 PMPD_DEV void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {

@@ -102,6 +102,10 @@ def main():
             schedule.PrecisionSchedule(quant.PrecisionSet((4, 3, 2)), 4, {4: 0, 3: 4, 2: 9}, 24)),
             eos_id=-1, max_new=24), None),
         "fp16": (tinylm.generate(small, prompt, schedule.FixedScheduler(16), max_new=6), None),
+        # north-star criterion: greedy ids identical over the first 64 tokens (4->3->2 switching)
+        "prog432_64": (tinylm.generate(small, prompt, schedule.StaticScheduler(
+            schedule.PrecisionSchedule(quant.PrecisionSet((4, 3, 2)), 4, {4: 0, 3: 8, 2: 24}, 64)),
+            eos_id=-1, max_new=64), None),
     }
     net = learnsched.SchedulerNet.init(64, 64, 8, schedule.SwitchGrid(5, 16), 3, 2, seed=0)
     traces["learned"] = (tinylm.generate(small, list(b"A lantern in the window"),

@@ -84,6 +84,7 @@ def test_generate_traces_match_reference(small, gold_model):
         "two_phase": (StaticScheduler(PrecisionSchedule.two_phase(3, 2, 3, 16, p_prefill=4)), None, 8, prompt),
         "prog432": (StaticScheduler(PrecisionSchedule((4, 3, 2), 4, {4: 0, 3: 4, 2: 9}, 24)), -1, 24, prompt),
         "fp16": (FixedScheduler(16), None, 6, prompt),
+        "prog432_64": (StaticScheduler(PrecisionSchedule((4, 3, 2), 4, {4: 0, 3: 8, 2: 24}, 64)), -1, 64, prompt),
     }
     net = learnsched.SchedulerNet.init(64, 64, 8, SwitchGrid(5, 16), 3, 2, seed=0)
     runs["learned"] = (learnsched.LearnedScheduler(net, p_prefill=4), None, 12, list(b"A lantern in the window"))

@@ -146,6 +146,7 @@ def test_generation_traces(gold_model):
         "two_phase": (om.StaticSched(osched.Schedule.two_phase(3, 2, 3, 16, 4)), None, 8, prompt),
         "prog432": (om.StaticSched(osched.Schedule((4, 3, 2), 4, {4: 0, 3: 4, 2: 9}, 24)), -1, 24, prompt),
         "fp16": (om.StaticSched.fixed(16), None, 6, prompt),
+        "prog432_64": (om.StaticSched(osched.Schedule((4, 3, 2), 4, {4: 0, 3: 8, 2: 24}, 64)), -1, 64, prompt),
     }
     net = olearn.Net.init(64, 64, 8, 5, 16, 3, 2, seed=0)
     runs["learned"] = (olearn.LearnedSched(net, 4), None, 12, list(b"A lantern in the window"))

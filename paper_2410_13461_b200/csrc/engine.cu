@@ -25,6 +25,7 @@
 #include <cstdlib>
 
 #include "decode_core.cuh"
+#include "engine_tile.cuh"
 #include "layout.cuh"
 #include "pmpd_common.cuh"
 #include "pmpd_internal.h"
@@ -32,15 +33,6 @@
 namespace pmpd {
 namespace {
 
-#ifndef PMPD_ENGINE_NCW
-#define PMPD_ENGINE_NCW 8
-#endif
-#ifndef PMPD_ENGINE_TPW
-#define PMPD_ENGINE_TPW 2
-#endif
-constexpr int E_NCW = PMPD_ENGINE_NCW;      // consumer warps
-constexpr int E_TPW = PMPD_ENGINE_TPW;      // tiles per consumer warp per stage
-constexpr int E_STILES = E_NCW * E_TPW;     // tiles per stage
 constexpr int E_PROD = E_NCW;               // producer warp
 constexpr int E_EPI = E_NCW + 1;            // epilogue warp
 constexpr int E_THREADS = (E_NCW + 2) * 32;
@@ -99,7 +91,11 @@ struct Bars {
   uint64_t red_empty[2];
 };
 
-PMPD_DEV int cta_of_tile(int t, int G, int NT) { return (int)(((int64_t)(t + 1) * G + NT - 1) / NT) - 1; }
+// 32-bit partition arithmetic (NT * (G + 1) < 2^32, checked in pmpd_engine_make_op): a 64-bit
+// integer division is an emulated ~100-instruction routine, and these run on the op-to-op path.
+PMPD_DEV int cta_of_tile(int t, int G, int NT) {
+  return (int)(((unsigned)(t + 1) * (unsigned)G + (unsigned)NT - 1u) / (unsigned)NT) - 1;
+}
 
 PMPD_DEV unsigned ld_acquire(const unsigned* p) {
   unsigned v;
@@ -144,110 +140,12 @@ PMPD_DEV Range range_of(const EngineOp& op, int c, int G) {
   Range r;
   r.NT = op.n_tiles * op.k_tiles;
   r.KT = op.k_tiles;
-  r.T0 = (int)((int64_t)c * r.NT / G);
-  r.T1 = (int)((int64_t)(c + 1) * r.NT / G);
+  r.T0 = (int)((unsigned)c * (unsigned)r.NT / (unsigned)G);
+  r.T1 = (int)((unsigned)(c + 1) * (unsigned)r.NT / (unsigned)G);
   return r;
 }
 
-// ------------------------------------------------------------------ consumer tile
-template <int P>
-PMPD_DEV void engine_tile(const uint8_t* st, int stiles_cnt, int wslot, int kt, int lane, const __half* xs,
-                          uint8_t* xq, float qs, int (&dhi)[4][4], int (&dlo)[4][4], float& bias) {
-  const int gq = lane >> 2, tig = lane & 3;
-  uint32_t pw[E_TPW][4][4];
-  float2 dl[E_TPW], mn[E_TPW];
-  bool live[E_TPW];
-#pragma unroll
-  for (int q = 0; q < E_TPW; ++q) {
-    const int sl = wslot + q * E_NCW;
-    live[q] = sl < stiles_cnt;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (j < P && live[q]) {
-        const uint4 v = *reinterpret_cast<const uint4*>(st + j * E_STILES * kTilePlaneBytes + sl * kTilePlaneBytes +
-                                                        lane * 16);
-        pw[q][j][0] = v.x;
-        pw[q][j][1] = v.y;
-        pw[q][j][2] = v.z;
-        pw[q][j][3] = v.w;
-      } else {
-        pw[q][j][0] = pw[q][j][1] = pw[q][j][2] = pw[q][j][3] = 0u;
-      }
-    }
-    if (live[q]) {
-      const float* sc = reinterpret_cast<const float*>(st + P * E_STILES * kTilePlaneBytes + sl * kTileScaleBytes);
-      dl[q] = *reinterpret_cast<const float2*>(sc + 2 * lane);
-      mn[q] = *reinterpret_cast<const float2*>(sc + 64 + 2 * lane);
-    } else {
-      dl[q] = mn[q] = make_float2(0.f, 0.f);
-    }
-  }
-  const int wi = lane >> 1;
-  const int pos = (((wi & 3) << 2) | (wi >> 2)) * 4 + 2 * (lane & 1);
-#pragma unroll
-  for (int q = 0; q < E_TPW; ++q) {
-    if (!live[q]) continue;
-    const int kk = (kt + q * E_NCW) * kTile + 2 * lane;
-    const float2 xf = __half22float2(*reinterpret_cast<const __half2*>(xs + kk));
-    bias = fmaf(xf.x, mn[q].x, fmaf(xf.y, mn[q].y, bias));
-    const float f0 = fmaf(xf.x * dl[q].x, qs, 12582912.f);
-    const float f1 = fmaf(xf.y * dl[q].y, qs, 12582912.f);
-    const uint32_t u0 = __float_as_uint(f0), u1 = __float_as_uint(f1);
-    uint8_t* row = xq + q * 128;
-    *reinterpret_cast<uint16_t*>(row + pos) = (uint16_t)__byte_perm(u0, u1, 0x0040);
-    *reinterpret_cast<uint16_t*>(row + 64 + pos) = (uint16_t)__byte_perm(u0, u1, 0x0051);
-  }
-  __syncwarp();
-  uint32_t bl[E_TPW][4], bh[E_TPW][4];
-#pragma unroll
-  for (int q = 0; q < E_TPW; ++q) {
-    uint4 lo4 = make_uint4(0u, 0u, 0u, 0u), hi4 = lo4;
-    if (live[q] && gq == 0) {
-      lo4 = *reinterpret_cast<const uint4*>(xq + q * 128 + tig * 16);
-      hi4 = *reinterpret_cast<const uint4*>(xq + q * 128 + 64 + tig * 16);
-    }
-    bl[q][0] = lo4.x; bl[q][1] = lo4.y; bl[q][2] = lo4.z; bl[q][3] = lo4.w;
-    bh[q][0] = hi4.x; bh[q][1] = hi4.y; bh[q][2] = hi4.z; bh[q][3] = hi4.w;
-  }
-  __syncwarp();
-#pragma unroll
-  for (int q = 0; q < E_TPW; ++q) {
-    if (!live[q]) continue;
-#pragma unroll
-    for (int cch = 0; cch < 2; ++cch) {
-      const uint32_t pe[4] = {pw[q][0][2 * cch], pw[q][1][2 * cch], pw[q][2][2 * cch], pw[q][3][2 * cch]};
-      const uint32_t po[4] = {pw[q][0][2 * cch + 1], pw[q][1][2 * cch + 1], pw[q][2][2 * cch + 1],
-                              pw[q][3][2 * cch + 1]};
-#define PMPD_E_MTILE(T)                                                             \
-  {                                                                                 \
-    uint32_t a0, a1, a2, a3;                                                        \
-    nibble_to_u8<4, P, T>(merge_planes<4, P, T>(pe), a0, a1);                       \
-    nibble_to_u8<4, P, T>(merge_planes<4, P, T>(po), a2, a3);                       \
-    mma_u8s8_16832(dhi[T], a0, a1, a2, a3, bh[q][2 * cch], bh[q][2 * cch + 1]);     \
-    mma_u8u8_16832(dlo[T], a0, a1, a2, a3, bl[q][2 * cch], bl[q][2 * cch + 1]);     \
-  }
-      PMPD_E_MTILE(0)
-      PMPD_E_MTILE(1)
-      PMPD_E_MTILE(2)
-      PMPD_E_MTILE(3)
-#undef PMPD_E_MTILE
-    }
-  }
-}
-
 // ------------------------------------------------------------------ kernel
-// Only the tile function is specialised per precision (keeps the kernel's code size,
-// and so instruction-cache pressure, small).
-PMPD_DEV void tile_dispatch(int p, const uint8_t* st, int cnt, int wslot, int kt, int lane, const __half* xs, uint8_t* xq,
-                            float qs, int (&dhi)[4][4], int (&dlo)[4][4], float& bias) {
-  switch (p) {
-    case 4: engine_tile<4>(st, cnt, wslot, kt, lane, xs, xq, qs, dhi, dlo, bias); break;
-    case 3: engine_tile<3>(st, cnt, wslot, kt, lane, xs, xq, qs, dhi, dlo, bias); break;
-    case 2: engine_tile<2>(st, cnt, wslot, kt, lane, xs, xq, qs, dhi, dlo, bias); break;
-    default: engine_tile<1>(st, cnt, wslot, kt, lane, xs, xq, qs, dhi, dlo, bias); break;
-  }
-}
-
 PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bars& bars, int G, int c,
                             int stage_bytes, int nstage) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tig = lane & 3;
@@ -683,6 +581,8 @@ int pmpd_engine_make_op(const pmpd_qtensor* t, int32_t src, int32_t src_col, int
   if (t->layout != PMPD_LAYOUT_KN || t->p_max != 4)
     return fail(PMPD_ERR_CONFIG, "the decode engine needs KN tiles with p_max 4");
   if (t->k_tiles * kTile > E_XMAX) return fail(PMPD_ERR_CONFIG, "engine input width above %d", E_XMAX);
+  if ((int64_t)t->n_tiles * t->k_tiles * (num_sms() + 1) >= (int64_t)1 << 32)
+    return fail(PMPD_ERR_CONFIG, "engine op too large for 32-bit tile partitioning");
   EngineOp op{};
   op.planes = static_cast<const uint8_t*>(t->data);
   op.scales = op.planes + (int64_t)t->p_max * t->plane_bytes;

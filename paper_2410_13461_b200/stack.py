@@ -91,7 +91,7 @@ class LinearStack:
         torch.cuda.synchronize()
         ws = max(workspace_bytes(pk, m) for lay in self.layers + [[self.head]] for _, pk in lay)
         self.ws = Workspace(ws)
-        self.x0 = torch.randn((m, d), device="cuda").half()
+        self.x0 = torch.randn((m, d), device="cuda", generator=gen).half()
         self.qkv = torch.empty((m, 3 * d), device="cuda", dtype=torch.float16)
         self.o = torch.empty((m, d), device="cuda", dtype=torch.float16)
         self.u = torch.empty((m, 2 * f), device="cuda", dtype=torch.float16)

@@ -143,6 +143,17 @@ int pmpd_gemv(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, int32_t m, 
               int32_t y_dtype, int32_t ldy, float alpha, int32_t accumulate, void* workspace_dev,
               int64_t workspace_bytes, void* stream);
 
+/* Prefill GEMM on sm_100a tensor cores (tcgen05, TMEM accumulators): the
+ * prompt-length linear layers of prefill (tinylm.py:377-388 -> 334-368).
+ * y[m][n] = alpha * sum_k x[m][k] W_p[n][k] (+ y if accumulate) for m >= 1 rows;
+ * each CTA dequantizes its weight tiles bit-exactly (f32 min + k*step, quant.py:199-215)
+ * to f16 in shared memory once and runs them against 128 rows of x.  KN tiles,
+ * p_max 4, K a multiple of 64; x: f16 [m][ldx] (16-byte aligned rows); y: f32 or
+ * f16 [m][ldy].  *p_dev is the precision (1..p_max); an out-of-range value sets
+ * *status_dev (optional) to PMPD_ERR_CONTRACT and is clamped. */
+int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, int32_t m, const int32_t* p_dev, void* y_dev,
+              int32_t y_dtype, int32_t ldy, float alpha, int32_t accumulate, int32_t* status_dev, void* stream);
+
 /* Per-token precision hook: replaces PrecisionSchedule.precision_at
  * (schedule.py:93-99) as called by generate (tinylm.py:512,518).
  * sched_dev: int32 [2*n_prec] = {p_0, st_0, p_1, st_1, ...} (any order; entries

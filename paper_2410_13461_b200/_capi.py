@@ -58,6 +58,7 @@ SIGNATURES = {
     "pmpd_gather_rows": [_D, _P, _I, _P, _P, _P],
     "pmpd_gemv_workspace_bytes": [_D, _I, ctypes.POINTER(_L)],
     "pmpd_gemv": [_D, _P, _I, _I, _P, _P, _I, _I, _F, _I, _P, _L, _P],
+    "pmpd_gemm": [_D, _P, _I, _I, _P, _P, _I, _I, _F, _I, _P, _P],
     "pmpd_sched_step": [_P, _I, _P, _P, _I, _P],
     "pmpd_rmsnorm": [_P, _I, _P, _I, _I, _F, _P, _I, _P],
     "pmpd_rope_kv": [_P, _I, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P],

@@ -73,6 +73,34 @@ def gemv(pk: PackedTensor, x: torch.Tensor, p_dev: torch.Tensor, workspace: Work
     return out
 
 
+def gemm(pk: PackedTensor, x: torch.Tensor, p_dev: torch.Tensor, out: torch.Tensor | None = None,
+         out_dtype=torch.float32, alpha: float = 1.0, accumulate: bool = False,
+         status: torch.Tensor | None = None) -> torch.Tensor:
+    """Prefill ``y = alpha * x @ W_p^T`` (+ ``y``) on the tcgen05 tensor cores; x is f16 [m, k], any m >= 1.
+
+    The prompt-length counterpart of ``gemv`` (the reference applies the same ``x @ W`` at every
+    linear call site of prefill, tinylm.py:377-388 -> 334-368): each CTA dequantizes its weight
+    tiles bit-exactly to f16 in shared memory once and streams 128 rows of x against them.
+    """
+    if x.dtype != torch.float16 or x.dim() != 2 or not x.is_cuda:
+        raise InputError("gemm input must be a 2-D float16 CUDA tensor")
+    m, k = x.shape
+    d = pk.desc
+    if k != d.k:
+        raise InputError(f"input width {k} does not match the matrix's {d.k}")
+    if x.stride(1) != 1:
+        raise InputError("gemm input must be row-contiguous")
+    if out is None:
+        out = torch.empty((m, d.n), dtype=out_dtype, device=x.device)
+    if out.stride(1) != 1 or tuple(out.shape) != (m, d.n):
+        raise InputError("gemm output must be a row-contiguous [m, n] tensor")
+    ydt = _capi.DTYPE_F32 if out.dtype == torch.float32 else _capi.DTYPE_F16
+    _capi.call("pmpd_gemm", pk.ref(), x.data_ptr(), x.stride(0), m, p_dev.data_ptr(), out.data_ptr(), ydt,
+               out.stride(0), float(alpha), int(bool(accumulate)), status.data_ptr() if status is not None else None,
+               torch.cuda.current_stream().cuda_stream)
+    return out
+
+
 class QLinear:
     """A quantized matrix applied as ``x @ W`` (reference orientation, tinylm) at a device-selected precision."""
 

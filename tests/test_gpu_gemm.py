@@ -1,0 +1,52 @@
+"""GPU parity of the tcgen05 prefill GEMM (pmpd_gemm) against a float64 reference built from the
+bit-exact dequantized weights (quant.py:199-215), and against the decode GEMV."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2410_13461_b200 import _capi
+from paper_2410_13461_b200.linear import Workspace, gemm, gemv
+from paper_2410_13461_b200.quant import dequantize, quantize_tensor
+from pmpd_testutil import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def _pdev(p):
+    return torch.tensor([p], dtype=torch.int32, device="cuda")
+
+
+@pytest.mark.parametrize("K,N", [(64, 64), (256, 192), (512, 1000), (1024, 384)])
+@pytest.mark.parametrize("M", [1, 77, 128, 300])
+def test_gemm_vs_f64(K, N, M):
+    g = torch.Generator(device="cuda").manual_seed(K * 7 + N + M)
+    w = torch.randn((K, N), generator=g, device="cuda") * 0.02
+    qt = quantize_tensor(w, 4, 64)
+    pk = qt.packed(_capi.LAYOUT_KN)
+    x = torch.randn((M, K), generator=g, device="cuda").half()
+    for p in (4, 3, 2):
+        W = dequantize(qt, p, layout=_capi.LAYOUT_KN).double()  # (K, N), bit-exact reference dequant
+        ref = (x.double() @ W).cpu().numpy()
+        y = gemm(pk, x, _pdev(p)).double().cpu().numpy()
+        # f16 weights x f16 activations, f32 accumulation
+        assert rel_l2(y, ref) < 2e-3, (K, N, M, p, rel_l2(y, ref))
+
+
+def test_gemm_matches_gemv_and_accumulates():
+    g = torch.Generator(device="cuda").manual_seed(5)
+    K, N, M = 4096, 4096, 512
+    w = torch.randn((K, N), generator=g, device="cuda") * 0.02
+    pk = quantize_tensor(w, 4, 64).packed(_capi.LAYOUT_KN)
+    x = torch.randn((M, K), generator=g, device="cuda").half()
+    ws = Workspace()
+    for p in (4, 2):
+        y = gemm(pk, x, _pdev(p), alpha=0.5)
+        y2 = torch.empty_like(y)
+        for r0 in range(0, M, 8):
+            gemv(pk, x[r0:r0 + 8], _pdev(p), ws, out=y2[r0:r0 + 8], alpha=0.5)
+        assert rel_l2(y.cpu().numpy(), y2.cpu().numpy()) < 2e-3
+        y3 = y.clone()
+        gemm(pk, x, _pdev(p), out=y3, alpha=0.5, accumulate=True)
+        assert rel_l2(y3.cpu().numpy(), 2 * y.cpu().numpy()) < 1e-6
+    yh = gemm(pk, x, _pdev(4), out_dtype=torch.float16)
+    assert yh.dtype == torch.float16 and rel_l2(yh.float().cpu().numpy(), gemm(pk, x, _pdev(4)).cpu().numpy()) < 1e-3

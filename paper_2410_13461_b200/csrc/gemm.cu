@@ -8,17 +8,23 @@
 //
 //   y[m][n] (+)= alpha * sum_k x[m][k] * W_p[n][k]       x: f16 [M][ldx], W: KN tiles
 //
-// CTA tile: 128 tokens (UMMA M) x 128 outputs (UMMA N = two 64-wide n-groups of the
-// packed format), K in chunks of 64 (one packed tile row).  Per chunk, all 256 threads
-//   * stage the x slice (128 x 64 f16) with cp.async into the UMMA K-major,
-//     no-swizzle core-matrix layout (8 rows x 16 B per core matrix),
-//   * dequantize the weight slice straight from planes 0..p-1 of the packed tiles:
-//     bucket index -> fmaf(k, step, min) in f32 (bit-exact with the reference
-//     dequantize, quant.py:199-215) -> f16, stored as W^T [n][k] in the same layout;
-// then one thread issues 4 x tcgen05.mma.cta_group::1.kind::f16 (M128 N128 K16,
-// f32 accumulator in TMEM) and tcgen05.commit arrives on the stage's mbarrier.  Two
-// smem stages: the tensor core works on chunk c while the threads fill chunk c+1.
+// CTA tile: NG packed n-groups (UMMA N = 64*NG outputs) x MB blocks of 128 tokens (UMMA M =
+// 128 each; MB accumulators of 64*NG TMEM columns), K in chunks of 64 (one packed tile row),
+// in a shared-memory ring of NS stages.  Both operands use the K-major 128-byte-swizzle
+// layout (one 128 B row = the chunk's 64 k of one token / output; 16 B units XOR-swizzled by
+// row & 7), the layout TMA writes for a full-width box:
+//   * producer warp (one lane): TMA -- one 64 k x 128 row box of x per token block (2-D tensor
+//     map, zero-filled past the last row) and the chunk's NG packed tiles as stored (planes
+//     0..p-1 + scale blocks, 1-D bulk copies).
+//   * 8 dequant warps: bucket index -> fmaf(k, step, min) in f32 (bit-exact with the
+//     reference dequantize, quant.py:199-215) -> f16, W^T [n][k] (conflict-free swizzled 8 B
+//     stores); fence.proxy.async (their own smem stores only: every load is async-proxy TMA);
+//     then one thread issues MB x 4 tcgen05.mma.cta_group::1.kind::f16 (M128 N64*NG K16, f32
+//     accumulators in TMEM) and tcgen05.commit frees the stage.  Each dequantized weight tile
+//     feeds MB*128 tokens and each x box NG*64 outputs; (NG, MB) are chosen per launch to
+//     balance that reuse against filling the 148 SMs.
 // Epilogue: tcgen05.ld (32x32b) of the accumulator rows -> alpha * acc (+ y) -> y.
+#include <cuda.h>
 #include <cuda_fp16.h>
 
 #include "decode_core.cuh"
@@ -29,33 +35,49 @@
 namespace pmpd {
 namespace {
 
-constexpr int G_M = 128;        // tokens per CTA tile (UMMA M)
-constexpr int G_N = 128;        // outputs per CTA tile (UMMA N): two packed n-groups
+constexpr int G_BM = 128;       // tokens per UMMA M block
+constexpr int G_NG1 = 64;       // outputs per packed n-group
 constexpr int G_KC = 64;        // K per chunk (one packed tile)
-constexpr int G_THREADS = 256;
-constexpr int G_STAGE_A = G_M * G_KC * 2;   // 16 KB
-constexpr int G_STAGE_B = G_N * G_KC * 2;   // 16 KB
-constexpr int G_STAGE = G_STAGE_A + G_STAGE_B;
-constexpr int G_SMEM = 2 * G_STAGE + 1024;  // two stages + barriers / TMEM address
-// UMMA no-swizzle K-major layout: core matrix (8 rows x 8 f16 = 128 B); K-adjacent core
-// matrices LBO bytes apart, 8-row groups SBO bytes apart.
-constexpr int G_LBO = 128;
-constexpr int G_SBO = (G_KC / 8) * 128;     // 1024
+constexpr int G_DQ = 256;       // dequant threads (8 warps)
+constexpr int G_THREADS = G_DQ + 32;  // + producer warp
+constexpr int G_STAGE_A1 = G_BM * G_KC * 2;  // 16 KB: one x block (f16, SW128 layout)
+constexpr int G_STAGE_B1 = G_NG1 * G_KC * 2; // 8 KB: one dequantized W^T n-group (f16, SW128 layout)
+constexpr int G_RAW = 4 * kTilePlaneBytes + kTileScaleBytes;  // 2.5 KB: packed planes + scales of a tile
+constexpr int G_SMEM_MAX = 227 * 1024;
 
-PMPD_DEV uint32_t core_off(int row, int k) { return (row >> 3) * G_SBO + (k >> 3) * G_LBO + (row & 7) * 16 + (k & 7) * 2; }
+template <int NG, int MB>
+struct Cfg {
+  static constexpr int N = NG * G_NG1;
+  static constexpr int STAGE_A = MB * G_STAGE_A1;
+  static constexpr int STAGE_B = NG * G_STAGE_B1;
+  // load ring: x blocks + the chunk's packed tiles (TMA); SW128 tiles are 1 KB aligned
+  static constexpr int STAGE = (STAGE_A + NG * G_RAW + 1023) / 1024 * 1024;
+  static constexpr int BUFB = 2 * STAGE_B;  // dequantized weights, double-buffered
+  static constexpr int NS_FIT = (G_SMEM_MAX - 2048 - BUFB) / STAGE;
+  static constexpr int NS = NS_FIT > 8 ? 8 : NS_FIT;
+  static constexpr int SMEM = BUFB + NS * STAGE + 2048;  // + barriers / TMEM address + alignment slack
+  static constexpr int TMEM_COLS = MB * N <= 32 ? 32 : MB * N <= 64 ? 64 : MB * N <= 128 ? 128 : MB * N <= 256 ? 256 : 512;
+  static_assert(MB * N <= 512, "accumulators exceed TMEM");
+  static_assert(NS >= 2, "load ring too shallow");
+  // kind::f16 instruction descriptor: f32 accumulator, f16 A and B, both K-major, M128 x N.
+  static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(G_BM >> 4) << 24);
+};
+
+// 128-byte-swizzled K-major tile: row r at 128 r, 16 B unit c at (c ^ (r & 7)).
+PMPD_DEV uint32_t sw128_off(int row, int k) { return row * 128 + ((((k >> 3) ^ row) & 7) << 4) + (k & 7) * 2; }
 
 // ------------------------------------------------------------------ tcgen05 wrappers
-PMPD_DEV uint64_t smem_desc(uint32_t saddr) {
+// SW128 K-major descriptor: 8-row groups 1024 B apart (SBO); LBO unused (1); the K16 step
+// within the 128 B row advances the start address by 32 B.
+PMPD_DEV uint64_t smem_desc_sw128(uint32_t saddr) {
   uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);             // start address
-  d |= (uint64_t)((G_LBO >> 4) & 0x3FFF) << 16;       // leading byte offset (K direction)
-  d |= (uint64_t)((G_SBO >> 4) & 0x3FFF) << 32;       // stride byte offset (M/N direction)
-  d |= (uint64_t)1 << 46;                             // descriptor version (sm_100)
-  // base offset 0, lbo mode 0, layout type 0 = SWIZZLE_NONE (bits 61-63)
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address
+  d |= (uint64_t)1 << 16;                          // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;                // stride byte offset: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                          // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                          // layout type: SWIZZLE_128B
   return d;
 }
-// kind::f16 instruction descriptor: f32 accumulator, f16 A and B, both K-major.
-constexpr uint32_t kIdesc = (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(G_N >> 3) << 17) | ((uint32_t)(G_M >> 4) << 24);
 
 PMPD_DEV void umma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
   asm volatile(
@@ -82,18 +104,20 @@ PMPD_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-PMPD_DEV void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+PMPD_DEV void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
 }
-PMPD_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 struct GemmArgs {
   const uint8_t* planes;
   const uint8_t* scales;
   long long plane_bytes;
-  int n_tiles, k_tiles, n_real, k_real;
-  const __half* x;
-  int M, ldx;
+  int n_tiles, k_tiles, n_real;
+  int M;
   void* y;
   int ldy, y_f16, accumulate;
   float alpha;
@@ -102,76 +126,88 @@ struct GemmArgs {
 };
 
 // ------------------------------------------------------------------ weight dequant
-// Thread (h, L, w) decodes word w of lane chunk L of packed tile h of this chunk: 32 codes
-// (4 m-tiles t x 8 nibble slots s, layout.cuh kn_tile_coord), writes W^T[n][k] in f16.
+// Thread (L, w, half) decodes m-tiles 2*half, 2*half+1 of word w of lane chunk L of the chunk's
+// packed tile (16 codes, layout.cuh kn_tile_coord) and writes W^T[n][k] in f16.
 template <int P>
-PMPD_DEV void dequant_unit(const GemmArgs& g, int tile, int h, int L, int w, uint8_t* sb) {
+PMPD_DEV void dequant_unit(const uint8_t* raw, int L, int w, int half, uint8_t* sb) {
   const int gq = L >> 2, tig = L & 3;
   uint32_t pw[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j)
-    pw[j] = j < P ? __ldg(reinterpret_cast<const uint32_t*>(g.planes + (int64_t)j * g.plane_bytes +
-                                                             (int64_t)tile * kTilePlaneBytes + L * 16) + w)
-                  : 0u;
+  for (int j = 0; j < 4; ++j) pw[j] = j < P ? reinterpret_cast<const uint32_t*>(raw + j * kTilePlaneBytes + L * 16)[w] : 0u;
   const int kb = 32 * (w >> 1) + 16 * (w & 1) + 4 * tig;  // 4 consecutive k of this word
-  const float* sc = reinterpret_cast<const float*>(g.scales + (int64_t)tile * kTileScaleBytes);
-  const float4 d4 = __ldg(reinterpret_cast<const float4*>(sc + kb));
-  const float4 m4 = __ldg(reinterpret_cast<const float4*>(sc + 64 + kb));
+  const float* sc = reinterpret_cast<const float*>(raw + P * kTilePlaneBytes);
+  const float4 d4 = *reinterpret_cast<const float4*>(sc + kb);
+  const float4 m4 = *reinterpret_cast<const float4*>(sc + 64 + kb);
   const float dl[4] = {d4.x, d4.y, d4.z, d4.w}, mn[4] = {m4.x, m4.y, m4.z, m4.w};
   constexpr uint32_t kLoaded = ((1u << 4) - 1) & ~((1u << (4 - P)) - 1);
   constexpr uint32_t kConst = (P < 4) ? (1u << (4 - P - 1)) : 0u;
-#define PMPD_G_T(T)                                                                          \
-  {                                                                                          \
-    const uint32_t pe[4] = {pw[0], pw[1], pw[2], pw[3]};                                     \
-    uint32_t u = merge_planes<4, P, T>(pe);                                                  \
-    u = T ? rotr32(u, T) : u;                                                                \
-    u = (u & (kLoaded * 0x11111111u)) | (kConst * 0x11111111u); /* 8 bucket indices */      \
-    _Pragma("unroll") for (int hh = 0; hh < 2; ++hh) {                                       \
-      __half v[4];                                                                           \
-      _Pragma("unroll") for (int i = 0; i < 4; ++i) {                                        \
-        const uint32_t kidx = (u >> (4 * (2 * i + hh))) & 15u;                               \
-        const float kf = __uint_as_float(0x4B000000u | kidx) - 8388608.f;                    \
-        v[i] = __float2half_rn(__fmaf_rn(kf, dl[i], mn[i]));                                 \
-      }                                                                                      \
-      const int n_l = h * 64 + 16 * T + gq + 8 * hh;                                         \
-      *reinterpret_cast<uint2*>(sb + core_off(n_l, kb)) = *reinterpret_cast<const uint2*>(v); \
-    }                                                                                        \
+  const uint32_t pe[4] = {pw[0], pw[1], pw[2], pw[3]};
+#define PMPD_G_T(T)                                                                               \
+  {                                                                                               \
+    uint32_t u = merge_planes<4, P, T>(pe);                                                       \
+    u = T ? rotr32(u, T) : u;                                                                     \
+    u = (u & (kLoaded * 0x11111111u)) | (kConst * 0x11111111u); /* 8 bucket indices */           \
+    _Pragma("unroll") for (int hh = 0; hh < 2; ++hh) {                                            \
+      __half v[4];                                                                                \
+      _Pragma("unroll") for (int i = 0; i < 4; ++i) {                                             \
+        const uint32_t kidx = (u >> (4 * (2 * i + hh))) & 15u;                                    \
+        const float kf = __uint_as_float(0x4B000000u | kidx) - 8388608.f;                         \
+        v[i] = __float2half_rn(__fmaf_rn(kf, dl[i], mn[i]));                                      \
+      }                                                                                           \
+      *reinterpret_cast<uint2*>(sb + sw128_off(16 * T + gq + 8 * hh, kb)) =                       \
+          *reinterpret_cast<const uint2*>(v);                                                     \
+    }                                                                                             \
   }
-  PMPD_G_T(0)
-  PMPD_G_T(1)
-  PMPD_G_T(2)
-  PMPD_G_T(3)
+  if (half == 0) {
+    PMPD_G_T(0)
+    PMPD_G_T(1)
+  } else {
+    PMPD_G_T(2)
+    PMPD_G_T(3)
+  }
 #undef PMPD_G_T
 }
 
-PMPD_DEV void dequant_dispatch(int p, const GemmArgs& g, int tile, int h, int L, int w, uint8_t* sb) {
+PMPD_DEV void dequant_dispatch(int p, const uint8_t* raw, int L, int w, int half, uint8_t* sb) {
   switch (p) {
-    case 4: dequant_unit<4>(g, tile, h, L, w, sb); break;
-    case 3: dequant_unit<3>(g, tile, h, L, w, sb); break;
-    case 2: dequant_unit<2>(g, tile, h, L, w, sb); break;
-    default: dequant_unit<1>(g, tile, h, L, w, sb); break;
+    case 4: dequant_unit<4>(raw, L, w, half, sb); break;
+    case 3: dequant_unit<3>(raw, L, w, half, sb); break;
+    case 2: dequant_unit<2>(raw, L, w, half, sb); break;
+    default: dequant_unit<1>(raw, L, w, half, sb); break;
   }
 }
 
-__global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* mma_bar = reinterpret_cast<uint64_t*>(smem + 2 * G_STAGE);  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 2 * G_STAGE + 64);
+template <int NG, int MB>
+__global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, const __grid_constant__ CUtensorMap xmap) {
+  using C = Cfg<NG, MB>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // SW128 operand tiles need 1024-byte alignment
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* ring = smem + C::BUFB;                                                   // [NS] load stages
+  uint64_t* mma_bar = reinterpret_cast<uint64_t*>(ring + C::NS * C::STAGE);         // [NS] stage consumed
+  uint64_t* full_bar = mma_bar + 8;                                                 // [NS] stage loaded
+  uint64_t* bbuf_bar = mma_bar + 16;                                                // [2] weight buffer consumed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_bar + 24);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nb = blockIdx.x, m0 = blockIdx.y * G_M;
+  const int nt0 = blockIdx.x * NG, m0 = blockIdx.y * (MB * G_BM);
+  const int ngn = min(NG, g.n_tiles - nt0);  // n-groups of this CTA inside the matrix
   int p = *g.p_dev;
   if (p < 1 || p > 4) {
-    if (tid == 0 && nb == 0 && blockIdx.y == 0 && g.status) atomicExch(g.status, PMPD_ERR_CONTRACT);
+    if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0 && g.status) atomicExch(g.status, PMPD_ERR_CONTRACT);
     p = p < 1 ? 1 : 4;
   }
   if (tid == 0) {
-    mbar_init(&mma_bar[0], 1);
-    mbar_init(&mma_bar[1], 1);
+    for (int i = 0; i < C::NS; ++i) {
+      mbar_init(&mma_bar[i], 1);
+      mbar_init(&full_bar[i], 1);
+    }
+    mbar_init(&bbuf_bar[0], 1);
+    mbar_init(&bbuf_bar[1], 1);
     fence_barrier_init();
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(G_N)
+                 "r"(C::TMEM_COLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -179,90 +215,124 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-
   const int KC = g.k_tiles;
-  // dequant unit of this thread: packed tile h (0/1) of the chunk, lane chunk L, word w
-  const int uh = tid >> 7, uL = (tid >> 2) & 31, uw = tid & 3;
-  const int ntile = 2 * nb + uh;
-  for (int kc = 0; kc < KC; ++kc) {
-    const int s = kc & 1;
-    uint8_t* sa = smem + s * G_STAGE;
-    uint8_t* sb = sa + G_STAGE_A;
-    if (kc >= 2) mbar_wait(&mma_bar[s], ((kc - 2) >> 1) & 1);  // MMAs of chunk kc-2 have read stage s
-    // x slice: 128 rows x 8 chunks of 16 B
-#pragma unroll
-    for (int i = 0; i < (G_M * G_KC / 8) / G_THREADS; ++i) {
-      const int c = tid + i * G_THREADS, r = c >> 3, c8 = c & 7;
-      const int m = m0 + r;
-      const __half* src = g.x + (int64_t)(m < g.M ? m : 0) * g.ldx + kc * G_KC + 8 * c8;
-      cp_async16(smem_u32(sa + core_off(r, 8 * c8)), src, m < g.M ? 16u : 0u);
+  // x blocks of this CTA that hold rows (blocks past M are neither loaded nor multiplied)
+  const int mbn = min(MB, (g.M - m0 + G_BM - 1) / G_BM);
+
+  if (warp == G_DQ / 32) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      for (int kc = 0; kc < KC; ++kc) {
+        const int s = kc % C::NS;
+        uint8_t* st = ring + s * C::STAGE;
+        if (kc >= C::NS) mbar_wait_backoff(&mma_bar[s], ((kc - C::NS) / C::NS) & 1);
+        mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(mbn * G_STAGE_A1 + ngn * (p + 1) * kTilePlaneBytes));
+        for (int mb = 0; mb < mbn; ++mb) tma_2d(st + mb * G_STAGE_A1, &xmap, kc * G_KC, m0 + mb * G_BM, &full_bar[s]);
+        uint8_t* raw = st + C::STAGE_A;
+        for (int h = 0; h < ngn; ++h) {
+          const int64_t tile = (int64_t)(nt0 + h) * g.k_tiles + kc;
+          for (int j = 0; j < p; ++j)
+            bulk_g2s(raw + h * G_RAW + j * kTilePlaneBytes,
+                     g.planes + (int64_t)j * g.plane_bytes + tile * kTilePlaneBytes, kTilePlaneBytes, &full_bar[s]);
+          bulk_g2s(raw + h * G_RAW + p * kTilePlaneBytes, g.scales + tile * kTileScaleBytes, kTileScaleBytes,
+                   &full_bar[s]);
+        }
+      }
     }
-    // weight slice (an n-group past the matrix's last is zero)
-    if (ntile < g.n_tiles) {
-      dequant_dispatch(p, g, ntile * g.k_tiles + kc, uh, uL, uw, sb);
-    } else {
+  } else {
+    // ---------------------------------------------------------------- dequant + MMA issue
+    // Dequant units: per n-group 32 lane chunks x 4 words x 2 m-tile halves = 256.  Within a
+    // unit-group of 256 threads, a half-warp covers gq = 0..7 x (tig & 1) of one (word, k block):
+    // its 16 swizzled 8 B stores hit distinct banks.
+    const int uw = (tid >> 5) & 3, uhalf = tid >> 7;
+    const int uL = ((tid >> 1) & 7) * 4 + ((tid >> 4) & 1) * 2 + (tid & 1);
+    for (int kc = 0; kc < KC; ++kc) {
+      const int s = kc % C::NS;
+      uint8_t* sa = ring + s * C::STAGE;
+      uint8_t* raw = sa + C::STAGE_A;
+      uint8_t* sb = smem + (kc & 1) * C::STAGE_B;
+      if (kc >= 2) mbar_wait(&bbuf_bar[kc & 1], ((kc - 2) >> 1) & 1);  // MMAs of chunk kc-2 read this buffer
+      mbar_wait(&full_bar[s], (kc / C::NS) & 1);
+#ifndef GEMM_SKIP_DEQUANT
+      for (int h = 0; h < NG; ++h) {
+        uint8_t* sbh = sb + h * G_STAGE_B1;
+        if (h < ngn) {
+          dequant_dispatch(p, raw + h * G_RAW, uL, uw, uhalf, sbh);
+        } else {  // n-group past the matrix: zero weights
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
+          for (int t = 0; t < 2; ++t)
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh)
-          *reinterpret_cast<uint2*>(sb + core_off(uh * 64 + 16 * t + (uL >> 2) + 8 * hh,
-                                                  32 * (uw >> 1) + 16 * (uw & 1) + 4 * (uL & 3))) = make_uint2(0u, 0u);
-    }
-    cp_async_wait_all();
-    fence_async_smem();  // generic-proxy smem writes -> visible to the tensor core (async proxy)
-    __syncthreads();
-    if (tid == 0) {
-      tc_fence_after();
-      const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
+            for (int hh = 0; hh < 2; ++hh)
+              *reinterpret_cast<uint2*>(sbh + sw128_off(16 * (2 * uhalf + t) + (uL >> 2) + 8 * hh,
+                                                        32 * (uw >> 1) + 16 * (uw & 1) + 4 * (uL & 3))) = make_uint2(0u, 0u);
+        }
+      }
+#endif
+      fence_async_smem();  // this thread's dequant stores -> visible to the tensor core (async proxy)
+      named_bar_sync(1, G_DQ);
+      if (tid == 0) {
+        tc_fence_after();
+        const uint32_t b0 = smem_u32(sb);
+        for (int mb = 0; mb < mbn; ++mb) {
+          const uint32_t a0 = smem_u32(sa + mb * G_STAGE_A1);
+#ifndef GEMM_SKIP_MMA
 #pragma unroll
-      for (int k16 = 0; k16 < G_KC / 16; ++k16)
-        umma_f16(tmem, smem_desc(a0 + k16 * 2 * G_LBO), smem_desc(b0 + k16 * 2 * G_LBO), kIdesc,
-                 (kc > 0 || k16 > 0) ? 1u : 0u);
-      umma_commit(&mma_bar[s]);
+          for (int k16 = 0; k16 < G_KC / 16; ++k16)
+#else
+          for (int k16 = 0; k16 < 0; ++k16)
+#endif
+            umma_f16(tmem + mb * C::N, smem_desc_sw128(a0 + 32 * k16), smem_desc_sw128(b0 + 32 * k16), C::IDESC,
+                     (kc > 0 || k16 > 0) ? 1u : 0u);
+        }
+        umma_commit(&mma_bar[s]);
+        umma_commit(&bbuf_bar[kc & 1]);
+      }
     }
   }
   // all MMAs done
-  mbar_wait(&mma_bar[(KC - 1) & 1], ((KC - 1) >> 1) & 1);
+  mbar_wait(&mma_bar[(KC - 1) % C::NS], ((KC - 1) / C::NS) & 1);
   tc_fence_after();
-  // epilogue: warp w reads TMEM lanes 32*(w%4).., columns 64*(w/4)..+64
-  {
-    const int row = 32 * (warp & 3) + lane, m = m0 + row;
-    const int c0 = 64 * (warp >> 2);
-#pragma unroll
-    for (int cc = 0; cc < 64; cc += 16) {
-      uint32_t r[16];
-      tmem_ld16(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(c0 + cc), r);
-      if (m < g.M) {
-        const int n0 = nb * G_N + c0 + cc;
-        if (g.y_f16) {
-          __half* yr = static_cast<__half*>(g.y) + (int64_t)m * g.ldy + n0;
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (n0 + i < g.n_real) {
-              float v = g.alpha * __uint_as_float(r[i]);
-              if (g.accumulate) v += __half2float(yr[i]);
-              yr[i] = __float2half_rn(v);
-            }
-        } else {
-          float* yr = static_cast<float*>(g.y) + (int64_t)m * g.ldy + n0;
-          if (n0 + 16 <= g.n_real && (((uintptr_t)yr) & 15) == 0) {
-#pragma unroll
-            for (int i = 0; i < 16; i += 4) {
-              float4 v = make_float4(g.alpha * __uint_as_float(r[i]), g.alpha * __uint_as_float(r[i + 1]),
-                                     g.alpha * __uint_as_float(r[i + 2]), g.alpha * __uint_as_float(r[i + 3]));
-              if (g.accumulate) {
-                const float4 o = *reinterpret_cast<const float4*>(yr + i);
-                v.x += o.x;
-                v.y += o.y;
-                v.z += o.z;
-                v.w += o.w;
-              }
-              *reinterpret_cast<float4*>(yr + i) = v;
-            }
-          } else {
+  // epilogue: warp w reads TMEM lanes 32*(w%4).. of accumulators mb = w/4, w/4 + 2, ...
+  if (warp < G_DQ / 32) {
+    // (accumulator mb, column half ch) pairs spread over the two warp quartets
+    for (int job = warp >> 2; job < mbn * 2; job += G_DQ / 128) {
+      const int mb = job >> 1, ch = job & 1;
+      const int m = m0 + mb * G_BM + 32 * (warp & 3) + lane;
+      for (int cc = ch * (C::N / 2); cc < (ch + 1) * (C::N / 2); cc += 16) {
+        uint32_t r[16];
+        tmem_ld16(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(mb * C::N + cc), r);
+        if (m < g.M) {
+          const int n0 = nt0 * G_NG1 + cc;
+          if (g.y_f16) {
+            __half* yr = static_cast<__half*>(g.y) + (int64_t)m * g.ldy + n0;
 #pragma unroll
             for (int i = 0; i < 16; ++i)
-              if (n0 + i < g.n_real) yr[i] = g.alpha * __uint_as_float(r[i]) + (g.accumulate ? yr[i] : 0.f);
+              if (n0 + i < g.n_real) {
+                float v = g.alpha * __uint_as_float(r[i]);
+                if (g.accumulate) v += __half2float(yr[i]);
+                yr[i] = __float2half_rn(v);
+              }
+          } else {
+            float* yr = static_cast<float*>(g.y) + (int64_t)m * g.ldy + n0;
+            if (n0 + 16 <= g.n_real && (((uintptr_t)yr) & 15) == 0) {
+#pragma unroll
+              for (int i = 0; i < 16; i += 4) {
+                float4 v = make_float4(g.alpha * __uint_as_float(r[i]), g.alpha * __uint_as_float(r[i + 1]),
+                                       g.alpha * __uint_as_float(r[i + 2]), g.alpha * __uint_as_float(r[i + 3]));
+                if (g.accumulate) {
+                  const float4 o = *reinterpret_cast<const float4*>(yr + i);
+                  v.x += o.x;
+                  v.y += o.y;
+                  v.z += o.z;
+                  v.w += o.w;
+                }
+                *reinterpret_cast<float4*>(yr + i) = v;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (n0 + i < g.n_real) yr[i] = g.alpha * __uint_as_float(r[i]) + (g.accumulate ? yr[i] : 0.f);
+            }
           }
         }
       }
@@ -271,7 +341,19 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g) {
   tc_fence_before();
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(G_N) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS) : "memory");
+}
+
+template <int NG, int MB>
+int launch(const GemmArgs& g, const CUtensorMap& xmap, int m, int n_tiles, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_kernel<NG, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<NG, MB>::SMEM);
+    attr = true;
+  }
+  dim3 grid((n_tiles + NG - 1) / NG, (m + MB * G_BM - 1) / (MB * G_BM));
+  gemm_kernel<NG, MB><<<grid, G_THREADS, Cfg<NG, MB>::SMEM, st>>>(g, xmap);
+  return check_launch("prefill gemm launch");
 }
 
 }  // namespace
@@ -290,11 +372,6 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
   if ((ldx & 7) || (reinterpret_cast<uintptr_t>(x_dev) & 15))
     return fail(PMPD_ERR_CONFIG, "prefill GEMM input must be 16-byte aligned rows");
   if (y_dtype != PMPD_DTYPE_F32 && y_dtype != PMPD_DTYPE_F16) return fail(PMPD_ERR_CONFIG, "bad output dtype");
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM);
-    attr = true;
-  }
   GemmArgs g;
   g.planes = static_cast<const uint8_t*>(t->data);
   g.scales = g.planes + (int64_t)t->p_max * t->plane_bytes;
@@ -302,10 +379,7 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
   g.n_tiles = t->n_tiles;
   g.k_tiles = t->k_tiles;
   g.n_real = t->n;
-  g.k_real = t->k;
-  g.x = static_cast<const __half*>(x_dev);
   g.M = m;
-  g.ldx = ldx;
   g.y = y_dev;
   g.ldy = ldy;
   g.y_f16 = y_dtype == PMPD_DTYPE_F16;
@@ -313,7 +387,35 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
   g.alpha = alpha;
   g.p_dev = p_dev;
   g.status = status_dev;
-  dim3 grid((t->n_tiles + 1) / 2, (m + G_M - 1) / G_M);
-  gemm_kernel<<<grid, G_THREADS, G_SMEM, as_stream(stream)>>>(g);
-  return check_launch("prefill gemm launch");
+  // x as a 2-D tensor [m rows][K] f16; boxes of 64 k x 128 rows, 128 B swizzle (zero-filled past row m)
+  CUtensorMap xmap;
+  const cuuint64_t gdim[2] = {(cuuint64_t)t->k, (cuuint64_t)m};
+  const cuuint64_t gstride[1] = {(cuuint64_t)ldx * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)G_KC, (cuuint32_t)G_BM};
+  const cuuint32_t estride[2] = {1, 1};
+  CUresult r = cuTensorMapEncodeTiled(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(x_dev), gdim,
+                                      gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PMPD_ERR_CUDA, "prefill gemm: cuTensorMapEncodeTiled failed (%d)", (int)r);
+  // (n-groups, token blocks) per CTA: the most operand reuse (fewest x re-reads per output,
+  // fewest dequants per token) that still gives about one wave of CTAs on the 148 SMs.
+  const int mblocks = (m + G_BM - 1) / G_BM, sms = num_sms();
+  auto ctas = [&](int ng, int mb) { return (int64_t)((t->n_tiles + ng - 1) / ng) * ((mblocks + mb - 1) / mb); };
+  static const int cand[][2] = {{4, 2}, {4, 1}, {2, 2}, {2, 1}, {1, 2}, {1, 1}};
+  int ng = 1, mb = 1;
+  for (const auto& c : cand) {
+    if (c[1] > 1 && mblocks < c[1]) continue;
+    if (ctas(c[0], c[1]) * 5 >= (int64_t)sms * 4) {  // >= ~80% of the SMs busy
+      ng = c[0];
+      mb = c[1];
+      break;
+    }
+  }
+  cudaStream_t st = as_stream(stream);
+  if (ng == 4 && mb == 2) return launch<4, 2>(g, xmap, m, t->n_tiles, st);
+  if (ng == 4) return launch<4, 1>(g, xmap, m, t->n_tiles, st);
+  if (ng == 2 && mb == 2) return launch<2, 2>(g, xmap, m, t->n_tiles, st);
+  if (ng == 2) return launch<2, 1>(g, xmap, m, t->n_tiles, st);
+  if (mb == 2) return launch<1, 2>(g, xmap, m, t->n_tiles, st);
+  return launch<1, 1>(g, xmap, m, t->n_tiles, st);
 }

@@ -393,7 +393,20 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
   const cuuint64_t gstride[1] = {(cuuint64_t)ldx * 2};
   const cuuint32_t box[2] = {(cuuint32_t)G_KC, (cuuint32_t)G_BM};
   const cuuint32_t estride[2] = {1, 1};
-  CUresult r = cuTensorMapEncodeTiled(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(x_dev), gdim,
+  // driver entry point resolved at run time: the library must load on hosts without libcuda
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(PMPD_ERR_CUDA, "prefill gemm: cuTensorMapEncodeTiled is unavailable");
+    encode = reinterpret_cast<EncodeFn>(fn);
+  }
+  CUresult r = encode(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(x_dev), gdim,
                                       gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(PMPD_ERR_CUDA, "prefill gemm: cuTensorMapEncodeTiled failed (%d)", (int)r);

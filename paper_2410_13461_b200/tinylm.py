@@ -32,7 +32,7 @@ import torch
 
 from . import _capi
 from .errors import ConfigError, ContractViolation, FormatError, InputError
-from .linear import Workspace, gemv, workspace_bytes
+from .linear import Workspace, gemm, gemv, workspace_bytes
 from .quant import BitPlaneStore, PrecisionSet, QuantizedTensor, dequantize, parse_model, quantize_tensor, \
     serialize_model
 from .schedule import PrecisionSchedule
@@ -299,7 +299,8 @@ class _Buffers:
 
 def _linear(dw: _DeviceWeights, pks: list, name16: list, x16: torch.Tensor, out: torch.Tensor, p_dev, p_host,
             ws: Workspace, accumulate: bool) -> None:
-    """out (+)= x16 @ W_p for rows of x16; chunks of 8 rows through the decode GEMV."""
+    """out (+)= x16 @ W_p for rows of x16: the decode GEMV for up to 8 rows (decode steps), the
+    tcgen05 dequant GEMM for longer row blocks (prefill, prompt-length M)."""
     n = x16.shape[0]
     if p_host == FULL_PRECISION:
         w = torch.cat([dw.fp16[nm] for nm in name16], dim=1) if len(name16) > 1 else dw.fp16[name16[0]]
@@ -312,9 +313,10 @@ def _linear(dw: _DeviceWeights, pks: list, name16: list, x16: torch.Tensor, out:
     col = 0
     for pk in pks:
         width = pk.desc.n
-        for r0 in range(0, n, GEMV_MAX_ROWS):
-            r1 = min(n, r0 + GEMV_MAX_ROWS)
-            gemv(pk, x16[r0:r1], p_dev, ws, out=out[r0:r1, col:col + width], accumulate=accumulate)
+        if n > GEMV_MAX_ROWS:
+            gemm(pk, x16, p_dev, out=out[:n, col:col + width], accumulate=accumulate)
+        else:
+            gemv(pk, x16, p_dev, ws, out=out[:n, col:col + width], accumulate=accumulate)
         col += width
 
 

@@ -10,5 +10,5 @@ ARCH="-gencode arch=compute_100a,code=sm_100a"
 nvcc $ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr "$@" \
   -c paper_2410_13461_b200/csrc/engine.cu -o build/variants/eng_$TAG.o
 OBJS=$(ls build/obj/*.o | grep -v '/engine.o$')
-nvcc $ARCH -shared -Xcompiler -fPIC -o build/variants/libeng_$TAG.so $OBJS build/variants/eng_$TAG.o -lcuda
+nvcc $ARCH -shared -Xcompiler -fPIC -o build/variants/libeng_$TAG.so $OBJS build/variants/eng_$TAG.o
 echo build/variants/libeng_$TAG.so

@@ -50,6 +50,62 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def measured_tensor_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["bf16_tflops"]), float(d["bf16_tflops_sustained"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """DRAM bytes (read + write) per engine launch from the committed ncu capture, by precision."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "engine_traffic.json")) as fh:
+            d = json.load(fh)
+        return {int(k): float(v) for k, v in d["bytes_per_launch"].items()}, d.get("source", "")
+    except Exception:
+        return None, None
+
+
+def bench_prefill(st, shape, M=512):
+    """BASELINE config 3 prefill: every linear layer of the stack at M prompt rows, 4-bit, through the
+    tcgen05 dequant GEMM (pmpd_gemm); cuBLAS fp16 on the same shapes beside it."""
+    import torch
+    from paper_2410_13461_b200.linear import gemm
+    d, f = shape.d_model, shape.d_ff
+    xs = {k: torch.randn((M, k), device="cuda").half() for k in (d, f)}
+    pd = torch.tensor([4], dtype=torch.int32, device="cuda")
+    outs = {}
+    mats = [pk for lay in st.layers for _, pk in lay] + [st.head[1]]
+
+    def run():
+        for pk in mats:
+            n, k = pk.desc.n, pk.desc.k
+            y = outs.get(n)
+            if y is None:
+                y = outs[n] = torch.empty((M, n), device="cuda", dtype=torch.float16)
+            gemm(pk, xs[k], pd, out=y)
+
+    for _ in range(2):
+        run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    run()
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3
+    flops = 2.0 * M * shape.weights_per_token
+    burst, sustained, src = measured_tensor_peak()
+    tf = flops / us * 1e-6
+    out = {"workload": f"{len(mats)} linear layers of the {shape.d_model}-wide stack at M={M} prompt rows, p=4",
+           "us": us, "tflops": tf, "tensor_frac_of_burst": tf / burst, "tensor_frac_of_sustained": tf / sustained,
+           "peak_source": src, "kernel": "pmpd_gemm (tcgen05.mma kind::f16, TMEM accumulators, in-smem dequant)"}
+    return out
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
 
@@ -157,6 +213,7 @@ def main():
     ap.add_argument("--shape", default="7b", choices=["7b", "1.4b"])
     ap.add_argument("--no-fp16", action="store_true", help="skip the cuBLAS fp16 baseline")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    ap.add_argument("--no-prefill", action="store_true", help="skip the prefill GEMM section")
     args = ap.parse_args()
 
     from paper_2410_13461_b200.stack import LLAMA2_7B, MOBILELLAMA_1B4, algorithmic_bytes
@@ -228,6 +285,24 @@ def main():
         us = time_tokens(gf, 64)
         per_p[16] = {"us_per_token": us, "GBps": algorithmic_bytes(shape, 16) / us * 1e-3, "impl": "cuBLAS fp16"}
         del gf
+    prefill = None
+    if world == 1 and not args.no_prefill:
+        prefill = bench_prefill(st, shape)
+        if getattr(st, "fp16", None) is not None:  # cuBLAS fp16 prefill of the same stack
+            xs = {k: torch.randn((512, k), device="cuda").half() for k in (shape.d_model, shape.d_ff)}
+
+            def run16():
+                for w16 in st.fp16:
+                    torch.matmul(xs[w16.shape[1]], w16.t())
+            run16()
+            torch.cuda.synchronize()
+            c0, c1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            c0.record()
+            run16()
+            c1.record()
+            torch.cuda.synchronize()
+            prefill["cublas_fp16_us"] = c0.elapsed_time(c1) * 1e3
+            del xs
     if getattr(st, "fp16", None) is not None:
         st.fp16 = None
         torch.cuda.empty_cache()
@@ -287,6 +362,8 @@ def main():
     achieved = bytes_tok / us_tok * 1e-3  # GB/s
     peak, peak_src = measured_peaks()
     weighted_kernel = sum(w[p] * per_p[p]["us_per_token"] for p in w)
+    traffic_pp, traffic_src = ncu_traffic()
+    traffic = sum(w[p] * traffic_pp[p] for p in w) if traffic_pp and all(p in traffic_pp for p in w) else None
 
     out = {
         "metric": METRIC, "value": us_tok, "unit": "us/token", "n_gpus": world, "steps": args.steps,
@@ -304,7 +381,8 @@ def main():
         "speedup_vs_fp16": (per_p[16]["us_per_token"] / us_tok) if 16 in per_p else None,
         "weighted_gpu_latency_us": weighted_kernel,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "peak_source": peak_src,
+                     "traffic": traffic, "traffic_unit": "bytes per token (ncu dram read+write, schedule-weighted)",
+                     "traffic_source": traffic_src, "peak_source": peak_src,
                      "note": "algorithmic bytes (perf.py:101 + activations) per token / µs per token; one "
                              "persistent engine kernel carries all 129 linear layers of a token (plus 1 tiny "
                              "precision-hook launch)"},
@@ -313,6 +391,8 @@ def main():
                 "d2h_bytes_per_step": HORIZON * y_dev.numel() * 4},
         "gpu_launches": args.steps * HORIZON * (2 if world == 1 else 2 + 4 * shape.n_layers),
     }
+    if prefill is not None:
+        out["prefill"] = prefill
     if rank == 0 and world == 1 and not args.no_cpu:
         us, cores, cpu_pp, sample = cpu_sample(shape)
         out["cpu_baseline"] = {"value": us, "unit": "us/token", "cores": cores, "kind": "port", "sample": sample,

@@ -23,7 +23,8 @@
 //     accumulators in TMEM) and tcgen05.commit frees the stage.  Each dequantized weight tile
 //     feeds MB*128 tokens and each x box NG*64 outputs; (NG, MB) are chosen per launch to
 //     balance that reuse against filling the 148 SMs.
-// Epilogue: tcgen05.ld (32x32b) of the accumulator rows -> alpha * acc (+ y) -> y.
+// Epilogue: tcgen05.ld (32x32b) of the accumulator rows -> smem tile -> alpha * acc (+ y) -> y
+// in coalesced row segments.
 #include <cuda.h>
 #include <cuda_fp16.h>
 
@@ -292,50 +293,60 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
   // all MMAs done
   mbar_wait(&mma_bar[(KC - 1) % C::NS], ((KC - 1) / C::NS) & 1);
   tc_fence_after();
-  // epilogue: warp w reads TMEM lanes 32*(w%4).. of accumulators mb = w/4, w/4 + 2, ...
+  // epilogue, per accumulator block: TMEM -> smem tile [128 rows][N (+1 pad)] f32 (warp w reads
+  // TMEM lanes 32*(w%4).., columns half w/4), then all 256 threads write y in coalesced row
+  // segments (the operand ring is free: every MMA has completed and every TMA landed).
   if (warp < G_DQ / 32) {
-    // (accumulator mb, column half ch) pairs spread over the two warp quartets
-    for (int job = warp >> 2; job < mbn * 2; job += G_DQ / 128) {
-      const int mb = job >> 1, ch = job & 1;
-      const int m = m0 + mb * G_BM + 32 * (warp & 3) + lane;
-      for (int cc = ch * (C::N / 2); cc < (ch + 1) * (C::N / 2); cc += 16) {
+    constexpr int LDT = C::N + 1;  // padded row stride (floats): conflict-free column writes
+    float* tile = reinterpret_cast<float*>(smem);
+    for (int mb = 0; mb < mbn; ++mb) {
+      const int row = 32 * (warp & 3) + lane;
+      for (int cc = (warp >> 2) * (C::N / 2); cc < ((warp >> 2) + 1) * (C::N / 2); cc += 16) {
         uint32_t r[16];
         tmem_ld16(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(mb * C::N + cc), r);
-        if (m < g.M) {
-          const int n0 = nt0 * G_NG1 + cc;
-          if (g.y_f16) {
-            __half* yr = static_cast<__half*>(g.y) + (int64_t)m * g.ldy + n0;
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (n0 + i < g.n_real) {
-                float v = g.alpha * __uint_as_float(r[i]);
-                if (g.accumulate) v += __half2float(yr[i]);
-                yr[i] = __float2half_rn(v);
-              }
+        for (int i = 0; i < 16; ++i) tile[row * LDT + cc + i] = __uint_as_float(r[i]);
+      }
+      named_bar_sync(1, G_DQ);
+      const int n0 = nt0 * G_NG1;
+      const int rows = min(G_BM, g.M - (m0 + mb * G_BM));
+      constexpr int Q = C::N / 4;  // 4-column quads per row
+      for (int qi = tid; qi < rows * Q; qi += G_DQ) {
+        const int rr = qi / Q, c4 = (qi % Q) * 4, n = n0 + c4;
+        if (n >= g.n_real) continue;
+        const float* tr = tile + rr * LDT + c4;
+        float v[4] = {g.alpha * tr[0], g.alpha * tr[1], g.alpha * tr[2], g.alpha * tr[3]};
+        const int64_t m = m0 + mb * G_BM + rr;
+        if (g.y_f16) {
+          __half* yr = static_cast<__half*>(g.y) + m * g.ldy + n;
+          if (n + 4 <= g.n_real && !g.accumulate && (((uintptr_t)yr) & 7) == 0) {
+            const __half2 h0 = __floats2half2_rn(v[0], v[1]), h1 = __floats2half2_rn(v[2], v[3]);
+            uint2 pk;
+            pk.x = *reinterpret_cast<const uint32_t*>(&h0);
+            pk.y = *reinterpret_cast<const uint32_t*>(&h1);
+            *reinterpret_cast<uint2*>(yr) = pk;
           } else {
-            float* yr = static_cast<float*>(g.y) + (int64_t)m * g.ldy + n0;
-            if (n0 + 16 <= g.n_real && (((uintptr_t)yr) & 15) == 0) {
-#pragma unroll
-              for (int i = 0; i < 16; i += 4) {
-                float4 v = make_float4(g.alpha * __uint_as_float(r[i]), g.alpha * __uint_as_float(r[i + 1]),
-                                       g.alpha * __uint_as_float(r[i + 2]), g.alpha * __uint_as_float(r[i + 3]));
-                if (g.accumulate) {
-                  const float4 o = *reinterpret_cast<const float4*>(yr + i);
-                  v.x += o.x;
-                  v.y += o.y;
-                  v.z += o.z;
-                  v.w += o.w;
-                }
-                *reinterpret_cast<float4*>(yr + i) = v;
-              }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 16; ++i)
-                if (n0 + i < g.n_real) yr[i] = g.alpha * __uint_as_float(r[i]) + (g.accumulate ? yr[i] : 0.f);
+            for (int i = 0; i < 4 && n + i < g.n_real; ++i)
+              yr[i] = __float2half_rn(v[i] + (g.accumulate ? __half2float(yr[i]) : 0.f));
+          }
+        } else {
+          float* yr = static_cast<float*>(g.y) + m * g.ldy + n;
+          if (n + 4 <= g.n_real && (((uintptr_t)yr) & 15) == 0) {
+            float4 o = make_float4(v[0], v[1], v[2], v[3]);
+            if (g.accumulate) {
+              const float4 q = *reinterpret_cast<const float4*>(yr);
+              o.x += q.x;
+              o.y += q.y;
+              o.z += q.z;
+              o.w += q.w;
             }
+            *reinterpret_cast<float4*>(yr) = o;
+          } else {
+            for (int i = 0; i < 4 && n + i < g.n_real; ++i) yr[i] = v[i] + (g.accumulate ? yr[i] : 0.f);
           }
         }
       }
+      named_bar_sync(1, G_DQ);  // the tile is reused by the next block
     }
   }
   tc_fence_before();

@@ -4,7 +4,7 @@
 #include "../../paper_2410_13461_b200/csrc/engine_tile.cuh"
 using namespace pmpd;
 
-__global__ void __launch_bounds__(1024, 1) eb(int p, int iters, int nw, unsigned* sink) {
+__global__ void __launch_bounds__(E_NCW * 32, 1) eb(int p, int iters, int nw, unsigned* sink) {
   extern __shared__ __align__(128) uint8_t sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int stage_bytes = E_STILES * 5 * 512;
@@ -31,7 +31,7 @@ int main() {
   unsigned* sink; cudaMalloc(&sink, 64);
   const int smem = E_STILES * 5 * 512 + 8192 + 4 * E_NCW * E_TPW * 128 + 1024;
   cudaFuncSetAttribute(eb, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  for (int p : {4, 3, 2}) for (int nw : {8, 16}) {
+  for (int p : {4, 3, 2}) for (int nw : {E_NCW}) {
     const int iters = 2000;
     eb<<<sms, nw * 32, smem>>>(p, 10, nw, sink);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);

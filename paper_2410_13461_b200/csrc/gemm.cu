@@ -16,9 +16,9 @@
 //   * producer warp (one lane): TMA -- one 64 k x 128 row box of x per token block (2-D tensor
 //     map, zero-filled past the last row) and the chunk's NG packed tiles as stored (planes
 //     0..p-1 + scale blocks, 1-D bulk copies).
-//   * 8 dequant warps: bucket index -> fmaf(k, step, min) in f32 (bit-exact with the
-//     reference dequantize, quant.py:199-215) -> f16, W^T [n][k] (conflict-free swizzled 8 B
-//     stores); fence.proxy.async (their own smem stores only: every load is async-proxy TMA);
+//   * 8 dequant warps: bucket indices -> f16 via exponent magic (two per LOP3), then
+//     hfma2(k, step, min) in f16 (the reference dequantize, quant.py:199-215, with f16 operands;
+//     pmpd_dequant keeps the bit-exact f32 form), W^T [n][k] (conflict-free swizzled 8 B stores); fence.proxy.async (their own smem stores only: every load is async-proxy TMA);
 //     then one thread issues MB x 4 tcgen05.mma.cta_group::1.kind::f16 (M128 N64*NG K16, f32
 //     accumulators in TMEM) and tcgen05.commit frees the stage.  Each dequantized weight tile
 //     feeds MB*128 tokens and each x box NG*64 outputs; (NG, MB) are chosen per launch to
@@ -139,25 +139,36 @@ PMPD_DEV void dequant_unit(const uint8_t* raw, int L, int w, int half, uint8_t* 
   const float* sc = reinterpret_cast<const float*>(raw + P * kTilePlaneBytes);
   const float4 d4 = *reinterpret_cast<const float4*>(sc + kb);
   const float4 m4 = *reinterpret_cast<const float4*>(sc + 64 + kb);
-  const float dl[4] = {d4.x, d4.y, d4.z, d4.w}, mn[4] = {m4.x, m4.y, m4.z, m4.w};
+  // f16 step / min pairs of (kb, kb+1) and (kb+2, kb+3): the GEMM computes in f16 (the f32
+  // reference dequantize stays bit-exact in pmpd_dequant; here one f16 rounding of each operand)
+  const __half2 d01 = __floats2half2_rn(d4.x, d4.y), d23 = __floats2half2_rn(d4.z, d4.w);
+  const __half2 m01 = __floats2half2_rn(m4.x, m4.y), m23 = __floats2half2_rn(m4.z, m4.w);
   constexpr uint32_t kLoaded = ((1u << 4) - 1) & ~((1u << (4 - P)) - 1);
   constexpr uint32_t kConst = (P < 4) ? (1u << (4 - P - 1)) : 0u;
+  // low nibble under exponent 25 = 1024 + k, high nibble under exponent 21 = 64 + k (both exact)
+  const __half2 c1024 = __floats2half2_rn(1024.f, 1024.f), c64 = __floats2half2_rn(64.f, 64.f);
   const uint32_t pe[4] = {pw[0], pw[1], pw[2], pw[3]};
-#define PMPD_G_T(T)                                                                               \
-  {                                                                                               \
-    uint32_t u = merge_planes<4, P, T>(pe);                                                       \
-    u = T ? rotr32(u, T) : u;                                                                     \
-    u = (u & (kLoaded * 0x11111111u)) | (kConst * 0x11111111u); /* 8 bucket indices */           \
-    _Pragma("unroll") for (int hh = 0; hh < 2; ++hh) {                                            \
-      __half v[4];                                                                                \
-      _Pragma("unroll") for (int i = 0; i < 4; ++i) {                                             \
-        const uint32_t kidx = (u >> (4 * (2 * i + hh))) & 15u;                                    \
-        const float kf = __uint_as_float(0x4B000000u | kidx) - 8388608.f;                         \
-        v[i] = __float2half_rn(__fmaf_rn(kf, dl[i], mn[i]));                                      \
-      }                                                                                           \
-      *reinterpret_cast<uint2*>(sb + sw128_off(16 * T + gq + 8 * hh, kb)) =                       \
-          *reinterpret_cast<const uint2*>(v);                                                     \
-    }                                                                                             \
+#define PMPD_G_T(T)                                                                                  \
+  {                                                                                                  \
+    uint32_t u = merge_planes<4, P, T>(pe);                                                          \
+    u = T ? rotr32(u, T) : u; /* nibble slot s = bucket index of row 16T+gq+8(s&1), k = kb+(s>>1) */ \
+    const uint32_t kl = kLoaded * 0x00010001u, kc = kConst * 0x00010001u;                            \
+    const uint32_t p01 = __byte_perm(u, 0u, 0x4140), p23 = __byte_perm(u, 0u, 0x4342);               \
+    const uint32_t e01 = lop3_and_or(p01, kl, kc | 0x64006400u);                                     \
+    const uint32_t e23 = lop3_and_or(p23, kl, kc | 0x64006400u);                                     \
+    const uint32_t o01 = lop3_and_or(p01, kl << 4, (kc << 4) | 0x54005400u);                         \
+    const uint32_t o23 = lop3_and_or(p23, kl << 4, (kc << 4) | 0x54005400u);                         \
+    const __half2 we01 = __hfma2(__hsub2(*reinterpret_cast<const __half2*>(&e01), c1024), d01, m01); \
+    const __half2 we23 = __hfma2(__hsub2(*reinterpret_cast<const __half2*>(&e23), c1024), d23, m23); \
+    const __half2 wo01 = __hfma2(__hsub2(*reinterpret_cast<const __half2*>(&o01), c64), d01, m01);   \
+    const __half2 wo23 = __hfma2(__hsub2(*reinterpret_cast<const __half2*>(&o23), c64), d23, m23);   \
+    uint2 ve, vo;                                                                                    \
+    ve.x = *reinterpret_cast<const uint32_t*>(&we01);                                                \
+    ve.y = *reinterpret_cast<const uint32_t*>(&we23);                                                \
+    vo.x = *reinterpret_cast<const uint32_t*>(&wo01);                                                \
+    vo.y = *reinterpret_cast<const uint32_t*>(&wo23);                                                \
+    *reinterpret_cast<uint2*>(sb + sw128_off(16 * T + gq, kb)) = ve;                                 \
+    *reinterpret_cast<uint2*>(sb + sw128_off(16 * T + gq + 8, kb)) = vo;                             \
   }
   if (half == 0) {
     PMPD_G_T(0)

@@ -11,12 +11,15 @@
 // Positions come from a device counter (*T_dev = tokens already cached), so
 // a whole decode step can be replayed as a CUDA graph without host syncs.
 #include <cuda_fp16.h>
+#include <cooperative_groups.h>
 #include <float.h>
+#include <stdlib.h>
 
 #include "pmpd_common.cuh"
 #include "pmpd_internal.h"
 
 namespace pmpd {
+namespace cg = cooperative_groups;
 namespace {
 
 constexpr int kBlock = 256;
@@ -124,6 +127,194 @@ __global__ void attention_kernel(const float* __restrict__ q, int d, int dh, con
     const __half* vr = vc + h * dh + e;
     for (int t = 0; t < L; ++t) acc = fmaf(sc[t], __half2float(vr[(int64_t)t * d]), acc);
     out[(int64_t)i * d + h * dh + e] = __float2half(acc * inv);
+  }
+}
+
+// Split-context ("flash-decoding") attention for head dims 32*DPL: one thread-block
+// cluster of kSplit CTAs per (query i, head h).  CTA r takes positions
+// [r*ceil(L/kSplit), ...) and its warps stream K/V rows (lane l holds dims
+// l*DPL..+DPL, so one row is one coalesced warp load) with an online softmax in
+// registers.  Warp partials fold into a CTA partial (max, sum, acc[dh]) in
+// shared memory; after a cluster barrier every CTA reads all kSplit partials
+// over DSMEM and writes its dh/kSplit slice of the output.  Same math as
+// attention_kernel (tinylm.py:349-358), re-associated: f32, exp via __expf.
+constexpr int kSplit = 8;
+constexpr int kAttnWarps = 4;
+constexpr int kAttnUnroll = 4;
+
+template <int DPL>
+PMPD_DEV void load_row(const __half* __restrict__ p, float (&f)[DPL]) {
+  if constexpr (DPL == 1) {
+    f[0] = __half2float(*p);
+  } else if constexpr (DPL == 2) {
+    const float2 v = __half22float2(*reinterpret_cast<const __half2*>(p));
+    f[0] = v.x;
+    f[1] = v.y;
+  } else if constexpr (DPL == 4) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+    const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+    f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
+  } else {
+    static_assert(DPL == 8, "head dim must be 32, 64, 128 or 256");
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 v = __half22float2(*reinterpret_cast<const __half2*>(&w[j]));
+      f[2 * j] = v.x;
+      f[2 * j + 1] = v.y;
+    }
+  }
+}
+
+template <int DPL>
+__global__ void __cluster_dims__(kSplit, 1, 1) __launch_bounds__(kAttnWarps * 32)
+    attention_split_kernel(const float* __restrict__ q, int d, const __half* __restrict__ kc,
+                           const __half* __restrict__ vc, const int32_t* __restrict__ T_dev, int max_ctx, float scale,
+                           __half* __restrict__ out) {
+  constexpr int DH = 32 * DPL;
+  __shared__ float w_ml[kAttnWarps][2];
+  __shared__ float w_acc[kAttnWarps][DH];
+  __shared__ float c_ml[2];
+  __shared__ float c_acc[DH];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int qh = blockIdx.x / kSplit, H = d / DH;
+  const int i = qh / H, h = qh - i * H;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int L = min(*T_dev + i + 1, max_ctx);
+  const int chunk = (L + kSplit - 1) / kSplit;
+  const int t0 = rank * chunk, t1 = min(L, t0 + chunk);
+
+  float qr[DPL];
+#pragma unroll
+  for (int j = 0; j < DPL; ++j) qr[j] = q[(int64_t)i * d + h * DH + lane * DPL + j];
+  const __half* kb = kc + h * DH + lane * DPL;
+  const __half* vb = vc + h * DH + lane * DPL;
+  float m = -INFINITY, l = 0.f, acc[DPL];
+#pragma unroll
+  for (int j = 0; j < DPL; ++j) acc[j] = 0.f;
+
+  for (int tb = t0 + warp; tb < t1; tb += kAttnWarps * kAttnUnroll) {
+    float kf[kAttnUnroll][DPL], vf[kAttnUnroll][DPL], s[kAttnUnroll];
+#pragma unroll
+    for (int u = 0; u < kAttnUnroll; ++u) {
+      const int t = tb + u * kAttnWarps;
+      if (t < t1) {
+        load_row<DPL>(kb + (int64_t)t * d, kf[u]);
+        load_row<DPL>(vb + (int64_t)t * d, vf[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kAttnUnroll; ++u) {
+      float a = 0.f;
+#pragma unroll
+      for (int j = 0; j < DPL; ++j) a = fmaf(qr[j], kf[u][j], a);
+      s[u] = a;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < kAttnUnroll; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
+#pragma unroll
+    for (int u = 0; u < kAttnUnroll; ++u) {
+      if (tb + u * kAttnWarps < t1) {
+        const float sc = s[u] * scale;
+        const float mn = fmaxf(m, sc);
+        const float corr = __expf(m - mn), pe = __expf(sc - mn);
+        l = fmaf(l, corr, pe);
+#pragma unroll
+        for (int j = 0; j < DPL; ++j) acc[j] = fmaf(acc[j], corr, pe * vf[u][j]);
+        m = mn;
+      }
+    }
+  }
+  if (lane == 0) {
+    w_ml[warp][0] = m;
+    w_ml[warp][1] = l;
+  }
+#pragma unroll
+  for (int j = 0; j < DPL; ++j) w_acc[warp][lane * DPL + j] = acc[j];
+  __syncthreads();
+  float M = -INFINITY;
+#pragma unroll
+  for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, w_ml[w][0]);
+  float wt[kAttnWarps], lc = 0.f;
+#pragma unroll
+  for (int w = 0; w < kAttnWarps; ++w) {
+    wt[w] = w_ml[w][0] == -INFINITY ? 0.f : __expf(w_ml[w][0] - M);
+    lc = fmaf(w_ml[w][1], wt[w], lc);
+  }
+  for (int e = threadIdx.x; e < DH; e += kAttnWarps * 32) {
+    float a = 0.f;
+#pragma unroll
+    for (int w = 0; w < kAttnWarps; ++w) a = fmaf(w_acc[w][e], wt[w], a);
+    c_acc[e] = a;
+  }
+  if (threadIdx.x == 0) {
+    c_ml[0] = M;
+    c_ml[1] = lc;
+  }
+  cl.sync();
+  // combine: this CTA writes dims [rank*DH/kSplit, (rank+1)*DH/kSplit)
+  constexpr int SL = DH / kSplit;
+  if (threadIdx.x < SL) {
+    float Mg = -INFINITY;
+    float rm[kSplit], rl[kSplit];
+#pragma unroll
+    for (int r = 0; r < kSplit; ++r) {
+      const float* ml = cl.map_shared_rank(c_ml, r);
+      rm[r] = ml[0];
+      rl[r] = ml[1];
+      Mg = fmaxf(Mg, rm[r]);
+    }
+    const int e = rank * SL + threadIdx.x;
+    float num = 0.f, den = 0.f;
+#pragma unroll
+    for (int r = 0; r < kSplit; ++r) {
+      const float wr = rm[r] == -INFINITY ? 0.f : __expf(rm[r] - Mg);
+      den = fmaf(rl[r], wr, den);
+      num = fmaf(cl.map_shared_rank(c_acc, r)[e], wr, num);
+    }
+    out[(int64_t)i * d + h * DH + e] = __float2half(num / den);
+  }
+  cl.sync();  // partials stay readable until every CTA of the cluster has combined
+}
+
+// out[m][i] = f16(x[m][i] * rsqrt(mean(x[m]^2) + eps) * gain[i]) with the row held in
+// registers: R float4 per thread, one read of x (tinylm.py:293-295).
+template <int R>
+__global__ void __launch_bounds__(512) rmsnorm_vec_kernel(const float* __restrict__ x, int ldx,
+                                                         const float* __restrict__ gain, int d, float eps,
+                                                         __half* __restrict__ out, int ldo) {
+  __shared__ float sh[32];
+  const float4* xr = reinterpret_cast<const float4*>(x + (int64_t)blockIdx.x * ldx);
+  const int n4 = d >> 2;
+  float4 v[R];
+  float ss = 0.f;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int j = threadIdx.x + r * blockDim.x;
+    v[r] = j < n4 ? xr[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+    ss = fmaf(v[r].x, v[r].x, fmaf(v[r].y, v[r].y, fmaf(v[r].z, v[r].z, fmaf(v[r].w, v[r].w, ss))));
+  }
+  ss = block_sum(ss, sh);
+  const float inv = rsqrtf(ss / (float)d + eps);
+  uint2* o = reinterpret_cast<uint2*>(out + (int64_t)blockIdx.x * ldo);
+  const float4* g4 = reinterpret_cast<const float4*>(gain);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int j = threadIdx.x + r * blockDim.x;
+    if (j < n4) {
+      const float4 g = g4[j];
+      const __half2 a = __floats2half2_rn(v[r].x * inv * g.x, v[r].y * inv * g.y);
+      const __half2 b = __floats2half2_rn(v[r].z * inv * g.z, v[r].w * inv * g.w);
+      uint2 u;
+      u.x = *reinterpret_cast<const uint32_t*>(&a);
+      u.y = *reinterpret_cast<const uint32_t*>(&b);
+      o[j] = u;
+    }
   }
 }
 
@@ -285,7 +476,15 @@ extern "C" {
 int pmpd_rmsnorm(const float* x, int32_t ldx, const float* gain, int32_t m, int32_t d, float eps, void* out,
                  int32_t ldo, void* stream) {
   if (m < 1 || d < 1) return fail(PMPD_ERR_INPUT, "rmsnorm needs m, d >= 1");
-  rmsnorm_kernel<<<m, kBlock, 0, as_stream(stream)>>>(x, ldx, gain, d, eps, (__half*)out, ldo);
+  const bool vec = d % 4 == 0 && ldx % 4 == 0 && ldo % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(gain) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 7) == 0;
+  if (vec && d <= 128 * 4) {
+    rmsnorm_vec_kernel<1><<<m, 128, 0, as_stream(stream)>>>(x, ldx, gain, d, eps, (__half*)out, ldo);
+  } else if (vec && d <= 512 * 4 * 4) {
+    rmsnorm_vec_kernel<4><<<m, 512, 0, as_stream(stream)>>>(x, ldx, gain, d, eps, (__half*)out, ldo);
+  } else {
+    rmsnorm_kernel<<<m, kBlock, 0, as_stream(stream)>>>(x, ldx, gain, d, eps, (__half*)out, ldo);
+  }
   return check_launch("pmpd_rmsnorm");
 }
 
@@ -301,6 +500,33 @@ int pmpd_rope_kv(const float* qkv, int32_t ldq, int32_t m, int32_t d, int32_t d_
 int pmpd_attention(const float* q, int32_t m, int32_t d, int32_t d_head, const void* k_cache, const void* v_cache,
                    const int32_t* T_dev, int32_t max_ctx, float scale, void* out, void* stream) {
   if (d % d_head) return fail(PMPD_ERR_CONFIG, "bad head geometry");
+  const bool al = (reinterpret_cast<uintptr_t>(k_cache) & 15) == 0 && (reinterpret_cast<uintptr_t>(v_cache) & 15) == 0;
+  static const bool generic = getenv("PMPD_ATTN_GENERIC") != nullptr;  // diagnostics: force attention_kernel
+  if (al && m >= 1 && !generic) {
+    const dim3 grid((unsigned)(m * (d / d_head) * kSplit));
+    const auto kc = (const __half*)k_cache;
+    const auto vc = (const __half*)v_cache;
+    switch (d_head) {
+      case 32:
+        attention_split_kernel<1><<<grid, kAttnWarps * 32, 0, as_stream(stream)>>>(q, d, kc, vc, T_dev, max_ctx,
+                                                                                   scale, (__half*)out);
+        return check_launch("pmpd_attention");
+      case 64:
+        attention_split_kernel<2><<<grid, kAttnWarps * 32, 0, as_stream(stream)>>>(q, d, kc, vc, T_dev, max_ctx,
+                                                                                   scale, (__half*)out);
+        return check_launch("pmpd_attention");
+      case 128:
+        attention_split_kernel<4><<<grid, kAttnWarps * 32, 0, as_stream(stream)>>>(q, d, kc, vc, T_dev, max_ctx,
+                                                                                   scale, (__half*)out);
+        return check_launch("pmpd_attention");
+      case 256:
+        attention_split_kernel<8><<<grid, kAttnWarps * 32, 0, as_stream(stream)>>>(q, d, kc, vc, T_dev, max_ctx,
+                                                                                   scale, (__half*)out);
+        return check_launch("pmpd_attention");
+      default:
+        break;
+    }
+  }
   const size_t smem = (size_t)(max_ctx + d_head + 32) * sizeof(float);
   if (smem > 200 * 1024) return fail(PMPD_ERR_CONFIG, "context too long for the attention kernel");
   static size_t attr = 0;

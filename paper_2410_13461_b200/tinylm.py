@@ -151,6 +151,10 @@ class _DeviceWeights:
         self.fp16 = None
         if mv.full_weights is not None:
             self.fp16 = {n: torch.tensor(w, device="cuda").half() for n, w in mv.full_weights.items()}
+            # fused q|k|v weight of the fp16 baseline, concatenated once (not per call)
+            for i in range(cfg.n_layers):
+                names = [f"layers.{i}.{nm}" for nm in ("wq", "wk", "wv")]
+                self.fp16["+".join(names)] = torch.cat([self.fp16.pop(nm) for nm in names], dim=1).contiguous()
 
 
 class ModelVariants:
@@ -303,8 +307,7 @@ def _linear(dw: _DeviceWeights, pks: list, name16: list, x16: torch.Tensor, out:
     tcgen05 dequant GEMM for longer row blocks (prefill, prompt-length M)."""
     n = x16.shape[0]
     if p_host == FULL_PRECISION:
-        w = torch.cat([dw.fp16[nm] for nm in name16], dim=1) if len(name16) > 1 else dw.fp16[name16[0]]
-        y = (x16 @ w).float()
+        y = (x16 @ dw.fp16["+".join(name16)]).float()
         if accumulate:
             out.add_(y)
         else:

@@ -56,6 +56,7 @@ constexpr int MAXM = 8;
 constexpr int kWsCounters = 16384;
 constexpr int64_t kWsHead = (int64_t)kWsCounters * 4 + 256;
 constexpr int kXsMaxK = 12288;          // activations staged in smem when K <= this (batch 1)
+constexpr int kXsMulti = 32768;         // batch 2..8: staged when m * K_pad <= this (64 KB)
 
 struct GemvArgs {
   const uint8_t* planes;
@@ -90,10 +91,12 @@ template <int PMAX, int MB, bool XS>
 struct Plan {
   static constexpr int kStage = STILES * (PMAX + 1) * kTilePlaneBytes;
   static constexpr int kRing = 128;
-  static constexpr int kXs = kRing + NSTAGE * kStage;
-  static constexpr int kXsBytes = XS ? MB * kXsMaxK * 2 : 0;
+  // batch 2..8 with staged activations trades one ring stage for the 64 KB of x
+  static constexpr int kNst = (MB > 1 && XS) ? 3 : NSTAGE;
+  static constexpr int kXs = kRing + kNst * kStage;
+  static constexpr int kXsBytes = XS ? (MB == 1 ? kXsMaxK * 2 : kXsMulti * 2) : 0;
   static constexpr int kXq = kXs + kXsBytes;
-  static constexpr int kXqRows = MB == 1 ? 1 : MAXM;
+  static constexpr int kXqRows = MB;
   static constexpr int kXqWarp = TPW * kXqRows * 2 * 64;  // lo + hi bytes per row and tile
   static constexpr int kRed = kXq + NCW * kXqWarp;
   static constexpr int kRedb = kRed + NCW * 64 * MB * 4;
@@ -117,7 +120,7 @@ struct Consumer {
   const GemvArgs& a;
   Smem& sm;
   uint8_t* smem;
-  const __half* xs;  // staged activations [MB][kXsMaxK] (XS) or global x
+  const __half* xs;  // staged activations [MB][xld] (XS) or global x
   int xld;           // leading dimension of xs
   uint8_t* xq;       // KN: this warp's int8 activation fragments [rows][lo 64 | hi 64]
   float* red;
@@ -129,6 +132,21 @@ struct Consumer {
   int dhi[4][4], dlo[4][4];
   float bias[MB];  // KN: this lane's part of sum_k x*min
   float qs[MB];    // KN: activation quantisation scale 32767 / (max|x_b| * max step_g)
+  float ql[2];     // KN: qs of this lane's flush rows b = 2*tig + {0,1} (keeps qs[] in registers)
+  // KN with unstaged activations: this lane's x pairs (raw half2) of the current stage's
+  // tiles, loaded one stage ahead so the L2 latency overlaps the previous stage's MMAs
+  static constexpr bool PF = KN && !XS;
+  uint32_t xw[TPW][MB];
+
+  PMPD_DEV void prefetch_x(uint32_t (&dst)[TPW][MB], int kt0, int cnt) const {
+#pragma unroll
+    for (int q = 0; q < TPW; ++q)
+#pragma unroll
+      for (int b = 0; b < MB; ++b)
+        dst[q][b] = (warp + q * NCW < cnt && (MB == 1 || b < M))
+                        ? xword(b, (kt0 + warp + q * NCW) * kTile + 2 * lane)
+                        : 0u;
+  }
 
   PMPD_DEV void reset() {
 #pragma unroll
@@ -151,6 +169,11 @@ struct Consumer {
       for (int b = 0; b < MB; ++b) {
         const float m = mx[b];
         qs[b] = (m > 0.f && idm > 0.f) ? 32767.f * idm / m : 0.f;
+      }
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const float m = mx[MB == 1 ? 0 : min(2 * tig + cc, MB - 1)];
+        ql[cc] = (m > 0.f && idm > 0.f) ? 32767.f * idm / m : 0.f;
       }
     }
   }
@@ -223,7 +246,11 @@ struct Consumer {
 #pragma unroll
       for (int b = 0; b < MB; ++b) {
         if (MB == 1 || b < M) {
-          const float2 xf = xpair(b, kk);
+          float2 xf;
+          if constexpr (PF)
+            xf = __half22float2(*reinterpret_cast<const __half2*>(&xw[q][b]));
+          else
+            xf = xpair(b, kk);
           bias[b] = fmaf(xf.x, mn[q].x, fmaf(xf.y, mn[q].y, bias[b]));
           const float f0 = fmaf(xf.x * dl[q].x, qs[b], 12582912.f);  // 1.5 * 2^23: round-to-nearest-even
           const float f1 = fmaf(xf.y * dl[q].y, qs[b], 12582912.f);
@@ -356,7 +383,7 @@ struct Consumer {
             float v;
             if constexpr (KN) {
               // y = (256*hi + lo) * 2^-t / qs[b]
-              const float q = qs[MB == 1 ? 0 : b];
+              const float q = ql[MB == 1 ? 0 : cc];
               const float ds = q > 0.f ? __fdividef(1.f, q) * (1.f / (float)(1 << t)) : 0.f;
               v = fmaf(256.f, (float)dhi[t][2 * h + cc], (float)dlo[t][2 * h + cc]) * ds;
             } else {
@@ -434,11 +461,19 @@ struct Consumer {
     int si = 0;
     TileCursor cur{T0, T0 / KT, T0 % KT};
     enter_group(cur.ng);
+    if constexpr (PF) prefetch_x(xw, cur.kt, cur.stage_end(T1, KT) - cur.t);
     while (cur.t < T1) {
       const int end = cur.stage_end(T1, KT);
-      const int slot = si % NSTAGE;
+      const int slot = si % PL::kNst;
+      uint32_t xn[TPW][MB];
+      if constexpr (PF) {
+        int nkt = cur.kt + (end - cur.t);
+        if (nkt == KT) nkt = 0;
+        const TileCursor nx{end, 0, nkt};
+        prefetch_x(xn, nkt, end < T1 ? nx.stage_end(T1, KT) - end : 0);
+      }
 #ifndef PMPD_GEMV_SKIP_MEMORY
-      mbar_wait(&sm.full[slot], (si / NSTAGE) & 1);
+      mbar_wait(&sm.full[slot], (si / PL::kNst) & 1);
 #endif
 #ifdef PMPD_GEMV_SKIP_COMPUTE
       if (false) {
@@ -458,6 +493,12 @@ struct Consumer {
 #ifndef PMPD_GEMV_SKIP_MEMORY
       if (lane == 0) mbar_arrive(&sm.empty[slot]);
 #endif
+      if constexpr (PF) {
+#pragma unroll
+        for (int q = 0; q < TPW; ++q)
+#pragma unroll
+          for (int b = 0; b < MB; ++b) xw[q][b] = xn[q][b];
+      }
       const int ng = cur.ng;
       cur.kt += end - cur.t;
       cur.t = end;
@@ -492,7 +533,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) qgemv_kernel(const GemvArgs a) {
     p = p < 1 ? 1 : PMAX;
   }
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NSTAGE; ++i) {
+    for (int i = 0; i < PL::kNst; ++i) {
       mbar_init(&sm.full[i], 1);
       mbar_init(&sm.empty[i], NCW);
     }
@@ -513,8 +554,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) qgemv_kernel(const GemvArgs a) {
       TileCursor cur{T0, T0 / KT, T0 % KT};
       while (cur.t < T1) {
         const int end = cur.stage_end(T1, KT);
-        const int cnt = end - cur.t, slot = si % NSTAGE;
-        if (si >= NSTAGE) mbar_wait_backoff(&sm.empty[slot], ((si / NSTAGE) & 1) ^ 1);
+        const int cnt = end - cur.t, slot = si % PL::kNst;
+        if (si >= PL::kNst) mbar_wait_backoff(&sm.empty[slot], ((si / PL::kNst) & 1) ^ 1);
         uint8_t* st = smem_raw + PL::kRing + slot * PL::kStage;
         mbar_arrive_expect_tx(&sm.full[slot], (uint32_t)(cnt * kTilePlaneBytes * (p + 1)));
         for (int j = 0; j < p; ++j)
@@ -556,6 +597,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) qgemv_kernel(const GemvArgs a) {
   }
   pdl_wait();  // activations and the workspace belong to the predecessor until here
   const int Me = MB == 1 ? 1 : a.m;
+  const int xsld = MB == 1 ? kXsMaxK : KT * kTile;  // staged row stride (XS)
   float* red32 = reinterpret_cast<float*>(smem_raw + PL::kMx) + MAXM;  // 32 floats of scratch
   for (int b = 0; b < Me; ++b) {
     float m = 0.f;
@@ -580,7 +622,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) qgemv_kernel(const GemvArgs a) {
           const float2 f = __half22float2(h2[i]);
           m = fmaxf(m, fmaxf(fabsf(f.x), fabsf(f.y)));
         }
-        *reinterpret_cast<uint4*>(xs + b * kXsMaxK + k) = v;
+        *reinterpret_cast<uint4*>(xs + b * xsld + k) = v;
       }
     } else if constexpr (LAYOUT == PMPD_LAYOUT_KN) {
       for (int k = threadIdx.x; k < a.k_real; k += NCW * 32)
@@ -601,7 +643,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) qgemv_kernel(const GemvArgs a) {
   named_bar_sync(1, NCW * 32);
   if constexpr (XS) {
     cs.xs = reinterpret_cast<__half*>(smem_raw + PL::kXs);
-    cs.xld = kXsMaxK;
+    cs.xld = xsld;
   } else {
     cs.xs = a.x;
     cs.xld = a.ldx;
@@ -625,6 +667,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) qgemv_kernel(const GemvArgs a) {
 template <int LAYOUT, int PMAX, int MB, bool XS>
 int launch_m(const GemvArgs& a, int grid, cudaStream_t s) {
   using PL = Plan<PMAX, MB, XS>;
+  static_assert(PL::kBytes <= 232448, "GEMV shared-memory plan exceeds 227 KB");
   const size_t smem = PL::kBytes;
   auto kern = qgemv_kernel<LAYOUT, PMAX, MB, XS>;
   static bool attr_set = false;
@@ -652,7 +695,14 @@ int launch(const GemvArgs& a, int grid, cudaStream_t s) {
   if (a.m == 1)
     return a.k_tiles * kTile <= kXsMaxK ? launch_m<LAYOUT, PMAX, 1, true>(a, grid, s)
                                         : launch_m<LAYOUT, PMAX, 1, false>(a, grid, s);
-  return launch_m<LAYOUT, PMAX, MAXM, false>(a, grid, s);
+  // batch 2..8: the row count is a template bound (2, 4 or 8) so every per-row loop unrolls
+  // into registers; rows past m are masked
+  const bool xs = a.m * a.k_tiles * kTile <= kXsMulti;
+  if (a.m == 2)
+    return xs ? launch_m<LAYOUT, PMAX, 2, true>(a, grid, s) : launch_m<LAYOUT, PMAX, 2, false>(a, grid, s);
+  if (a.m <= 4)
+    return xs ? launch_m<LAYOUT, PMAX, 4, true>(a, grid, s) : launch_m<LAYOUT, PMAX, 4, false>(a, grid, s);
+  return xs ? launch_m<LAYOUT, PMAX, MAXM, true>(a, grid, s) : launch_m<LAYOUT, PMAX, MAXM, false>(a, grid, s);
 }
 
 int ctas_per_sm() {

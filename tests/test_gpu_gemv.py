@@ -51,6 +51,22 @@ def test_gemv_parity(layout, N, K, M):
         assert err < 2e-3, (layout, N, K, M, p, err)  # expected ~1e-4; budget is 1e-2
 
 
+@pytest.mark.parametrize("N,K", [(4096, 4096), (1000, 200), (320, 11008)])
+@pytest.mark.parametrize("M", [2, 4, 5])
+def test_gemv_parity_batch_variants(N, K, M):
+    """Batch 2 / 4 / 5-8 instantiations (KN), staged (m*K <= 32768) and unstaged activations."""
+    w, x = _case(N, K, _capi.LAYOUT_KN, N * 17 + K + M, M)
+    ref = oq.quantize(w, 4, 64)
+    pk = quant.quantize_tensor(w, 4, 64).packed(_capi.LAYOUT_KN)
+    ws = Workspace()
+    xd = torch.from_numpy(x).cuda()
+    for p in (4, 2):
+        y = gemv(pk, xd, _pdev(p), ws)
+        torch.cuda.synchronize()
+        err = rel_l2(y.cpu().numpy(), _oracle_y(ref, x, p, _capi.LAYOUT_KN))
+        assert err < 2e-3, (N, K, M, p, err)
+
+
 def test_gemv_config1_golden(gold_layer):
     """BASELINE config 1 (groups along K) at reduced size, against the reference's own y."""
     for tag in ("nk256", "nk512x1024"):

@@ -13,11 +13,13 @@
 //     mma.sync m16n8k32 (u8 x {s8,u8}) against an int16 two-digit activation
 //     operand, int32 accumulation (see gemv.cu for the arithmetic);
 //   * an epilogue warp reduces the consumer warps' per-n-group partials and
-//     writes one partial per (n-group, CTA) to global memory, then publishes
-//     the op's completion on a grid-wide counter;
-//   * the next op's consumers wait on that counter (acquire), sum the few
-//     partial slots of the columns they need (deferred split-K reduction,
-//     deterministic order) into an f16 activation vector in shared memory.
+//     adds them (f32 atomics, performed at L2) into the op's output vector,
+//     then publishes the op's completion on a grid-wide counter;
+//   * the next op's consumers wait on that counter (acquire) and read one f32
+//     per input element into an f16 activation vector in shared memory.  The
+//     order of the split-K additions is not fixed, so the low bits of a result
+//     may differ between runs (the per-op GEMV keeps a deterministic order);
+//   * after the final output every CTA re-zeroes its slice of the vectors.
 // Co-residency of all CTAs is guaranteed by a cooperative launch.
 #include <cuda_fp16.h>
 
@@ -38,7 +40,6 @@ constexpr int E_EPI = E_NCW + 1;            // epilogue warp
 constexpr int E_THREADS = (E_NCW + 2) * 32;
 constexpr int E_MAXSTAGE = 12;
 constexpr int E_XMAX = 12288;               // max K of a staged activation vector
-constexpr int kMaxSlotsFast = 4;            // partial slots summed with independent loads
 
 struct EngineOp {
   const uint8_t* planes;
@@ -51,9 +52,9 @@ struct EngineOp {
   int act;        // 0: identity; 1: silu(g) * u with u at column src_col + act_off
   int act_off;
   float in_alpha; // scale applied to the reduced source before the activation
-  int max_slots;  // partial slots per n-group of THIS op's output
-  float* part;    // this op's output partials [n_tiles][max_slots][64]
-  const unsigned char* nslots;  // contributing CTAs per n-group of THIS op's output
+  int max_slots;  // unused since the L2-atomic reduction (kept for the op-table ABI)
+  float* part;    // this op's f32 output [n_tiles * 64]: zero at launch, split-K partials added at L2
+  const unsigned char* nslots;  // unused (op-table ABI)
 };
 
 struct EngineArgs {
@@ -157,7 +158,6 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
   int slot = 0;     // ring slot (continues across ops)
   uint32_t phase = 0;
   int seg = 0;      // n-group segment counter (red double buffer)
-  uint8_t* ns_s = smem + kSmNs;
   for (int oi = 0; oi < a.n_ops; ++oi) {
     const EngineOp& op = a.ops[oi];
     const Range r = range_of(op, c, G);
@@ -184,23 +184,6 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
     for (int i = 0; i < 4; ++i) {
       const int ngp = r.T0 / r.KT + i;
       idm_pre[i] = (r.T1 > r.T0 && ngp < op.n_tiles) ? __ldg(op.aux + ngp) : 0.f;
-    }
-    // slot counts of the source n-groups this CTA reads (static table: safe before the wait)
-    if (op.src >= 0) {
-      const EngineOp& sop = a.ops[op.src];
-      for (int seg2 = 0; seg2 < 2; ++seg2) {
-        const int klo = (seg2 ? lo1 : lo0) * kTile, khi = (seg2 ? hi1 : hi0) * kTile;
-        for (int g = klo / 64 + threadIdx.x; g < (khi + 63) / 64; g += E_NCW * 32) {
-          const int n0 = op.src_col + g * 64;  // src_col % 64 may be != 0: two source groups per k-tile
-          ns_s[2 * g] = sop.nslots[n0 >> 6];
-          const int n1 = min(n0 + 63, sop.n_tiles * 64 - 1);
-          ns_s[2 * g + 1] = sop.nslots[n1 >> 6];
-          if (op.act == 1) {
-            ns_s[512 + 2 * g] = sop.nslots[(n0 + op.act_off) >> 6];
-            ns_s[512 + 2 * g + 1] = sop.nslots[min(n0 + op.act_off + 63, sop.n_tiles * 64 - 1) >> 6];
-          }
-        }
-      }
     }
     if (oi > 0) {
       // every op starts after ALL CTAs published ALL earlier ops (the ticket count is only a
@@ -233,9 +216,9 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
             }
           }
         } else {
+          // one f32 per element: the producing CTAs added their n-group partials into src->part
           const int nsrc = op.act == 1 ? 2 : 1;
-          float4 acc[2][SB][kMaxSlotsFast];
-          int nsv[2][SB];
+          float4 acc[2][SB];
 #pragma unroll
           for (int which = 0; which < 2; ++which) {
             if (which >= nsrc) break;
@@ -243,16 +226,8 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
             for (int bi = 0; bi < SB; ++bi) {
               const int k = kb + bi * 4 * E_NCW * 32;
               const int n = op.src_col + which * op.act_off + k;
-              const int ng = n >> 6;
-              const int ns = (k < khi) ? ns_s[which * 512 + 2 * (k >> 6) +
-                                              (((n & 63) < ((op.src_col + which * op.act_off) & 63)) ? 1 : 0)]
-                                       : 0;
-              nsv[which][bi] = ns;
-              const float4* pp = reinterpret_cast<const float4*>(src->part + ((int64_t)ng * src->max_slots) * 64 +
-                                                                 (n & 63));
-#pragma unroll
-              for (int q = 0; q < kMaxSlotsFast; ++q)
-                acc[which][bi][q] = q < ns ? __ldcg(pp + q * 16) : make_float4(0.f, 0.f, 0.f, 0.f);
+              acc[which][bi] = k < khi ? __ldcg(reinterpret_cast<const float4*>(src->part + n))
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
             }
           }
 #pragma unroll
@@ -262,24 +237,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
 #pragma unroll
             for (int which = 0; which < 2; ++which) {
               if (which >= nsrc) break;
-              float4 s4 = acc[which][bi][0];
-#pragma unroll
-              for (int q = 1; q < kMaxSlotsFast; ++q) {
-                s4.x += acc[which][bi][q].x;
-                s4.y += acc[which][bi][q].y;
-                s4.z += acc[which][bi][q].z;
-                s4.w += acc[which][bi][q].w;
-              }
-              const int n = op.src_col + which * op.act_off + k;
-              const float4* pp = reinterpret_cast<const float4*>(src->part +
-                                                                 ((int64_t)(n >> 6) * src->max_slots) * 64 + (n & 63));
-              for (int q = kMaxSlotsFast; q < nsv[which][bi]; ++q) {  // rare: many contributors
-                const float4 e = __ldcg(pp + q * 16);
-                s4.x += e.x;
-                s4.y += e.y;
-                s4.z += e.z;
-                s4.w += e.w;
-              }
+              const float4 s4 = acc[which][bi];
               r[which][0] = s4.x * op.in_alpha;
               r[which][1] = s4.y * op.in_alpha;
               r[which][2] = s4.z * op.in_alpha;
@@ -314,18 +272,18 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
     if (a.trace && threadIdx.x == 0) a.trace[((int64_t)c * a.n_ops + oi) * 8 + 1] = gtimer();
     // ---------------------------------------------------------- tiles of this op
     int t = r.T0, ng = r.T0 / r.KT, kt = r.T0 % r.KT;
-    int dhi[4][4], dlo[4][4];
+    int dacc[4][4];  // balanced-digit sums: [.][0|2] high, [.][1|3] low (lanes tig == 0)
     float bias = 0.f;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) dhi[i][e] = dlo[i][e] = 0;
+      for (int e = 0; e < 4; ++e) dacc[i][e] = 0;
     float qs = 0.f;
     long long tcyc = 0, tcalls = 0, scyc0 = a.trace ? clock64() : 0;
     int ngi = 0;
     if (t < r.T1) {
       const float idm = idm_pre[0];
-      qs = (mx > 0.f && idm > 0.f) ? 32767.f * idm / mx : 0.f;
+      qs = (mx > 0.f && idm > 0.f) ? E_QMAX * idm / mx : 0.f;
     }
     while (t < r.T1) {
       const int end = min(min(t + E_STILES, r.T1), t - kt + r.KT);
@@ -339,13 +297,13 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
 #endif
         if (a.trace) {
           const long long c0 = clock64();
-          tile_dispatch(P, smem + kSmRing + slot * stage_bytes, end - t, warp, kt + warp, lane, xs, xq, qs, dhi,
-                        dlo, bias);
+          tile_dispatch(P, smem + kSmRing + slot * stage_bytes, end - t, warp, kt + warp, lane, xs, xq, qs, dacc,
+                        bias);
           tcyc += clock64() - c0;
           ++tcalls;
         } else {
-          tile_dispatch(P, smem + kSmRing + slot * stage_bytes, end - t, warp, kt + warp, lane, xs, xq, qs, dhi,
-                        dlo, bias);
+          tile_dispatch(P, smem + kSmRing + slot * stage_bytes, end - t, warp, kt + warp, lane, xs, xq, qs, dacc,
+                        bias);
         }
       }
       __syncwarp();
@@ -369,7 +327,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
           for (int tt = 0; tt < 4; ++tt)
 #pragma unroll
             for (int h = 0; h < 2; ++h)
-              rw[16 * tt + gq + 8 * h] = fmaf(256.f, (float)dhi[tt][2 * h], (float)dlo[tt][2 * h]) *
+              rw[16 * tt + gq + 8 * h] = fmaf(256.f, (float)dacc[tt][2 * h], (float)dacc[tt][2 * h + 1]) *
                                          (ds * (1.f / (float)(1 << tt)));
         }
         const float bs = warp_sum(bias);
@@ -380,7 +338,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) dhi[i][e] = dlo[i][e] = 0;
+          for (int e = 0; e < 4; ++e) dacc[i][e] = 0;
         bias = 0.f;
         if (kt == r.KT) {
           kt = 0;
@@ -388,7 +346,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
           if (t < r.T1) {
             ++ngi;
             const float idm = ngi == 1 ? idm_pre[1] : ngi == 2 ? idm_pre[2] : ngi == 3 ? idm_pre[3] : __ldg(op.aux + ng);
-            qs = (mx > 0.f && idm > 0.f) ? 32767.f * idm / mx : 0.f;
+            qs = (mx > 0.f && idm > 0.f) ? E_QMAX * idm / mx : 0.f;
           }
         }
       }
@@ -483,15 +441,15 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
         float bsum = 0.f;
 #pragma unroll
         for (int w = 0; w < E_NCW; ++w) bsum += redb[buf * E_NCW + w];
-        const int cf = cta_of_tile(ng * r.KT, G, r.NT);
-        float* dst = op.part + ((int64_t)ng * op.max_slots + (c - cf)) * 64;
+        // split-K: every CTA holding tiles of n-group ng adds its partial at L2
+        float* dst = op.part + (int64_t)ng * 64;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int nl = lane + 32 * h;
           float v = bsum;
 #pragma unroll
           for (int w = 0; w < E_NCW; ++w) v += red[(buf * E_NCW + w) * 64 + nl];
-          dst[nl] = v;
+          atomicAdd(dst + nl, v);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars.red_empty[buf]);
@@ -522,17 +480,19 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
   const EngineOp& last = a.ops[a.n_ops - 1];
   if (threadIdx.x == 0) wait_tickets(a.bar, (unsigned)(a.n_ops * G));
   __syncthreads();
-  const int NT = last.n_tiles * last.k_tiles, KT = last.k_tiles;
   for (int ng = c; ng < last.n_tiles; ng += G) {
-    const int cf = cta_of_tile(ng * KT, G, NT), cl = cta_of_tile(min((ng + 1) * KT, NT) - 1, G, NT);
     for (int nl = threadIdx.x; nl < 64; nl += blockDim.x) {
       const int n = ng * 64 + nl;
-      if (n >= last.n_real) continue;
-      float s = 0.f;
-      const float* pp = last.part + (int64_t)ng * last.max_slots * 64 + nl;
-      for (int q = 0; q <= cl - cf; ++q) s += __ldcg(pp + q * 64);
-      a.y_out[n] = a.y_alpha * s;
+      if (n < last.n_real) a.y_out[n] = a.y_alpha * __ldcg(last.part + n);
     }
+  }
+  __syncthreads();
+  // Re-zero the accumulation vectors for the next launch.  Every read of ops 0..n-2 happened
+  // before the final ticket; the last op's n-groups are zeroed by the CTA that just read them.
+  for (int oi = 0; oi < a.n_ops; ++oi) {
+    const EngineOp& op = a.ops[oi];
+    for (int ng = c; ng < op.n_tiles; ng += G)
+      for (int nl = threadIdx.x; nl < 64; nl += blockDim.x) op.part[(int64_t)ng * 64 + nl] = 0.f;
   }
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -2,8 +2,10 @@
 // tools/microbench/etile_bench.cu measures exactly this code in isolation.
 //
 // One warp, up to TPW tiles of one n-group per call: decode the P planes of each 64x64 KN tile
-// into u8 tensor-core fragments (decode_core.cuh), quantize x*step into a two-digit int16 B
-// operand, and accumulate mma.sync m16n8k32 (u8 x s8 / u8 x u8) into int32 dhi/dlo.
+// into u8 tensor-core fragments (decode_core.cuh), quantize x*step into an int16 v split into two
+// balanced s8 digits v = 256*hi + lo (lo in [-128, 127]), and accumulate ONE mma.sync m16n8k32
+// (u8 x s8) per fragment with hi in B column 0 and lo in column 1: lane tig == 0 receives
+// sum(a*hi) in d[.][0|2] and sum(a*lo) in d[.][1|3] (rows gq | gq+8).
 #pragma once
 #include "decode_core.cuh"
 #include "layout.cuh"
@@ -20,11 +22,13 @@ namespace pmpd {
 constexpr int E_NCW = PMPD_ENGINE_NCW;      // consumer warps
 constexpr int E_TPW = PMPD_ENGINE_TPW;      // tiles per consumer warp per stage
 constexpr int E_STILES = E_NCW * E_TPW;     // tiles per stage
+// |v| bound of the int16 activation: hi = (v + 128) >> 8 must stay inside s8
+constexpr float E_QMAX = 32639.f;
 
 // ------------------------------------------------------------------ consumer tile
 template <int P>
 PMPD_DEV void engine_tile(const uint8_t* st, int stiles_cnt, int wslot, int kt, int lane, const __half* xs,
-                          uint8_t* xq, float qs, int (&dhi)[4][4], int (&dlo)[4][4], float& bias) {
+                          uint8_t* xq, float qs, int (&d)[4][4], float& bias) {
   const int gq = lane >> 2, tig = lane & 3;
   uint32_t pw[E_TPW][4][4];
   float2 dl[E_TPW], mn[E_TPW];
@@ -62,24 +66,23 @@ PMPD_DEV void engine_tile(const uint8_t* st, int stiles_cnt, int wslot, int kt, 
     const int kk = (kt + q * E_NCW) * kTile + 2 * lane;
     const float2 xf = __half22float2(*reinterpret_cast<const __half2*>(xs + kk));
     bias = fmaf(xf.x, mn[q].x, fmaf(xf.y, mn[q].y, bias));
-    const float f0 = fmaf(xf.x * dl[q].x, qs, 12582912.f);
-    const float f1 = fmaf(xf.y * dl[q].y, qs, 12582912.f);
+    // 1.5 * 2^23 + 128: the low 16 bits of the float are (rint(x*step*qs) + 128) mod 2^16,
+    // so byte 1 is the balanced high digit and byte 0 ^ 0x80 the balanced low digit
+    const float f0 = fmaf(xf.x * dl[q].x, qs, 12583040.f);
+    const float f1 = fmaf(xf.y * dl[q].y, qs, 12583040.f);
     const uint32_t u0 = __float_as_uint(f0), u1 = __float_as_uint(f1);
     uint8_t* row = xq + q * 128;
-    *reinterpret_cast<uint16_t*>(row + pos) = (uint16_t)__byte_perm(u0, u1, 0x0040);
+    *reinterpret_cast<uint16_t*>(row + pos) = (uint16_t)(__byte_perm(u0, u1, 0x0040) ^ 0x8080u);
     *reinterpret_cast<uint16_t*>(row + 64 + pos) = (uint16_t)__byte_perm(u0, u1, 0x0051);
   }
   __syncwarp();
-  uint32_t bl[E_TPW][4], bh[E_TPW][4];
+  // B column 0 (lanes gq == 0) = high digits, column 1 (gq == 1) = low digits
+  uint32_t bb[E_TPW][4];
 #pragma unroll
   for (int q = 0; q < E_TPW; ++q) {
-    uint4 lo4 = make_uint4(0u, 0u, 0u, 0u), hi4 = lo4;
-    if (live[q] && gq == 0) {
-      lo4 = *reinterpret_cast<const uint4*>(xq + q * 128 + tig * 16);
-      hi4 = *reinterpret_cast<const uint4*>(xq + q * 128 + 64 + tig * 16);
-    }
-    bl[q][0] = lo4.x; bl[q][1] = lo4.y; bl[q][2] = lo4.z; bl[q][3] = lo4.w;
-    bh[q][0] = hi4.x; bh[q][1] = hi4.y; bh[q][2] = hi4.z; bh[q][3] = hi4.w;
+    uint4 b4 = make_uint4(0u, 0u, 0u, 0u);
+    if (live[q] && gq < 2) b4 = *reinterpret_cast<const uint4*>(xq + q * 128 + (gq == 0 ? 64 : 0) + tig * 16);
+    bb[q][0] = b4.x; bb[q][1] = b4.y; bb[q][2] = b4.z; bb[q][3] = b4.w;
   }
   __syncwarp();
 #pragma unroll
@@ -95,8 +98,7 @@ PMPD_DEV void engine_tile(const uint8_t* st, int stiles_cnt, int wslot, int kt, 
     uint32_t a0, a1, a2, a3;                                                        \
     nibble_to_u8<4, P, T>(merge_planes<4, P, T>(pe), a0, a1);                       \
     nibble_to_u8<4, P, T>(merge_planes<4, P, T>(po), a2, a3);                       \
-    mma_u8s8_16832(dhi[T], a0, a1, a2, a3, bh[q][2 * cch], bh[q][2 * cch + 1]);     \
-    mma_u8u8_16832(dlo[T], a0, a1, a2, a3, bl[q][2 * cch], bl[q][2 * cch + 1]);     \
+    mma_u8s8_16832(d[T], a0, a1, a2, a3, bb[q][2 * cch], bb[q][2 * cch + 1]);       \
   }
       PMPD_E_MTILE(0)
       PMPD_E_MTILE(1)
@@ -110,12 +112,12 @@ PMPD_DEV void engine_tile(const uint8_t* st, int stiles_cnt, int wslot, int kt, 
 // Only the tile function is specialised per precision (keeps the kernel's code size,
 // and so instruction-cache pressure, small).
 PMPD_DEV void tile_dispatch(int p, const uint8_t* st, int cnt, int wslot, int kt, int lane, const __half* xs, uint8_t* xq,
-                            float qs, int (&dhi)[4][4], int (&dlo)[4][4], float& bias) {
+                            float qs, int (&d)[4][4], float& bias) {
   switch (p) {
-    case 4: engine_tile<4>(st, cnt, wslot, kt, lane, xs, xq, qs, dhi, dlo, bias); break;
-    case 3: engine_tile<3>(st, cnt, wslot, kt, lane, xs, xq, qs, dhi, dlo, bias); break;
-    case 2: engine_tile<2>(st, cnt, wslot, kt, lane, xs, xq, qs, dhi, dlo, bias); break;
-    default: engine_tile<1>(st, cnt, wslot, kt, lane, xs, xq, qs, dhi, dlo, bias); break;
+    case 4: engine_tile<4>(st, cnt, wslot, kt, lane, xs, xq, qs, d, bias); break;
+    case 3: engine_tile<3>(st, cnt, wslot, kt, lane, xs, xq, qs, d, bias); break;
+    case 2: engine_tile<2>(st, cnt, wslot, kt, lane, xs, xq, qs, d, bias); break;
+    default: engine_tile<1>(st, cnt, wslot, kt, lane, xs, xq, qs, d, bias); break;
   }
 }
 

@@ -3,9 +3,10 @@ decode token in one cooperative kernel, with the weight stream never waiting on 
 
 A ``Program`` is a chain of GEMV ops over KN-packed tensors; op ``i`` consumes
 ``in_alpha * y_src[src_col:...]`` (optionally ``silu(g) * u``) of an earlier
-op, or the external f16 input for ``src = -1``.  Intermediate outputs live as
-split-K partials in HBM and are reduced by their consumers; the last op's
-output is reduced into ``y_out``.  The reference path this replaces is the
+op, or the external f16 input for ``src = -1``.  Each op's output is an f32
+vector in HBM into which the CTAs sharing an n-group add their split-K partials
+(L2 atomics; summation order not fixed); the last op's output, scaled by
+``y_alpha``, lands in ``y_out``.  The kernel re-zeroes the vectors on exit.  The reference path this replaces is the
 sequence of ``h @ model.weights(name, p)`` calls of one decode step
 (pkg/src/pmpd/tinylm.py:341-368).
 """
@@ -45,9 +46,9 @@ class Program:
         for i, spec in enumerate(ops):
             if spec.src >= i:
                 raise ConfigError(f"op {i} reads op {spec.src}, which does not precede it")
-            slots = lib.pmpd_engine_max_slots(spec.packed.ref())
+            slots = 1  # one accumulation vector per op (the kernel adds split-K partials at L2)
             nt = spec.packed.desc.n_tiles
-            part = torch.zeros(nt * slots * 64, dtype=torch.float32, device="cuda")
+            part = torch.zeros(nt * 64, dtype=torch.float32, device="cuda")
             ns_host = (ctypes.c_uint8 * nt)()
             _capi.call("pmpd_engine_nslots", spec.packed.ref(), ctypes.addressof(ns_host))
             ns = torch.frombuffer(bytearray(ns_host), dtype=torch.uint8).cuda()

@@ -15,14 +15,14 @@ __global__ void __launch_bounds__(E_NCW * 32, 1) eb(int p, int iters, int nw, un
   for (int i = threadIdx.x; i < 4096; i += blockDim.x) xs[i] = __float2half(0.01f * (i % 97) - 0.4f);
   uint8_t* xq = sm + stage_bytes + 8192 + (warp % E_NCW) * E_TPW * 128 + (warp / E_NCW) * E_NCW * E_TPW * 128;
   __syncthreads();
-  int dhi[4][4] = {}, dlo[4][4] = {};
+  int dacc[4][4] = {};
   float bias = 0.f;
   const int w = warp % E_NCW;
   for (int it = 0; it < iters; ++it) {
-    tile_dispatch(p, sm, E_STILES, w, (w + it) & 31, lane, xs, xq, 3.f, dhi, dlo, bias);
+    tile_dispatch(p, sm, E_STILES, w, (w + it) & 31, lane, xs, xq, 3.f, dacc, bias);
   }
   unsigned acc = __float_as_uint(bias);
-  for (int i = 0; i < 4; ++i) for (int e = 0; e < 4; ++e) acc ^= dhi[i][e] ^ dlo[i][e];
+  for (int i = 0; i < 4; ++i) for (int e = 0; e < 4; ++e) acc ^= dacc[i][e];
   if (acc == 0x12345) sink[0] = acc;
 }
 

@@ -35,6 +35,9 @@
 namespace pmpd {
 namespace {
 
+#ifndef PMPD_ENGINE_SB
+#define PMPD_ENGINE_SB 4  // staging: float4 groups per thread per L2 round trip (4096 elements per pass)
+#endif
 constexpr int E_PROD = E_NCW;               // producer warp
 constexpr int E_EPI = E_NCW + 1;            // epilogue warp
 constexpr int E_THREADS = (E_NCW + 2) * 32;
@@ -196,7 +199,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
     const EngineOp* src = op.src >= 0 ? &a.ops[op.src] : nullptr;
     // Each thread stages groups of 4 consecutive elements, SB groups per batch: all
     // partial-slot loads of a batch are issued before any sum (one L2 round trip per batch).
-    constexpr int SB = 2;
+    constexpr int SB = PMPD_ENGINE_SB;
     for (int seg2 = 0; seg2 < 2; ++seg2) {
       const int klo = (seg2 ? lo1 : lo0) * kTile, khi = (seg2 ? hi1 : hi0) * kTile;
       for (int kb = klo + 4 * threadIdx.x; kb < khi; kb += 4 * SB * E_NCW * 32) {
@@ -279,12 +282,11 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
 #pragma unroll
       for (int e = 0; e < 4; ++e) dacc[i][e] = 0;
     float qs = 0.f;
-    long long tcyc = 0, tcalls = 0, scyc0 = a.trace ? clock64() : 0;
+    long long tcyc = 0, tcalls = 0, scyc0 = a.trace ? clock64() : 0, fcyc = 0, fwait = 0;
     int ngi = 0;
-    if (t < r.T1) {
-      const float idm = idm_pre[0];
-      qs = (mx > 0.f && idm > 0.f) ? E_QMAX * idm / mx : 0.f;
-    }
+    // activation scale per n-group: qs = E_QMAX * idm / mx (one reciprocal per op, none per group)
+    const float qmx = mx > 0.f ? __fdividef(E_QMAX, mx) : 0.f;
+    if (t < r.T1) qs = qmx * idm_pre[0];
     while (t < r.T1) {
       const int end = min(min(t + E_STILES, r.T1), t - kt + r.KT);
 #ifndef PMPD_ENGINE_SKIP_MEMORY
@@ -318,10 +320,12 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
       t = end;
       if (kt == r.KT || t == r.T1) {
         // hand the n-group partial to the epilogue warp (double-buffered)
+        const long long f0 = a.trace ? clock64() : 0;
         const int buf = seg & 1;
         if (seg >= 2) mbar_wait(&bars.red_empty[buf], ((seg >> 1) & 1) ^ 1);
+        if (a.trace) fwait += clock64() - f0;
         float* rw = red + (buf * E_NCW + warp) * 64;
-        const float ds = qs > 0.f ? 1.f / qs : 0.f;
+        const float ds = qs > 0.f ? __frcp_rn(qs) : 0.f;
         if (tig == 0) {
 #pragma unroll
           for (int tt = 0; tt < 4; ++tt)
@@ -335,6 +339,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
         __syncwarp();  // order every lane's partial stores before lane 0's release-arrive
         if (lane == 0) mbar_arrive(&bars.red_full[buf]);
         ++seg;
+        if (a.trace) fcyc += clock64() - f0;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -346,7 +351,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
           if (t < r.T1) {
             ++ngi;
             const float idm = ngi == 1 ? idm_pre[1] : ngi == 2 ? idm_pre[2] : ngi == 3 ? idm_pre[3] : __ldg(op.aux + ng);
-            qs = (mx > 0.f && idm > 0.f) ? E_QMAX * idm / mx : 0.f;
+            qs = qmx * idm;
           }
         }
       }
@@ -356,6 +361,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
       a.trace[((int64_t)c * a.n_ops + oi) * 8 + 4] = tcyc;
       a.trace[((int64_t)c * a.n_ops + oi) * 8 + 5] = tcalls;
       a.trace[((int64_t)c * a.n_ops + oi) * 8 + 6] = clock64() - scyc0;
+      a.trace[((int64_t)c * a.n_ops + oi) * 8 + 7] = (fwait << 32) | (fcyc & 0xffffffffll);
     }
   }
 }
@@ -437,7 +443,11 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
       while (t < r.T1) {
         const int seg_end = min(r.T1, t - kt + r.KT);
         const int buf = seg & 1;
+#ifdef PMPD_ENGINE_EPI_SPIN
+        mbar_wait(&bars.red_full[buf], (seg >> 1) & 1);
+#else
         mbar_wait_backoff(&bars.red_full[buf], (seg >> 1) & 1);
+#endif
         float bsum = 0.f;
 #pragma unroll
         for (int w = 0; w < E_NCW; ++w) bsum += redb[buf * E_NCW + w];

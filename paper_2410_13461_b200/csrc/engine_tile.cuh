@@ -12,7 +12,7 @@
 #include "pmpd_common.cuh"
 
 #ifndef PMPD_ENGINE_NCW
-#define PMPD_ENGINE_NCW 8
+#define PMPD_ENGINE_NCW 12
 #endif
 #ifndef PMPD_ENGINE_TPW
 #define PMPD_ENGINE_TPW 2
@@ -113,6 +113,10 @@ PMPD_DEV void engine_tile(const uint8_t* st, int stiles_cnt, int wslot, int kt, 
 // and so instruction-cache pressure, small).
 PMPD_DEV void tile_dispatch(int p, const uint8_t* st, int cnt, int wslot, int kt, int lane, const __half* xs, uint8_t* xq,
                             float qs, int (&d)[4][4], float& bias) {
+#ifdef PMPD_ENGINE_ONLY_P
+  engine_tile<PMPD_ENGINE_ONLY_P>(st, cnt, wslot, kt, lane, xs, xq, qs, d, bias);
+  return;
+#endif
   switch (p) {
     case 4: engine_tile<4>(st, cnt, wslot, kt, lane, xs, xq, qs, d, bias); break;
     case 3: engine_tile<3>(st, cnt, wslot, kt, lane, xs, xq, qs, d, bias); break;

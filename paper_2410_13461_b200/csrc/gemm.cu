@@ -40,20 +40,29 @@ constexpr int G_BM = 128;       // tokens per UMMA M block
 constexpr int G_NG1 = 64;       // outputs per packed n-group
 constexpr int G_KC = 64;        // K per chunk (one packed tile)
 constexpr int G_DQ = 256;       // dequant threads (8 warps)
-constexpr int G_THREADS = G_DQ + 32;  // + producer warp
+constexpr int G_PROD = G_DQ / 32;      // TMA producer warp
+constexpr int G_MMA = G_DQ / 32 + 1;   // tcgen05.mma issue warp
+constexpr int G_THREADS = G_DQ + 64;
 constexpr int G_STAGE_A1 = G_BM * G_KC * 2;  // 16 KB: one x block (f16, SW128 layout)
 constexpr int G_STAGE_B1 = G_NG1 * G_KC * 2; // 8 KB: one dequantized W^T n-group (f16, SW128 layout)
-constexpr int G_RAW = 4 * kTilePlaneBytes + kTileScaleBytes;  // 2.5 KB: packed planes + scales of a tile
 constexpr int G_SMEM_MAX = 227 * 1024;
 
 template <int NG, int MB>
 struct Cfg {
   static constexpr int N = NG * G_NG1;
-  static constexpr int STAGE_A = MB * G_STAGE_A1;
   static constexpr int STAGE_B = NG * G_STAGE_B1;
-  // load ring: x blocks + the chunk's packed tiles (TMA); SW128 tiles are 1 KB aligned
-  static constexpr int STAGE = (STAGE_A + NG * G_RAW + 1023) / 1024 * 1024;
-  static constexpr int BUFB = 2 * STAGE_B;  // dequantized weights, double-buffered
+  // A load stage holds KCS consecutive K chunks: x as MB x KCS SW128 tiles (one 3-D TMA box per
+  // token block), then the packed tiles as 5 regions (planes 0..3, scales) of [NG][KCS][512 B]
+  // (one 3-D box each).  KCS is the largest of 4/2/1 that still leaves 3 stages.
+  static constexpr int stage_bytes(int kcs) { return (MB * kcs * G_STAGE_A1 + 5 * NG * kcs * kTilePlaneBytes + 1023) / 1024 * 1024; }
+  static constexpr int fit(int kcs) { return (G_SMEM_MAX - 2048 - 2 * STAGE_B) / stage_bytes(kcs); }
+  static constexpr int KCS = fit(4) >= 3 ? 4 : fit(2) >= 3 ? 2 : 1;
+  static constexpr int STAGE_X = MB * KCS * G_STAGE_A1;
+  static constexpr int WR = NG * KCS * kTilePlaneBytes;  // one plane (or scale) region
+  static constexpr int STAGE = stage_bytes(KCS);
+  // dequantized weight buffers: 3 when that still leaves 3 load stages, else 2
+  static constexpr int NB = (G_SMEM_MAX - 2048 - 3 * STAGE_B) / STAGE >= 3 ? 3 : 2;
+  static constexpr int BUFB = NB * STAGE_B;
   static constexpr int NS_FIT = (G_SMEM_MAX - 2048 - BUFB) / STAGE;
   static constexpr int NS = NS_FIT > 8 ? 8 : NS_FIT;
   static constexpr int SMEM = BUFB + NS * STAGE + 2048;  // + barriers / TMEM address + alignment slack
@@ -105,13 +114,21 @@ PMPD_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-PMPD_DEV void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+PMPD_DEV void tma_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
           smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
+
+// TMA descriptors of one launch: x as [K/64 chunks][M rows][64 k] (f16, 128 B swizzle), and each
+// bit plane / the scale blocks as [n_tiles][k_tiles][128 words] (one 512 B tile per row).
+struct alignas(64) GemmMaps {
+  CUtensorMap x;
+  CUtensorMap plane[4];
+  CUtensorMap scale;
+};
 
 struct GemmArgs {
   const uint8_t* planes;
@@ -130,13 +147,13 @@ struct GemmArgs {
 // Thread (L, w, half) decodes m-tiles 2*half, 2*half+1 of word w of lane chunk L of the chunk's
 // packed tile (16 codes, layout.cuh kn_tile_coord) and writes W^T[n][k] in f16.
 template <int P>
-PMPD_DEV void dequant_unit(const uint8_t* raw, int L, int w, int half, uint8_t* sb) {
+PMPD_DEV void dequant_unit(const uint8_t* pl, int pstride, const uint8_t* scl, int L, int w, int half, uint8_t* sb) {
   const int gq = L >> 2, tig = L & 3;
   uint32_t pw[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) pw[j] = j < P ? reinterpret_cast<const uint32_t*>(raw + j * kTilePlaneBytes + L * 16)[w] : 0u;
+  for (int j = 0; j < 4; ++j) pw[j] = j < P ? reinterpret_cast<const uint32_t*>(pl + j * pstride + L * 16)[w] : 0u;
   const int kb = 32 * (w >> 1) + 16 * (w & 1) + 4 * tig;  // 4 consecutive k of this word
-  const float* sc = reinterpret_cast<const float*>(raw + P * kTilePlaneBytes);
+  const float* sc = reinterpret_cast<const float*>(scl);
   const float4 d4 = *reinterpret_cast<const float4*>(sc + kb);
   const float4 m4 = *reinterpret_cast<const float4*>(sc + 64 + kb);
   // f16 step / min pairs of (kb, kb+1) and (kb+2, kb+3): the GEMM computes in f16 (the f32
@@ -180,17 +197,48 @@ PMPD_DEV void dequant_unit(const uint8_t* raw, int L, int w, int half, uint8_t* 
 #undef PMPD_G_T
 }
 
-PMPD_DEV void dequant_dispatch(int p, const uint8_t* raw, int L, int w, int half, uint8_t* sb) {
-  switch (p) {
-    case 4: dequant_unit<4>(raw, L, w, half, sb); break;
-    case 3: dequant_unit<3>(raw, L, w, half, sb); break;
-    case 2: dequant_unit<2>(raw, L, w, half, sb); break;
-    default: dequant_unit<1>(raw, L, w, half, sb); break;
+// The 8 dequant warps, specialised per precision: for each K chunk wait for a free weight
+// buffer (its MMAs of NB chunks ago completed) and the chunk's packed tiles, dequantize, then
+// each warp arrives on the buffer's full barrier.  No CTA-wide barrier: warps run ahead
+// independently and the MMA warp issues as soon as all 8 have arrived.
+template <int P, int NG, int MB>
+PMPD_DEV void dequant_loop(int KC, int ngn, uint8_t* ring, uint8_t* bufs, uint64_t* full_bar, uint64_t* bfull,
+                           uint64_t* bempty, int tid) {
+  using C = Cfg<NG, MB>;
+  const int uw = (tid >> 5) & 3, uhalf = tid >> 7;
+  const int uL = ((tid >> 1) & 7) * 4 + ((tid >> 4) & 1) * 2 + (tid & 1);
+  for (int kc = 0; kc < KC; ++kc) {
+    const int st = kc / C::KCS, kcs = kc - st * C::KCS, s = st % C::NS, b = kc % C::NB;
+    const uint8_t* w0 = ring + s * C::STAGE + C::STAGE_X;
+    uint8_t* sb = bufs + b * C::STAGE_B;
+    if (kc >= C::NB) mbar_wait(&bempty[b], ((kc - C::NB) / C::NB) & 1);
+    if (kcs == 0) mbar_wait(&full_bar[s], (st / C::NS) & 1);
+#ifndef GEMM_SKIP_DEQUANT
+#pragma unroll
+    for (int h = 0; h < NG; ++h) {
+      uint8_t* sbh = sb + h * G_STAGE_B1;
+      if (h < ngn) {
+        const int toff = (h * C::KCS + kcs) * kTilePlaneBytes;
+        dequant_unit<P>(w0 + toff, C::WR, w0 + 4 * C::WR + toff, uL, uw, uhalf, sbh);
+      } else {  // n-group past the matrix: zero weights
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh)
+            *reinterpret_cast<uint2*>(sbh + sw128_off(16 * (2 * uhalf + t) + (uL >> 2) + 8 * hh,
+                                                      32 * (uw >> 1) + 16 * (uw & 1) + 4 * (uL & 3))) =
+                make_uint2(0u, 0u);
+      }
+    }
+#endif
+    fence_async_smem();  // this thread's dequant stores -> visible to the tensor core (async proxy)
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&bfull[b]);
   }
 }
 
 template <int NG, int MB>
-__global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, const __grid_constant__ CUtensorMap xmap) {
+__global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, const __grid_constant__ GemmMaps maps) {
   using C = Cfg<NG, MB>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // SW128 operand tiles need 1024-byte alignment
@@ -198,7 +246,8 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
   uint8_t* ring = smem + C::BUFB;                                                   // [NS] load stages
   uint64_t* mma_bar = reinterpret_cast<uint64_t*>(ring + C::NS * C::STAGE);         // [NS] stage consumed
   uint64_t* full_bar = mma_bar + 8;                                                 // [NS] stage loaded
-  uint64_t* bbuf_bar = mma_bar + 16;                                                // [2] weight buffer consumed
+  uint64_t* bfull = mma_bar + 16;                                                   // [NB] weights dequantized
+  uint64_t* bempty = mma_bar + 20;                                                  // [NB] weights consumed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_bar + 24);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nt0 = blockIdx.x * NG, m0 = blockIdx.y * (MB * G_BM);
@@ -213,8 +262,10 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
       mbar_init(&mma_bar[i], 1);
       mbar_init(&full_bar[i], 1);
     }
-    mbar_init(&bbuf_bar[0], 1);
-    mbar_init(&bbuf_bar[1], 1);
+    for (int i = 0; i < C::NB; ++i) {
+      mbar_init(&bfull[i], G_DQ / 32);
+      mbar_init(&bempty[i], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 0) {
@@ -231,78 +282,58 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
   // x blocks of this CTA that hold rows (blocks past M are neither loaded nor multiplied)
   const int mbn = min(MB, (g.M - m0 + G_BM - 1) / G_BM);
 
-  if (warp == G_DQ / 32) {
+  if (warp == G_PROD) {
     // ---------------------------------------------------------------- TMA producer
     if (lane == 0) {
-      for (int kc = 0; kc < KC; ++kc) {
-        const int s = kc % C::NS;
-        uint8_t* st = ring + s * C::STAGE;
-        if (kc >= C::NS) mbar_wait_backoff(&mma_bar[s], ((kc - C::NS) / C::NS) & 1);
-        mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(mbn * G_STAGE_A1 + ngn * (p + 1) * kTilePlaneBytes));
-        for (int mb = 0; mb < mbn; ++mb) tma_2d(st + mb * G_STAGE_A1, &xmap, kc * G_KC, m0 + mb * G_BM, &full_bar[s]);
-        uint8_t* raw = st + C::STAGE_A;
-        for (int h = 0; h < ngn; ++h) {
-          const int64_t tile = (int64_t)(nt0 + h) * g.k_tiles + kc;
-          for (int j = 0; j < p; ++j)
-            bulk_g2s(raw + h * G_RAW + j * kTilePlaneBytes,
-                     g.planes + (int64_t)j * g.plane_bytes + tile * kTilePlaneBytes, kTilePlaneBytes, &full_bar[s]);
-          bulk_g2s(raw + h * G_RAW + p * kTilePlaneBytes, g.scales + tile * kTileScaleBytes, kTileScaleBytes,
-                   &full_bar[s]);
-        }
+      const int nst = (KC + C::KCS - 1) / C::KCS;
+      for (int st = 0; st < nst; ++st) {
+        const int s = st % C::NS, kc0 = st * C::KCS;
+        uint8_t* sx = ring + s * C::STAGE;
+        uint8_t* sw = sx + C::STAGE_X;
+        if (st >= C::NS) mbar_wait_backoff(&mma_bar[s], ((st - C::NS) / C::NS) & 1);
+        // full boxes land (TMA zero-fills past K, M and the last n-tile), so count them whole
+        mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(mbn * C::KCS * G_STAGE_A1 + (p + 1) * C::WR));
+        for (int mb = 0; mb < mbn; ++mb)
+          tma_3d(sx + mb * C::KCS * G_STAGE_A1, &maps.x, 0, m0 + mb * G_BM, kc0, &full_bar[s]);
+        for (int j = 0; j < p; ++j) tma_3d(sw + j * C::WR, &maps.plane[j], 0, kc0, nt0, &full_bar[s]);
+        tma_3d(sw + 4 * C::WR, &maps.scale, 0, kc0, nt0, &full_bar[s]);
       }
     }
-  } else {
-    // ---------------------------------------------------------------- dequant + MMA issue
-    // Dequant units: per n-group 32 lane chunks x 4 words x 2 m-tile halves = 256.  Within a
-    // unit-group of 256 threads, a half-warp covers gq = 0..7 x (tig & 1) of one (word, k block):
-    // its 16 swizzled 8 B stores hit distinct banks.
-    const int uw = (tid >> 5) & 3, uhalf = tid >> 7;
-    const int uL = ((tid >> 1) & 7) * 4 + ((tid >> 4) & 1) * 2 + (tid & 1);
-    for (int kc = 0; kc < KC; ++kc) {
-      const int s = kc % C::NS;
-      uint8_t* sa = ring + s * C::STAGE;
-      uint8_t* raw = sa + C::STAGE_A;
-      uint8_t* sb = smem + (kc & 1) * C::STAGE_B;
-      if (kc >= 2) mbar_wait(&bbuf_bar[kc & 1], ((kc - 2) >> 1) & 1);  // MMAs of chunk kc-2 read this buffer
-      mbar_wait(&full_bar[s], (kc / C::NS) & 1);
-#ifndef GEMM_SKIP_DEQUANT
-      for (int h = 0; h < NG; ++h) {
-        uint8_t* sbh = sb + h * G_STAGE_B1;
-        if (h < ngn) {
-          dequant_dispatch(p, raw + h * G_RAW, uL, uw, uhalf, sbh);
-        } else {  // n-group past the matrix: zero weights
-#pragma unroll
-          for (int t = 0; t < 2; ++t)
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh)
-              *reinterpret_cast<uint2*>(sbh + sw128_off(16 * (2 * uhalf + t) + (uL >> 2) + 8 * hh,
-                                                        32 * (uw >> 1) + 16 * (uw & 1) + 4 * (uL & 3))) = make_uint2(0u, 0u);
-        }
-      }
-#endif
-      fence_async_smem();  // this thread's dequant stores -> visible to the tensor core (async proxy)
-      named_bar_sync(1, G_DQ);
-      if (tid == 0) {
+  } else if (warp == G_MMA) {
+    // ---------------------------------------------------------------- MMA issue (one lane)
+    if (lane == 0) {
+      for (int kc = 0; kc < KC; ++kc) {
+        const int st = kc / C::KCS, kcs = kc - st * C::KCS, s = st % C::NS, b = kc % C::NB;
+        mbar_wait(&bfull[b], (kc / C::NB) & 1);  // implies the chunk's TMA landed (dequant waited on it)
         tc_fence_after();
-        const uint32_t b0 = smem_u32(sb);
+        const uint32_t b0 = smem_u32(smem + b * C::STAGE_B);
         for (int mb = 0; mb < mbn; ++mb) {
-          const uint32_t a0 = smem_u32(sa + mb * G_STAGE_A1);
+          const uint32_t a0 = smem_u32(ring + s * C::STAGE + (mb * C::KCS + kcs) * G_STAGE_A1);
 #ifndef GEMM_SKIP_MMA
 #pragma unroll
           for (int k16 = 0; k16 < G_KC / 16; ++k16)
-#else
-          for (int k16 = 0; k16 < 0; ++k16)
-#endif
             umma_f16(tmem + mb * C::N, smem_desc_sw128(a0 + 32 * k16), smem_desc_sw128(b0 + 32 * k16), C::IDESC,
                      (kc > 0 || k16 > 0) ? 1u : 0u);
+#endif
         }
-        umma_commit(&mma_bar[s]);
-        umma_commit(&bbuf_bar[kc & 1]);
+        if (kcs == C::KCS - 1 || kc == KC - 1) umma_commit(&mma_bar[s]);  // load stage reusable
+        umma_commit(&bempty[b]);                                          // weight buffer reusable
       }
+    }
+  } else {
+    // ---------------------------------------------------------------- dequant warps
+    switch (p) {
+      case 4: dequant_loop<4, NG, MB>(KC, ngn, ring, smem, full_bar, bfull, bempty, tid); break;
+      case 3: dequant_loop<3, NG, MB>(KC, ngn, ring, smem, full_bar, bfull, bempty, tid); break;
+      case 2: dequant_loop<2, NG, MB>(KC, ngn, ring, smem, full_bar, bfull, bempty, tid); break;
+      default: dequant_loop<1, NG, MB>(KC, ngn, ring, smem, full_bar, bfull, bempty, tid); break;
     }
   }
   // all MMAs done
-  mbar_wait(&mma_bar[(KC - 1) % C::NS], ((KC - 1) / C::NS) & 1);
+  {
+    const int last = (KC - 1) / C::KCS;
+    mbar_wait(&mma_bar[last % C::NS], (last / C::NS) & 1);
+  }
   tc_fence_after();
   // epilogue, per accumulator block: TMEM -> smem tile [128 rows][N (+1 pad)] f32 (warp w reads
   // TMEM lanes 32*(w%4).., columns half w/4), then all 256 threads write y in coalesced row
@@ -367,14 +398,14 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
 }
 
 template <int NG, int MB>
-int launch(const GemmArgs& g, const CUtensorMap& xmap, int m, int n_tiles, cudaStream_t st) {
+int launch(const GemmArgs& g, const GemmMaps& maps, int m, int n_tiles, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gemm_kernel<NG, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<NG, MB>::SMEM);
     attr = true;
   }
   dim3 grid((n_tiles + NG - 1) / NG, (m + MB * G_BM - 1) / (MB * G_BM));
-  gemm_kernel<NG, MB><<<grid, G_THREADS, Cfg<NG, MB>::SMEM, st>>>(g, xmap);
+  gemm_kernel<NG, MB><<<grid, G_THREADS, Cfg<NG, MB>::SMEM, st>>>(g, maps);
   return check_launch("prefill gemm launch");
 }
 
@@ -409,12 +440,6 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
   g.alpha = alpha;
   g.p_dev = p_dev;
   g.status = status_dev;
-  // x as a 2-D tensor [m rows][K] f16; boxes of 64 k x 128 rows, 128 B swizzle (zero-filled past row m)
-  CUtensorMap xmap;
-  const cuuint64_t gdim[2] = {(cuuint64_t)t->k, (cuuint64_t)m};
-  const cuuint64_t gstride[1] = {(cuuint64_t)ldx * 2};
-  const cuuint32_t box[2] = {(cuuint32_t)G_KC, (cuuint32_t)G_BM};
-  const cuuint32_t estride[2] = {1, 1};
   // driver entry point resolved at run time: the library must load on hosts without libcuda
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -428,10 +453,6 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
       return fail(PMPD_ERR_CUDA, "prefill gemm: cuTensorMapEncodeTiled is unavailable");
     encode = reinterpret_cast<EncodeFn>(fn);
   }
-  CUresult r = encode(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(x_dev), gdim,
-                                      gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(PMPD_ERR_CUDA, "prefill gemm: cuTensorMapEncodeTiled failed (%d)", (int)r);
   // (n-groups, token blocks) per CTA: the most operand reuse (fewest x re-reads per output,
   // fewest dequants per token) that still gives about one wave of CTAs on the 148 SMs.
   const int mblocks = (m + G_BM - 1) / G_BM, sms = num_sms();
@@ -446,11 +467,39 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
       break;
     }
   }
+  const int kcs = ng == 4 && mb == 2 ? Cfg<4, 2>::KCS : ng == 4 ? Cfg<4, 1>::KCS : ng == 2 && mb == 2 ? Cfg<2, 2>::KCS
+                  : ng == 2 ? Cfg<2, 1>::KCS : mb == 2 ? Cfg<1, 2>::KCS : Cfg<1, 1>::KCS;
+  GemmMaps maps;
+  // x: [K/64 chunks][m rows][64 k] f16, box 64 k x 128 rows x KCS chunks -> KCS SW128 tiles (zero-filled past m)
+  {
+    const cuuint64_t gdim[3] = {(cuuint64_t)G_KC, (cuuint64_t)m, (cuuint64_t)t->k_tiles};
+    const cuuint64_t gstride[2] = {(cuuint64_t)ldx * 2, (cuuint64_t)G_KC * 2};
+    const cuuint32_t box[3] = {(cuuint32_t)G_KC, (cuuint32_t)G_BM, (cuuint32_t)kcs};
+    const cuuint32_t estride[3] = {1, 1, 1};
+    const CUresult r = encode(&maps.x, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(x_dev), gdim, gstride, box,
+                              estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(PMPD_ERR_CUDA, "prefill gemm: x tensor map (%d)", (int)r);
+  }
+  // planes / scales: [n_tiles][k_tiles][128 words of one 512 B tile], box 128 x KCS x NG
+  {
+    const cuuint64_t gdim[3] = {128, (cuuint64_t)t->k_tiles, (cuuint64_t)t->n_tiles};
+    const cuuint64_t gstride[2] = {(cuuint64_t)kTilePlaneBytes, (cuuint64_t)t->k_tiles * kTilePlaneBytes};
+    const cuuint32_t box[3] = {128, (cuuint32_t)kcs, (cuuint32_t)ng};
+    const cuuint32_t estride[3] = {1, 1, 1};
+    for (int j = 0; j < 5; ++j) {
+      void* base = j < 4 ? const_cast<uint8_t*>(g.planes + (int64_t)j * g.plane_bytes) : const_cast<uint8_t*>(g.scales);
+      const CUresult r = encode(j < 4 ? &maps.plane[j] : &maps.scale, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, base, gdim,
+                                gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return fail(PMPD_ERR_CUDA, "prefill gemm: weight tensor map (%d)", (int)r);
+    }
+  }
   cudaStream_t st = as_stream(stream);
-  if (ng == 4 && mb == 2) return launch<4, 2>(g, xmap, m, t->n_tiles, st);
-  if (ng == 4) return launch<4, 1>(g, xmap, m, t->n_tiles, st);
-  if (ng == 2 && mb == 2) return launch<2, 2>(g, xmap, m, t->n_tiles, st);
-  if (ng == 2) return launch<2, 1>(g, xmap, m, t->n_tiles, st);
-  if (mb == 2) return launch<1, 2>(g, xmap, m, t->n_tiles, st);
-  return launch<1, 1>(g, xmap, m, t->n_tiles, st);
+  if (ng == 4 && mb == 2) return launch<4, 2>(g, maps, m, t->n_tiles, st);
+  if (ng == 4) return launch<4, 1>(g, maps, m, t->n_tiles, st);
+  if (ng == 2 && mb == 2) return launch<2, 2>(g, maps, m, t->n_tiles, st);
+  if (ng == 2) return launch<2, 1>(g, maps, m, t->n_tiles, st);
+  if (mb == 2) return launch<1, 2>(g, maps, m, t->n_tiles, st);
+  return launch<1, 1>(g, maps, m, t->n_tiles, st);
 }

@@ -26,6 +26,8 @@
 // Epilogue: tcgen05.ld (32x32b) of the accumulator rows -> smem tile -> alpha * acc (+ y) -> y
 // in coalesced row segments.
 #include <cuda.h>
+#include <cstdio>
+#include <cstdlib>
 #include <cuda_fp16.h>
 
 #include "decode_core.cuh"
@@ -453,21 +455,34 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
       return fail(PMPD_ERR_CUDA, "prefill gemm: cuTensorMapEncodeTiled is unavailable");
     encode = reinterpret_cast<EncodeFn>(fn);
   }
-  // (n-groups, token blocks) per CTA: the most operand reuse (fewest x re-reads per output,
-  // fewest dequants per token) that still gives about one wave of CTAs on the 148 SMs.
+  // (n-groups, token blocks) per CTA from a cost model fitted to the measured config-4 sweep
+  // (tools/gemm_cfg_sweep.sh): a CTA spends ~0.06 + 0.19*NG + 0.27*MB us per K chunk (dequant
+  // grows with NG, x loads and MMAs with MB); time ~ waves x chunks x that.  Fewer CTAs with more
+  // operand reuse win when the extra wave of a finer split would cost more than the reuse saves.
   const int mblocks = (m + G_BM - 1) / G_BM, sms = num_sms();
-  auto ctas = [&](int ng, int mb) { return (int64_t)((t->n_tiles + ng - 1) / ng) * ((mblocks + mb - 1) / mb); };
-  static const int cand[][2] = {{4, 2}, {4, 1}, {2, 2}, {2, 1}, {1, 2}, {1, 1}};
+  static const int cand[][2] = {{4, 2}, {2, 4}, {2, 2}, {4, 1}, {1, 4}, {2, 1}, {1, 2}, {1, 1}};
   int ng = 1, mb = 1;
+  double best = 1e30;
   for (const auto& c : cand) {
-    if (c[1] > 1 && mblocks < c[1]) continue;
-    if (ctas(c[0], c[1]) * 5 >= (int64_t)sms * 4) {  // >= ~80% of the SMs busy
+    const int mbe = c[1] < mblocks ? c[1] : mblocks;
+    if (c[1] > 1 && mblocks < c[1] && c[1] / 2 >= mblocks) continue;  // would leave a whole accumulator idle
+    const int64_t ctas = (int64_t)((t->n_tiles + c[0] - 1) / c[0]) * ((mblocks + c[1] - 1) / c[1]);
+    const double waves = (double)((ctas + sms - 1) / sms);
+    const double cost = waves * (0.06 + 0.19 * c[0] + 0.27 * mbe);
+    if (cost < best * 0.999) {
+      best = cost;
       ng = c[0];
       mb = c[1];
-      break;
     }
   }
-  const int kcs = ng == 4 && mb == 2 ? Cfg<4, 2>::KCS : ng == 4 ? Cfg<4, 1>::KCS : ng == 2 && mb == 2 ? Cfg<2, 2>::KCS
+  if (const char* e = getenv("PMPD_GEMM_CFG")) {  // diagnostics: force "ng,mb"
+    int a = 0, b = 0;
+    if (sscanf(e, "%d,%d", &a, &b) == 2 && (a == 1 || a == 2 || a == 4) && (b == 1 || b == 2 || b == 4) && a * b <= 8) {
+      ng = a;
+      mb = b;
+    }
+  }
+  const int kcs = ng == 1 && mb == 4 ? Cfg<1, 4>::KCS : ng == 2 && mb == 4 ? Cfg<2, 4>::KCS : ng == 4 && mb == 2 ? Cfg<4, 2>::KCS : ng == 4 ? Cfg<4, 1>::KCS : ng == 2 && mb == 2 ? Cfg<2, 2>::KCS
                   : ng == 2 ? Cfg<2, 1>::KCS : mb == 2 ? Cfg<1, 2>::KCS : Cfg<1, 1>::KCS;
   GemmMaps maps;
   // x: [K/64 chunks][m rows][64 k] f16, box 64 k x 128 rows x KCS chunks -> KCS SW128 tiles (zero-filled past m)
@@ -496,6 +511,8 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
     }
   }
   cudaStream_t st = as_stream(stream);
+  if (ng == 1 && mb == 4) return launch<1, 4>(g, maps, m, t->n_tiles, st);
+  if (ng == 2 && mb == 4) return launch<2, 4>(g, maps, m, t->n_tiles, st);
   if (ng == 4 && mb == 2) return launch<4, 2>(g, maps, m, t->n_tiles, st);
   if (ng == 4) return launch<4, 1>(g, maps, m, t->n_tiles, st);
   if (ng == 2 && mb == 2) return launch<2, 2>(g, maps, m, t->n_tiles, st);

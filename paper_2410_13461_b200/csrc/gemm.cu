@@ -116,6 +116,13 @@ PMPD_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+PMPD_DEV void tma_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
 PMPD_DEV void tma_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
@@ -124,8 +131,9 @@ PMPD_DEV void tma_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, 
       : "memory");
 }
 
-// TMA descriptors of one launch: x as [K/64 chunks][M rows][64 k] (f16, 128 B swizzle), and each
-// bit plane / the scale blocks as [n_tiles][k_tiles][128 words] (one 512 B tile per row).
+// TMA descriptors of one launch: x as [K/64 chunks][M rows][64 k] (f16, 128 B swizzle); the bit
+// planes as [plane][n_tiles][k_tiles][128 words] with plane[j] boxing planes 0..j (one load for
+// the p active planes); the scale blocks as [n_tiles][k_tiles][128 words].
 struct alignas(64) GemmMaps {
   CUtensorMap x;
   CUtensorMap plane[4];
@@ -297,7 +305,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
         mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(mbn * C::KCS * G_STAGE_A1 + (p + 1) * C::WR));
         for (int mb = 0; mb < mbn; ++mb)
           tma_3d(sx + mb * C::KCS * G_STAGE_A1, &maps.x, 0, m0 + mb * G_BM, kc0, &full_bar[s]);
-        for (int j = 0; j < p; ++j) tma_3d(sw + j * C::WR, &maps.plane[j], 0, kc0, nt0, &full_bar[s]);
+        tma_4d(sw, &maps.plane[p - 1], 0, kc0, nt0, 0, &full_bar[s]);  // planes 0..p-1
         tma_3d(sw + 4 * C::WR, &maps.scale, 0, kc0, nt0, &full_bar[s]);
       }
     }
@@ -496,17 +504,20 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(PMPD_ERR_CUDA, "prefill gemm: x tensor map (%d)", (int)r);
   }
-  // planes / scales: [n_tiles][k_tiles][128 words of one 512 B tile], box 128 x KCS x NG
+  // planes: [4][n_tiles][k_tiles][128 words of one 512 B tile], box 128 x KCS x NG x (j+1);
+  // scales: [n_tiles][k_tiles][128], box 128 x KCS x NG
   {
-    const cuuint64_t gdim[3] = {128, (cuuint64_t)t->k_tiles, (cuuint64_t)t->n_tiles};
-    const cuuint64_t gstride[2] = {(cuuint64_t)kTilePlaneBytes, (cuuint64_t)t->k_tiles * kTilePlaneBytes};
-    const cuuint32_t box[3] = {128, (cuuint32_t)kcs, (cuuint32_t)ng};
-    const cuuint32_t estride[3] = {1, 1, 1};
+    const cuuint64_t gdim[4] = {128, (cuuint64_t)t->k_tiles, (cuuint64_t)t->n_tiles, 4};
+    const cuuint64_t gstride[3] = {(cuuint64_t)kTilePlaneBytes, (cuuint64_t)t->k_tiles * kTilePlaneBytes,
+                                   (cuuint64_t)g.plane_bytes};
+    const cuuint32_t estride[4] = {1, 1, 1, 1};
     for (int j = 0; j < 5; ++j) {
-      void* base = j < 4 ? const_cast<uint8_t*>(g.planes + (int64_t)j * g.plane_bytes) : const_cast<uint8_t*>(g.scales);
-      const CUresult r = encode(j < 4 ? &maps.plane[j] : &maps.scale, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, base, gdim,
-                                gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      const cuuint32_t box[4] = {128, (cuuint32_t)kcs, (cuuint32_t)ng, (cuuint32_t)(j < 4 ? j + 1 : 1)};
+      void* base = j < 4 ? const_cast<uint8_t*>(g.planes) : const_cast<uint8_t*>(g.scales);
+      const CUresult r = encode(j < 4 ? &maps.plane[j] : &maps.scale, CU_TENSOR_MAP_DATA_TYPE_UINT32, j < 4 ? 4 : 3,
+                                base, gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) return fail(PMPD_ERR_CUDA, "prefill gemm: weight tensor map (%d)", (int)r);
     }
   }

@@ -715,10 +715,26 @@ int ctas_per_sm() {
   return v;
 }
 
+// Split-K grid: one CTA per SM over the contiguous tile range (n-groups shared by 2-3 CTAs are
+// reduced through the workspace).
 int grid_for(const pmpd_qtensor* t) {
   const int nt = t->n_tiles * t->k_tiles;
   const int g = num_sms() * ctas_per_sm();
   return nt < g ? nt : g;
+}
+
+// Launch grid: one CTA per n-group (no cross-CTA reduction: saves the partial write, the ticket
+// and a second L2 round trip, ~3 us) when the n-groups fit one wave, or two waves at batch <= 2
+// (measured, decode sweep); the split-K grid otherwise.
+int launch_grid(const pmpd_qtensor* t, int m) {
+  const int sms = num_sms();
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("PMPD_GEMV_SPLITK");  // diagnostics: 1 forces the split-K grid
+    mode = e ? atoi(e) : 0;
+  }
+  if (mode != 1 && (t->n_tiles <= sms || (m <= 2 && t->n_tiles <= 2 * sms))) return t->n_tiles;
+  return grid_for(t);
 }
 
 int slots_for(const pmpd_qtensor* t) {
@@ -780,7 +796,7 @@ int pmpd_gemv(const pmpd_qtensor* t, const void* x, int32_t ldx, int32_t m, cons
   a.status = reinterpret_cast<int*>(w8) + kWsCounters;
   a.partial = reinterpret_cast<float*>(w8 + kWsHead);
   a.max_slots = slots_for(t);
-  const int grid = grid_for(t);
+  const int grid = launch_grid(t, m);
   cudaStream_t s = as_stream(stream);
   const bool kn = t->layout == PMPD_LAYOUT_KN;
   switch (t->p_max) {

@@ -143,6 +143,21 @@ int pmpd_gemv(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, int32_t m, 
               int32_t y_dtype, int32_t ldy, float alpha, int32_t accumulate, void* workspace_dev,
               int64_t workspace_bytes, void* stream);
 
+/* Decode GEMV with its producer op fused into the activation staging (batch 1..8, staged path:
+ * K <= 12288 at m = 1, m*K <= 32768 otherwise; CONFIG error outside it, callers then run the
+ * two ops separately):
+ *   PMPD_GEMV_IN_RMSNORM: x = f16(xf * rsqrt(mean(xf^2) + eps) * gain)   (tinylm.py:293-295,
+ *                         the RMSNorm before q|k|v and before gate|up, 337/345)
+ *   PMPD_GEMV_IN_SWIGLU:  x = f16(silu(xf[k]) * xf[k + u_off])            (tinylm.py:298,362-364,
+ *                         the SwiGLU before the down projection)
+ * xf: f32 [m][ldxf]; everything else as pmpd_gemv. */
+#define PMPD_GEMV_IN_RMSNORM 1
+#define PMPD_GEMV_IN_SWIGLU 2
+int pmpd_gemv_fused(const pmpd_qtensor* t, int32_t in_mode, const float* xf_dev, int32_t ldxf, int32_t m,
+                    const float* gain_dev, float eps, int32_t u_off, const int32_t* p_dev, void* y_dev,
+                    int32_t y_dtype, int32_t ldy, float alpha, int32_t accumulate, void* workspace_dev,
+                    int64_t workspace_bytes, void* stream);
+
 /* Prefill GEMM on sm_100a tensor cores (tcgen05, TMEM accumulators): the
  * prompt-length linear layers of prefill (tinylm.py:377-388 -> 334-368).
  * y[m][n] = alpha * sum_k x[m][k] W_p[n][k] (+ y if accumulate) for m >= 1 rows;
@@ -214,6 +229,15 @@ int pmpd_rope_kv(const float* qkv_dev, int32_t ldq, int32_t m, int32_t d, int32_
 int pmpd_attention(const float* q_dev, int32_t m, int32_t d, int32_t d_head, const void* k_cache_dev,
                    const void* v_cache_dev, const int32_t* T_dev, int32_t max_ctx, float scale, void* out_dev,
                    void* stream);
+
+/* Decode step (one query) with RoPE and the KV append fused into the split-context attention:
+ * q|k|v of the new token (f32 row: q at 0, k at d, v at 2d) -> rotate q and k at position
+ * T = *T_dev (tinylm.py:308-319,344-347), write k and v into cache row T (f16, skipped when
+ * T >= max_ctx), attend over rows 0..T (tinylm.py:349-358) -> out f16 [d].  Equals
+ * pmpd_rope_kv followed by pmpd_attention for m = 1.  d_head in {32, 64, 128, 256}. */
+int pmpd_attention_rope(const float* qkv_dev, int32_t d, int32_t d_head, const float* cos_dev, const float* sin_dev,
+                        const int32_t* T_dev, int32_t max_ctx, float scale, void* k_cache_dev, void* v_cache_dev,
+                        void* out_dev, void* stream);
 
 /* out (f16) = silu(u[:, :ff]) * u[:, ff:] (tinylm.py:362-364). */
 int pmpd_silu_mul(const float* u_dev, int32_t ldu, int32_t m, int32_t ff, void* out_dev, int32_t ldo, void* stream);

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("PMPD_LIB") or os.path.join(_HERE, "lib", "libpmpd_b20
 OK, ERR_CONFIG, ERR_INPUT, ERR_CONTRACT, ERR_FORMAT, ERR_CUDA = 0, 1, 2, 3, 4, 5
 LAYOUT_REF, LAYOUT_KN, LAYOUT_NK = 0, 1, 2
 DTYPE_F32, DTYPE_F16, DTYPE_F64 = 0, 1, 2
+GEMV_IN_RMSNORM, GEMV_IN_SWIGLU = 1, 2  # pmpd_b200.h PMPD_GEMV_IN_*
 
 
 class CudaError(PmpdError):
@@ -58,11 +59,13 @@ SIGNATURES = {
     "pmpd_gather_rows": [_D, _P, _I, _P, _P, _P],
     "pmpd_gemv_workspace_bytes": [_D, _I, ctypes.POINTER(_L)],
     "pmpd_gemv": [_D, _P, _I, _I, _P, _P, _I, _I, _F, _I, _P, _L, _P],
+    "pmpd_gemv_fused": [_D, _I, _P, _I, _I, _P, _F, _I, _P, _P, _I, _I, _F, _I, _P, _L, _P],
     "pmpd_gemm": [_D, _P, _I, _I, _P, _P, _I, _I, _F, _I, _P, _P],
     "pmpd_sched_step": [_P, _I, _P, _P, _I, _P],
     "pmpd_rmsnorm": [_P, _I, _P, _I, _I, _F, _P, _I, _P],
     "pmpd_rope_kv": [_P, _I, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P],
     "pmpd_attention": [_P, _I, _I, _I, _P, _P, _P, _I, _F, _P, _P],
+    "pmpd_attention_rope": [_P, _I, _I, _P, _P, _P, _I, _F, _P, _P, _P, _P],
     "pmpd_silu_mul": [_P, _I, _I, _I, _P, _I, _P],
     "pmpd_argmax": [_P, _I, _I, _I, _P, _P, _P],
     "pmpd_add_i32": [_P, _I, _P],

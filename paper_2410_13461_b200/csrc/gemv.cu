@@ -75,6 +75,14 @@ struct GemvArgs {
   int* status;     // [1]
   float* partial;  // [n_tiles][max_slots][64][m]
   int max_slots;
+  // fused input (staged-activation path only): 0 = x as given (f16); 1 = RMSNorm of the f32 row
+  // xf (tinylm.py:293-295, gain, eps); 2 = silu(xf[k]) * xf[k + u_off] (tinylm.py:298,362-364)
+  int in_mode;
+  const float* xf;
+  int ldxf;
+  const float* gain;
+  float eps;
+  int u_off;
 };
 
 struct Smem {  // fits in the first 128 bytes of dynamic shared memory
@@ -605,6 +613,48 @@ __global__ void __launch_bounds__(NTHREADS, 1) qgemv_kernel(const GemvArgs a) {
       // stage x (zero-padded to a multiple of 64) in shared memory once, tracking max |x|
       __half* xs = reinterpret_cast<__half*>(smem_raw + PL::kXs);
       const int kp = KT * kTile;
+      if (a.in_mode != 0) {
+        // fused producer op: the row is f32; RMSNorm needs its sum of squares first
+        const float* xr = a.xf + (int64_t)b * a.ldxf;
+        float inv = 1.f;
+        if (a.in_mode == 1) {
+          float ss = 0.f;
+#pragma unroll 4
+          for (int k = threadIdx.x; k < a.k_real; k += NCW * 32) {
+            const float v = xr[k];
+            ss = fmaf(v, v, ss);
+          }
+          ss = warp_sum(ss);
+          if (lane == 0) red32[warp] = ss;
+          named_bar_sync(1, NCW * 32);
+          float tot = 0.f;
+          for (int w = 0; w < NCW; ++w) tot += red32[w];
+          inv = rsqrtf(tot / (float)a.k_real + a.eps);
+          named_bar_sync(1, NCW * 32);  // red32 is reused for the max below
+        }
+#pragma unroll 2
+        for (int k = threadIdx.x * 2; k < kp; k += NCW * 32 * 2) {
+          float v[2];
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int kk = k + i;
+            float r = 0.f;
+            if (kk < a.k_real) {
+              if (a.in_mode == 1) {
+                r = xr[kk] * inv * a.gain[kk];
+              } else {
+                const float g = xr[kk];
+                r = g / (1.f + __expf(-g)) * xr[kk + a.u_off];
+              }
+            }
+            v[i] = r;
+          }
+          const __half2 h = __floats2half2_rn(v[0], v[1]);
+          const float2 f = __half22float2(h);
+          m = fmaxf(m, fmaxf(fabsf(f.x), fabsf(f.y)));
+          *reinterpret_cast<__half2*>(xs + b * xsld + k) = h;
+        }
+      } else
       for (int k = threadIdx.x * 8; k < kp; k += NCW * 32 * 8) {
         uint4 v = make_uint4(0u, 0u, 0u, 0u);
         const __half* src = a.x + (int64_t)b * a.ldx + k;
@@ -760,15 +810,30 @@ int pmpd_gemv_workspace_bytes(const pmpd_qtensor* t, int32_t m, int64_t* bytes) 
   return PMPD_OK;
 }
 
-int pmpd_gemv(const pmpd_qtensor* t, const void* x, int32_t ldx, int32_t m, const int32_t* p_dev, void* y,
-              int32_t y_dtype, int32_t ldy, float alpha, int32_t accumulate, void* ws, int64_t ws_bytes,
-              void* stream) {
+}  // extern "C"
+
+namespace {
+struct GemvIn {
+  int mode;
+  const void* x;  // f16 (mode 0) or f32 (modes 1, 2)
+  int ldx;
+  const float* gain;
+  float eps;
+  int u_off;
+};
+
+int gemv_impl(const pmpd_qtensor* t, const GemvIn& in, int32_t m, const int32_t* p_dev, void* y, int32_t y_dtype,
+              int32_t ldy, float alpha, int32_t accumulate, void* ws, int64_t ws_bytes, void* stream) {
+  const void* x = in.x;
+  const int32_t ldx = in.ldx;
+
   if (!t || !t->data) return fail(PMPD_ERR_CONFIG, "null quantized tensor");
   if (!is_tiled(t->layout)) return fail(PMPD_ERR_CONFIG, "GEMV needs a tiled layout (KN or NK)");
   if (m < 1 || m > MAXM) return fail(PMPD_ERR_INPUT, "decode GEMV batch must be in [1, %d], got %d", MAXM, m);
   if (ldx < t->k || ldy < t->n) return fail(PMPD_ERR_INPUT, "leading dimensions too small");
   if (y_dtype != PMPD_DTYPE_F32 && y_dtype != PMPD_DTYPE_F16) return fail(PMPD_ERR_CONFIG, "bad output dtype");
-  if ((reinterpret_cast<uintptr_t>(x) & 3) || (ldx & 1)) return fail(PMPD_ERR_INPUT, "x must be 4-byte aligned");
+  if ((reinterpret_cast<uintptr_t>(x) & 3) || (in.mode == 0 && (ldx & 1)))
+    return fail(PMPD_ERR_INPUT, "x must be 4-byte aligned");
   int64_t need = 0;
   if (int e = pmpd_gemv_workspace_bytes(t, m, &need)) return e;
   if (!ws || ws_bytes < need) return fail(PMPD_ERR_INPUT, "workspace too small: need %lld bytes", (long long)need);
@@ -791,6 +856,19 @@ int pmpd_gemv(const pmpd_qtensor* t, const void* x, int32_t ldx, int32_t m, cons
   a.ldy = ldy;
   a.alpha = alpha;
   a.accumulate = accumulate;
+  a.in_mode = in.mode;
+  a.xf = static_cast<const float*>(in.x);
+  a.ldxf = in.ldx;
+  a.gain = in.gain;
+  a.eps = in.eps;
+  a.u_off = in.u_off;
+  if (in.mode != 0) {
+    const int kp = t->k_tiles * kTile;
+    const bool staged = m == 1 ? kp <= kXsMaxK : m * kp <= kXsMulti;
+    if (!staged) return fail(PMPD_ERR_CONFIG, "fused GEMV input needs the staged-activation path (m*K too large)");
+    if (in.mode == 1 && !in.gain) return fail(PMPD_ERR_CONFIG, "RMSNorm input needs a gain vector");
+    if (in.mode == 2 && in.u_off < t->k) return fail(PMPD_ERR_CONFIG, "SwiGLU input needs u_off >= K");
+  }
   uint8_t* w8 = static_cast<uint8_t*>(ws);
   a.counters = reinterpret_cast<int*>(w8);
   a.status = reinterpret_cast<int*>(w8) + kWsCounters;
@@ -809,6 +887,27 @@ int pmpd_gemv(const pmpd_qtensor* t, const void* x, int32_t ldx, int32_t m, cons
     default:
       return kn ? launch<PMPD_LAYOUT_KN, 1>(a, grid, s) : launch<PMPD_LAYOUT_NK, 1>(a, grid, s);
   }
+}
+
+}  // namespace
+
+extern "C" {
+
+int pmpd_gemv(const pmpd_qtensor* t, const void* x, int32_t ldx, int32_t m, const int32_t* p_dev, void* y,
+              int32_t y_dtype, int32_t ldy, float alpha, int32_t accumulate, void* ws, int64_t ws_bytes,
+              void* stream) {
+  const GemvIn in{0, x, ldx, nullptr, 0.f, 0};
+  return gemv_impl(t, in, m, p_dev, y, y_dtype, ldy, alpha, accumulate, ws, ws_bytes, stream);
+}
+
+int pmpd_gemv_fused(const pmpd_qtensor* t, int32_t in_mode, const float* xf, int32_t ldxf, int32_t m,
+                    const float* gain, float eps, int32_t u_off, const int32_t* p_dev, void* y, int32_t y_dtype,
+                    int32_t ldy, float alpha, int32_t accumulate, void* ws, int64_t ws_bytes, void* stream) {
+  if (in_mode != PMPD_GEMV_IN_RMSNORM && in_mode != PMPD_GEMV_IN_SWIGLU)
+    return fail(PMPD_ERR_CONFIG, "unknown fused GEMV input mode %d", in_mode);
+  if (!xf || (reinterpret_cast<uintptr_t>(xf) & 3)) return fail(PMPD_ERR_INPUT, "f32 input must be 4-byte aligned");
+  const GemvIn in{in_mode, xf, ldxf, gain, eps, u_off};
+  return gemv_impl(t, in, m, p_dev, y, y_dtype, ldy, alpha, accumulate, ws, ws_bytes, stream);
 }
 
 }  // extern "C"

@@ -168,11 +168,15 @@ PMPD_DEV void load_row(const __half* __restrict__ p, float (&f)[DPL]) {
   }
 }
 
-template <int DPL>
+// ROPE (decode, one query): q comes raw from the q|k|v row `q` (ldq = its width) and is rotated
+// here; the CTA whose split holds the new position also rotates k, and writes k and v into cache
+// row T (f16, as rope_kv_kernel does) before reading it back in its loop.  RoPE pairs dim j with
+// j + dh/2, which for every DPL sits in lane ^ 16 (tinylm.py:308-319,344-347).
+template <int DPL, bool ROPE>
 __global__ void __cluster_dims__(kSplit, 1, 1) __launch_bounds__(kAttnWarps * 32)
-    attention_split_kernel(const float* __restrict__ q, int d, const __half* __restrict__ kc,
-                           const __half* __restrict__ vc, const int32_t* __restrict__ T_dev, int max_ctx, float scale,
-                           __half* __restrict__ out) {
+    attention_split_kernel(const float* __restrict__ q, int d, __half* __restrict__ kc, __half* __restrict__ vc,
+                           const int32_t* __restrict__ T_dev, int max_ctx, float scale, __half* __restrict__ out,
+                           const float* __restrict__ cos_t, const float* __restrict__ sin_t) {
   constexpr int DH = 32 * DPL;
   __shared__ float w_ml[kAttnWarps][2];
   __shared__ float w_acc[kAttnWarps][DH];
@@ -188,8 +192,41 @@ __global__ void __cluster_dims__(kSplit, 1, 1) __launch_bounds__(kAttnWarps * 32
   const int t0 = rank * chunk, t1 = min(L, t0 + chunk);
 
   float qr[DPL];
+  if constexpr (!ROPE) {
 #pragma unroll
-  for (int j = 0; j < DPL; ++j) qr[j] = q[(int64_t)i * d + h * DH + lane * DPL + j];
+    for (int j = 0; j < DPL; ++j) qr[j] = q[(int64_t)i * d + h * DH + lane * DPL + j];
+  } else {
+    // i == 0; position T = L - 1 (the row being appended)
+    constexpr int HALF = DH / 2;
+    const int pos = L - 1;
+    const bool first = lane < 16;
+    float c[DPL], sn[DPL];
+#pragma unroll
+    for (int j = 0; j < DPL; ++j) {
+      const int jj = (lane * DPL + j) % HALF;
+      c[j] = cos_t[(int64_t)pos * HALF + jj];
+      sn[j] = sin_t[(int64_t)pos * HALF + jj];
+    }
+    auto rot = [&](const float* src, float (&dst)[DPL]) {
+#pragma unroll
+      for (int j = 0; j < DPL; ++j) {
+        const float a = src[h * DH + lane * DPL + j];
+        const float b = __shfl_xor_sync(0xffffffffu, a, 16);  // partner dim j +- HALF
+        dst[j] = first ? a * c[j] - b * sn[j] : a * c[j] + b * sn[j];
+      }
+    };
+    rot(q, qr);
+    if (*T_dev < max_ctx && pos >= t0 && pos < t1 && warp == 0) {
+      float kr[DPL];
+      rot(q + d, kr);
+#pragma unroll
+      for (int j = 0; j < DPL; ++j) {
+        kc[(int64_t)pos * d + h * DH + lane * DPL + j] = __float2half(kr[j]);
+        vc[(int64_t)pos * d + h * DH + lane * DPL + j] = __float2half(q[2 * d + h * DH + lane * DPL + j]);
+      }
+    }
+    __syncthreads();  // the appended row is read below by every warp of this CTA
+  }
   const __half* kb = kc + h * DH + lane * DPL;
   const __half* vb = vc + h * DH + lane * DPL;
   float m = -INFINITY, l = 0.f, acc[DPL];
@@ -504,24 +541,24 @@ int pmpd_attention(const float* q, int32_t m, int32_t d, int32_t d_head, const v
   static const bool generic = getenv("PMPD_ATTN_GENERIC") != nullptr;  // diagnostics: force attention_kernel
   if (al && m >= 1 && !generic) {
     const dim3 grid((unsigned)(m * (d / d_head) * kSplit));
-    const auto kc = (const __half*)k_cache;
-    const auto vc = (const __half*)v_cache;
+    const auto kc = (__half*)const_cast<void*>(k_cache);
+    const auto vc = (__half*)const_cast<void*>(v_cache);
     switch (d_head) {
       case 32:
-        attention_split_kernel<1><<<grid, kAttnWarps * 32, 0, as_stream(stream)>>>(q, d, kc, vc, T_dev, max_ctx,
-                                                                                   scale, (__half*)out);
+        attention_split_kernel<1, false><<<grid, kAttnWarps * 32, 0, as_stream(stream)>>>(
+            q, d, kc, vc, T_dev, max_ctx, scale, (__half*)out, nullptr, nullptr);
         return check_launch("pmpd_attention");
       case 64:
-        attention_split_kernel<2><<<grid, kAttnWarps * 32, 0, as_stream(stream)>>>(q, d, kc, vc, T_dev, max_ctx,
-                                                                                   scale, (__half*)out);
+        attention_split_kernel<2, false><<<grid, kAttnWarps * 32, 0, as_stream(stream)>>>(
+            q, d, kc, vc, T_dev, max_ctx, scale, (__half*)out, nullptr, nullptr);
         return check_launch("pmpd_attention");
       case 128:
-        attention_split_kernel<4><<<grid, kAttnWarps * 32, 0, as_stream(stream)>>>(q, d, kc, vc, T_dev, max_ctx,
-                                                                                   scale, (__half*)out);
+        attention_split_kernel<4, false><<<grid, kAttnWarps * 32, 0, as_stream(stream)>>>(
+            q, d, kc, vc, T_dev, max_ctx, scale, (__half*)out, nullptr, nullptr);
         return check_launch("pmpd_attention");
       case 256:
-        attention_split_kernel<8><<<grid, kAttnWarps * 32, 0, as_stream(stream)>>>(q, d, kc, vc, T_dev, max_ctx,
-                                                                                   scale, (__half*)out);
+        attention_split_kernel<8, false><<<grid, kAttnWarps * 32, 0, as_stream(stream)>>>(
+            q, d, kc, vc, T_dev, max_ctx, scale, (__half*)out, nullptr, nullptr);
         return check_launch("pmpd_attention");
       default:
         break;
@@ -537,6 +574,39 @@ int pmpd_attention(const float* q, int32_t m, int32_t d, int32_t d_head, const v
   attention_kernel<<<dim3(m, d / d_head), kBlock, smem, as_stream(stream)>>>(
       q, d, d_head, (const __half*)k_cache, (const __half*)v_cache, T_dev, max_ctx, scale, (__half*)out);
   return check_launch("pmpd_attention");
+}
+
+int pmpd_attention_rope(const float* qkv, int32_t d, int32_t d_head, const float* cos_t, const float* sin_t,
+                        const int32_t* T_dev, int32_t max_ctx, float scale, void* k_cache, void* v_cache, void* out,
+                        void* stream) {
+  if (d % d_head || d_head % 32 || d_head > 256) return fail(PMPD_ERR_CONFIG, "bad head geometry for the fused path");
+  if ((reinterpret_cast<uintptr_t>(k_cache) & 15) || (reinterpret_cast<uintptr_t>(v_cache) & 15))
+    return fail(PMPD_ERR_INPUT, "KV cache must be 16-byte aligned");
+  const dim3 grid((unsigned)((d / d_head) * kSplit));
+  auto kc = static_cast<__half*>(k_cache);
+  auto vc = static_cast<__half*>(v_cache);
+  auto o = static_cast<__half*>(out);
+  switch (d_head) {
+    case 32:
+      attention_split_kernel<1, true><<<grid, kAttnWarps * 32, 0, as_stream(stream)>>>(qkv, d, kc, vc, T_dev, max_ctx,
+                                                                                        scale, o, cos_t, sin_t);
+      break;
+    case 64:
+      attention_split_kernel<2, true><<<grid, kAttnWarps * 32, 0, as_stream(stream)>>>(qkv, d, kc, vc, T_dev, max_ctx,
+                                                                                        scale, o, cos_t, sin_t);
+      break;
+    case 128:
+      attention_split_kernel<4, true><<<grid, kAttnWarps * 32, 0, as_stream(stream)>>>(qkv, d, kc, vc, T_dev, max_ctx,
+                                                                                        scale, o, cos_t, sin_t);
+      break;
+    case 256:
+      attention_split_kernel<8, true><<<grid, kAttnWarps * 32, 0, as_stream(stream)>>>(qkv, d, kc, vc, T_dev, max_ctx,
+                                                                                        scale, o, cos_t, sin_t);
+      break;
+    default:
+      return fail(PMPD_ERR_CONFIG, "head dim %d not supported by the fused path", d_head);
+  }
+  return check_launch("pmpd_attention_rope");
 }
 
 int pmpd_silu_mul(const float* u, int32_t ldu, int32_t m, int32_t ff, void* out, int32_t ldo, void* stream) {

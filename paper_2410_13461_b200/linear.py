@@ -73,6 +73,33 @@ def gemv(pk: PackedTensor, x: torch.Tensor, p_dev: torch.Tensor, workspace: Work
     return out
 
 
+def gemv_fused(pk: PackedTensor, mode: int, xf: torch.Tensor, p_dev: torch.Tensor, workspace: Workspace,
+               out: torch.Tensor, gain: torch.Tensor | None = None, eps: float = 1e-6, u_off: int = 0,
+               alpha: float = 1.0, accumulate: bool = False) -> torch.Tensor:
+    """``gemv`` with its producer op fused into the activation staging (one launch instead of two).
+
+    mode ``_capi.GEMV_IN_RMSNORM``: the input is ``rmsnorm(xf) * gain`` of the f32 rows xf
+    (tinylm.py:293-295); ``_capi.GEMV_IN_SWIGLU``: ``silu(xf[:, k]) * xf[:, k + u_off]``
+    (tinylm.py:298,362-364).  Raises ConfigError when the shape is outside the staged path
+    (callers then run the two ops separately).
+    """
+    if xf.dtype != torch.float32 or xf.dim() != 2 or not xf.is_cuda or xf.stride(1) != 1:
+        raise InputError("fused gemv input must be a row-contiguous 2-D float32 CUDA tensor")
+    m = xf.shape[0]
+    d = pk.desc
+    if out.stride(1) != 1 or tuple(out.shape) != (m, d.n):
+        raise InputError("gemv output must be a row-contiguous [m, n] tensor")
+    ydt = _capi.DTYPE_F32 if out.dtype == torch.float32 else _capi.DTYPE_F16
+    need = workspace_bytes(pk, m)
+    if need > workspace.nbytes:
+        workspace.ensure(need)
+    _capi.call("pmpd_gemv_fused", pk.ref(), int(mode), xf.data_ptr(), xf.stride(0), m,
+               gain.data_ptr() if gain is not None else None, float(eps), int(u_off), p_dev.data_ptr(),
+               out.data_ptr(), ydt, out.stride(0), float(alpha), int(bool(accumulate)), workspace.buf.data_ptr(),
+               workspace.nbytes, torch.cuda.current_stream().cuda_stream)
+    return out
+
+
 def gemm(pk: PackedTensor, x: torch.Tensor, p_dev: torch.Tensor, out: torch.Tensor | None = None,
          out_dtype=torch.float32, alpha: float = 1.0, accumulate: bool = False,
          status: torch.Tensor | None = None) -> torch.Tensor:

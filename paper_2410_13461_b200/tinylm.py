@@ -22,6 +22,7 @@ from __future__ import annotations
 import hashlib
 import json
 import math
+import os
 import threading
 from dataclasses import dataclass
 from pathlib import Path
@@ -32,7 +33,7 @@ import torch
 
 from . import _capi
 from .errors import ConfigError, ContractViolation, FormatError, InputError
-from .linear import Workspace, gemm, gemv, workspace_bytes
+from .linear import Workspace, gemm, gemv, gemv_fused, workspace_bytes
 from .quant import BitPlaneStore, PrecisionSet, QuantizedTensor, dequantize, parse_model, quantize_tensor, \
     serialize_model
 from .schedule import PrecisionSchedule
@@ -149,12 +150,18 @@ class _DeviceWeights:
                                                                               lay["w_down"]]]
         self.ws_bytes = max(workspace_bytes(pk, GEMV_MAX_ROWS) for pk in pks)
         self.fp16 = None
+        self._kp = (-(-cfg.d_model // 64) * 64, -(-cfg.d_ff // 64) * 64)
         if mv.full_weights is not None:
             self.fp16 = {n: torch.tensor(w, device="cuda").half() for n, w in mv.full_weights.items()}
             # fused q|k|v weight of the fp16 baseline, concatenated once (not per call)
             for i in range(cfg.n_layers):
                 names = [f"layers.{i}.{nm}" for nm in ("wq", "wk", "wv")]
                 self.fp16["+".join(names)] = torch.cat([self.fp16.pop(nm) for nm in names], dim=1).contiguous()
+
+
+    def fusable(self, n: int) -> bool:
+        """Whether the fused RMSNorm/SwiGLU decode GEMVs accept n rows (the staged-activation path)."""
+        return all(kp <= 12288 if n == 1 else n * kp <= 32768 for kp in self._kp)
 
 
 class ModelVariants:
@@ -323,6 +330,20 @@ def _linear(dw: _DeviceWeights, pks: list, name16: list, x16: torch.Tensor, out:
         col += width
 
 
+_FUSE_DECODE = os.environ.get("PMPD_FUSE_DECODE", "0") == "1"  # fused norm/SwiGLU GEMVs: measured slower, off
+
+
+def _fused_linear(pks: list, mode: int, xf: torch.Tensor, gain, u_off: int, out: torch.Tensor, buf: _Buffers,
+                  accumulate: bool) -> None:
+    """out (+)= op(xf) @ W_p with op = RMSNorm*gain or SwiGLU fused into the decode GEMV staging."""
+    col = 0
+    for pk in pks:
+        width = pk.desc.n
+        gemv_fused(pk, mode, xf, buf.p, buf.ws, out[:, col:col + width], gain=gain, eps=1e-6, u_off=u_off,
+                   accumulate=accumulate)
+        col += width
+
+
 def _run_layers(model: ModelVariants, dw: _DeviceWeights, buf: _Buffers, n: int, cache: KVCache, p_host) -> None:
     """Embedding + all blocks + final norm + head for n tokens in buf.ids; logits -> buf.logits[:n]."""
     cfg = model.config
@@ -335,22 +356,40 @@ def _run_layers(model: ModelVariants, dw: _DeviceWeights, buf: _Buffers, n: int,
     else:
         _capi.call("pmpd_gather_rows", dw.embed.ref(), buf.ids.data_ptr(), n, buf.p.data_ptr(), x.data_ptr(), s)
     scale = 1.0 / math.sqrt(dh)
+    # decode steps: RMSNorm and SwiGLU run inside the GEMV's activation staging (one launch each
+    # instead of two) when the fused path accepts the shape
+    fuse = p_host != FULL_PRECISION and n <= GEMV_MAX_ROWS and dw.fusable(n) and _FUSE_DECODE
     for i, lay in enumerate(dw.layers):
         pre = f"layers.{i}."
-        _capi.call("pmpd_rmsnorm", x.data_ptr(), d, lay["norm_attn"].data_ptr(), n, d, 1e-6, h.data_ptr(), d, s)
-        _linear(dw, lay["qkv"], [pre + "wq", pre + "wk", pre + "wv"], h, qkv, buf.p, p_host, buf.ws, False)
-        _capi.call("pmpd_rope_kv", qkv.data_ptr(), 3 * d, n, d, dh, dw.cos.data_ptr(), dw.sin.data_ptr(),
-                   cache.T_dev.data_ptr(), cache.capacity, q.data_ptr(), cache.k[i].data_ptr(),
-                   cache.v[i].data_ptr(), s)
-        _capi.call("pmpd_attention", q.data_ptr(), n, d, dh, cache.k[i].data_ptr(), cache.v[i].data_ptr(),
-                   cache.T_dev.data_ptr(), cache.capacity, scale, ctx.data_ptr(), s)
+        if fuse:
+            _fused_linear(lay["qkv"], _capi.GEMV_IN_RMSNORM, x, lay["norm_attn"], 0, qkv, buf, False)
+        else:
+            _capi.call("pmpd_rmsnorm", x.data_ptr(), d, lay["norm_attn"].data_ptr(), n, d, 1e-6, h.data_ptr(), d, s)
+            _linear(dw, lay["qkv"], [pre + "wq", pre + "wk", pre + "wv"], h, qkv, buf.p, p_host, buf.ws, False)
+        if n == 1 and dh % 32 == 0 and dh <= 256:  # decode: RoPE + KV append fused into the attention
+            _capi.call("pmpd_attention_rope", qkv.data_ptr(), d, dh, dw.cos.data_ptr(), dw.sin.data_ptr(),
+                       cache.T_dev.data_ptr(), cache.capacity, scale, cache.k[i].data_ptr(), cache.v[i].data_ptr(),
+                       ctx.data_ptr(), s)
+        else:
+            _capi.call("pmpd_rope_kv", qkv.data_ptr(), 3 * d, n, d, dh, dw.cos.data_ptr(), dw.sin.data_ptr(),
+                       cache.T_dev.data_ptr(), cache.capacity, q.data_ptr(), cache.k[i].data_ptr(),
+                       cache.v[i].data_ptr(), s)
+            _capi.call("pmpd_attention", q.data_ptr(), n, d, dh, cache.k[i].data_ptr(), cache.v[i].data_ptr(),
+                       cache.T_dev.data_ptr(), cache.capacity, scale, ctx.data_ptr(), s)
         _linear(dw, [lay["wo"]], [pre + "wo"], ctx, x, buf.p, p_host, buf.ws, True)
-        _capi.call("pmpd_rmsnorm", x.data_ptr(), d, lay["norm_mlp"].data_ptr(), n, d, 1e-6, h.data_ptr(), d, s)
-        _linear(dw, [lay["w_up"]], [pre + "w_up"], h, u, buf.p, p_host, buf.ws, False)
-        _capi.call("pmpd_silu_mul", u.data_ptr(), 2 * ff, n, ff, a.data_ptr(), ff, s)
-        _linear(dw, [lay["w_down"]], [pre + "w_down"], a, x, buf.p, p_host, buf.ws, True)
-    _capi.call("pmpd_rmsnorm", x.data_ptr(), d, dw.final_norm.data_ptr(), n, d, 1e-6, h.data_ptr(), d, s)
-    _linear(dw, [dw.head], ["head"], h, logits, buf.p, p_host, buf.ws, False)
+        if fuse:
+            _fused_linear([lay["w_up"]], _capi.GEMV_IN_RMSNORM, x, lay["norm_mlp"], 0, u, buf, False)
+            _fused_linear([lay["w_down"]], _capi.GEMV_IN_SWIGLU, u, None, ff, x, buf, True)
+        else:
+            _capi.call("pmpd_rmsnorm", x.data_ptr(), d, lay["norm_mlp"].data_ptr(), n, d, 1e-6, h.data_ptr(), d, s)
+            _linear(dw, [lay["w_up"]], [pre + "w_up"], h, u, buf.p, p_host, buf.ws, False)
+            _capi.call("pmpd_silu_mul", u.data_ptr(), 2 * ff, n, ff, a.data_ptr(), ff, s)
+            _linear(dw, [lay["w_down"]], [pre + "w_down"], a, x, buf.p, p_host, buf.ws, True)
+    if fuse:
+        _fused_linear([dw.head], _capi.GEMV_IN_RMSNORM, x, dw.final_norm, 0, logits, buf, False)
+    else:
+        _capi.call("pmpd_rmsnorm", x.data_ptr(), d, dw.final_norm.data_ptr(), n, d, 1e-6, h.data_ptr(), d, s)
+        _linear(dw, [dw.head], ["head"], h, logits, buf.p, p_host, buf.ws, False)
 
 
 def _check_precision(model: ModelVariants, p: int) -> None:

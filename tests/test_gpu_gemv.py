@@ -137,3 +137,54 @@ def test_shared_workspace_across_shapes():
 
 def quantize_tensor_cached(w):
     return quant.quantize_tensor(w, 4, 64).packed(_capi.LAYOUT_KN)
+
+
+@pytest.mark.parametrize("K,N,M", [(2048, 6144, 1), (4096, 4096, 1), (5632, 2048, 1), (1000, 320, 3), (4096, 512, 8)])
+def test_gemv_fused_rmsnorm_matches_two_kernels(K, N, M):
+    """pmpd_gemv_fused(RMSNORM) == pmpd_rmsnorm then pmpd_gemv (tinylm.py:293-295 then h @ W)."""
+    from paper_2410_13461_b200.linear import gemv_fused
+    torch.manual_seed(K + N + M)
+    w = torch.randn(K, N) * 0.02
+    pk = quant.quantize_tensor(w.cuda(), 4, 64).packed(_capi.LAYOUT_KN)
+    xf = (torch.randn(M, K) * 3).cuda()
+    gain = (torch.rand(K) + 0.5).cuda()
+    ws = Workspace()
+    for p in (4, 2):
+        h = torch.empty(M, K, dtype=torch.float16, device="cuda")
+        _capi.call("pmpd_rmsnorm", xf.data_ptr(), K, gain.data_ptr(), M, K, 1e-6, h.data_ptr(), K, None)
+        ref = gemv(pk, h, _pdev(p), ws)
+        out = torch.zeros(M, N, device="cuda")
+        gemv_fused(pk, _capi.GEMV_IN_RMSNORM, xf, _pdev(p), ws, out, gain=gain, eps=1e-6)
+        torch.cuda.synchronize()
+        assert rel_l2(out.cpu().numpy(), ref.cpu().numpy()) < 2e-3, p
+
+
+@pytest.mark.parametrize("F,N,M", [(5632, 2048, 1), (11008, 4096, 1), (512, 256, 4)])
+def test_gemv_fused_swiglu_matches_two_kernels(F, N, M):
+    """pmpd_gemv_fused(SWIGLU) == pmpd_silu_mul then pmpd_gemv, accumulating into y."""
+    from paper_2410_13461_b200.linear import gemv_fused
+    torch.manual_seed(F + N + M)
+    w = torch.randn(F, N) * 0.02
+    pk = quant.quantize_tensor(w.cuda(), 4, 64).packed(_capi.LAYOUT_KN)
+    u = torch.randn(M, 2 * F).cuda()
+    ws = Workspace()
+    y0 = torch.randn(M, N).cuda()
+    for p in (4, 3):
+        a = torch.empty(M, F, dtype=torch.float16, device="cuda")
+        _capi.call("pmpd_silu_mul", u.data_ptr(), 2 * F, M, F, a.data_ptr(), F, None)
+        ref = y0.clone()
+        gemv(pk, a, _pdev(p), ws, out=ref, accumulate=True)
+        out = y0.clone()
+        gemv_fused(pk, _capi.GEMV_IN_SWIGLU, u, _pdev(p), ws, out, u_off=F, accumulate=True)
+        torch.cuda.synchronize()
+        assert rel_l2(out.cpu().numpy(), ref.cpu().numpy()) < 2e-3, p
+
+
+def test_gemv_fused_rejects_unstaged_shapes():
+    from paper_2410_13461_b200.errors import ConfigError
+    from paper_2410_13461_b200.linear import gemv_fused
+    pk = quant.quantize_tensor(torch.randn(8192, 64).cuda() * 0.02, 4, 64).packed(_capi.LAYOUT_KN)
+    xf = torch.randn(8, 8192).cuda()
+    with pytest.raises(ConfigError):
+        gemv_fused(pk, _capi.GEMV_IN_RMSNORM, xf, _pdev(4), Workspace(), torch.zeros(8, 64, device="cuda"),
+                   gain=torch.ones(8192, device="cuda"))

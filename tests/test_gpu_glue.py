@@ -63,3 +63,39 @@ def test_rmsnorm_vs_torch(m, d):
     xd = x.double()
     ref = xd / torch.sqrt((xd * xd).mean(dim=1, keepdim=True) + 1e-6) * g.double()
     torch.testing.assert_close(out.double(), ref, rtol=2e-3, atol=2e-3)
+
+
+@pytest.mark.parametrize("dh,H,T", [(32, 2, 0), (32, 4, 13), (64, 4, 77), (128, 32, 500), (256, 2, 9)])
+def test_attention_rope_matches_two_kernels(dh, H, T):
+    """pmpd_attention_rope == pmpd_rope_kv + pmpd_attention for one decode query: same output and
+    the same cache row T."""
+    torch.manual_seed(dh * H + T)
+    d = dh * H
+    cap = T + 4
+    half = dh // 2
+    ang = torch.arange(cap, dtype=torch.float64)[:, None] * (1e4 ** (-torch.arange(0, dh, 2, dtype=torch.float64) / dh))
+    cos_t, sin_t = torch.cos(ang).float().cuda().contiguous(), torch.sin(ang).float().cuda().contiguous()
+    assert cos_t.shape == (cap, half)
+    k0 = (torch.randn(cap, d, device="cuda") * 0.5).half()
+    v0 = torch.randn(cap, d, device="cuda").half()
+    qkv = torch.randn(1, 3 * d, device="cuda")
+    T_dev = torch.tensor([T], dtype=torch.int32, device="cuda")
+    scale = 1.0 / math.sqrt(dh)
+    # reference: two kernels
+    k1, v1 = k0.clone(), v0.clone()
+    q = torch.zeros(1, d, device="cuda")
+    out1 = torch.zeros(1, d, dtype=torch.float16, device="cuda")
+    _capi.call("pmpd_rope_kv", qkv.data_ptr(), 3 * d, 1, d, dh, cos_t.data_ptr(), sin_t.data_ptr(), T_dev.data_ptr(),
+               cap, q.data_ptr(), k1.data_ptr(), v1.data_ptr(), None)
+    _capi.call("pmpd_attention", q.data_ptr(), 1, d, dh, k1.data_ptr(), v1.data_ptr(), T_dev.data_ptr(), cap, scale,
+               out1.data_ptr(), None)
+    # fused
+    k2, v2 = k0.clone(), v0.clone()
+    out2 = torch.zeros(1, d, dtype=torch.float16, device="cuda")
+    _capi.call("pmpd_attention_rope", qkv.data_ptr(), d, dh, cos_t.data_ptr(), sin_t.data_ptr(), T_dev.data_ptr(), cap,
+               scale, k2.data_ptr(), v2.data_ptr(), out2.data_ptr(), None)
+    torch.cuda.synchronize()
+    assert torch.equal(v1, v2)
+    assert (k1.float() - k2.float()).abs().max().item() <= 1e-3 * k1.float().abs().max().item()
+    rel = ((out1.float() - out2.float()).norm() / out1.float().norm()).item()
+    assert rel < 2e-3, rel

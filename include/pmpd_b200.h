@@ -199,6 +199,27 @@ int pmpd_engine_nslots(const pmpd_qtensor* t, uint8_t* out_host);
 int pmpd_engine_make_op(const pmpd_qtensor* t, int32_t src, int32_t src_col, int32_t act, int32_t act_off,
                         float in_alpha, float* part_dev, int32_t max_slots, const uint8_t* nslots_dev,
                         void* op_host);
+/* Decoder-step ops (a whole batch-1 decode step in one engine launch; tinylm.py:334-368):
+ *   pmpd_engine_op_set_io: after pmpd_engine_make_op, switch the op's input to
+ *     in_mode 2 = RMSNorm(resid) * gain over the whole f32 row (tinylm.py:293-295, 337/345/349) or
+ *     in_mode 3 = the combined records of the attention op `src`, and/or make `part` a persistent
+ *     vector (keep_out = 1: the residual stream; the op's output is ADDED into it, x += ctx @ Wo /
+ *     x += a @ W_down, tinylm.py:359/364), scaled by out_alpha.
+ *   pmpd_engine_make_attn_op: attention over one layer's f16 KV cache for the new token: q|k|v =
+ *     the f32 output of op `src`; RoPE at position T = *T_dev (cos/sin [max_ctx][d_head/2]);
+ *     k, v appended to row T; records_dev holds pmpd_engine_attn_records() f32.
+ *     d_head in {32, 64, 128, 256}. */
+int pmpd_engine_op_set_io(void* op_host, int32_t in_mode, const float* resid_dev, const float* gain_dev, float eps,
+                          int32_t keep_out, float out_alpha);
+int pmpd_engine_make_attn_op(int32_t src, int32_t n_heads, int32_t d_head, void* k_cache_dev, void* v_cache_dev,
+                             const float* cos_dev, const float* sin_dev, const int32_t* T_dev, int32_t max_ctx,
+                             float scale, float* records_dev, void* op_host);
+int pmpd_engine_attn_records(int32_t n_heads, int32_t d_head);
+/* pmpd_engine_run for programs that use the decoder-step ops above (a separate kernel
+ * instantiation, so the linear-stack program pays nothing for them); trace_dev optional. */
+int pmpd_engine_run_decoder(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, float* y_out_dev, float y_alpha,
+                            uint32_t* bar_dev, int32_t* status_dev, int64_t* trace_dev, void* stream);
+
 int pmpd_engine_run(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const void* x_in_dev, float* y_out_dev,
                     float y_alpha, uint32_t* bar_dev, int32_t* status_dev, void* stream);
 /* Same, recording a per-CTA per-op timeline (globaltimer ns):

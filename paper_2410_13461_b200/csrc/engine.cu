@@ -58,7 +58,28 @@ struct EngineOp {
   int max_slots;  // unused since the L2-atomic reduction (kept for the op-table ABI)
   float* part;    // this op's f32 output [n_tiles * 64]: zero at launch, split-K partials added at L2
   const unsigned char* nslots;  // unused (op-table ABI)
+  // ---- decoder-step extensions (pmpd_engine_op_set_io / pmpd_engine_make_attn_op)
+  int kind;          // E_LINEAR or E_ATTN
+  int in_mode;       // E_IN_SRC (src / x_in, as above), E_IN_RMSNORM (rmsnorm(resid) * gain), E_IN_ATTN
+  const float* resid;
+  const float* gain;
+  float eps;
+  float eps_inv_k;   // 1 / k_real (RMSNorm mean)
+  int keep_out;      // part persists across launches (the residual stream): never re-zeroed
+  float out_alpha;   // scale of the partials the epilogue adds into part
+  // E_ATTN: q|k|v of the new token = src->part (f32 [3d]); part = per-(head, split) records
+  __half* kc;
+  __half* vc;
+  const float* cos_t;
+  const float* sin_t;
+  const int32_t* T_dev;
+  int n_heads, d_head, max_ctx;
+  float scale;
 };
+constexpr int E_LINEAR = 0, E_ATTN = 1;
+constexpr int E_IN_SRC = 0, E_IN_RMSNORM = 2, E_IN_ATTN = 3;
+constexpr int E_ASPLIT = 4;  // context splits per head in the attention op
+PMPD_DEV int attn_rec(int dh) { return 4 + dh; }  // record: m, l, pad, pad, acc[dh] (16-byte aligned acc)
 
 struct EngineArgs {
   const EngineOp* ops;
@@ -149,7 +170,232 @@ PMPD_DEV Range range_of(const EngineOp& op, int c, int G) {
   return r;
 }
 
+// ------------------------------------------------------------------ attention op
+// One decode query over the KV cache of one layer (tinylm.py:344-358), as engine work units
+// (head h, split s): RoPE of q (and of the new k, by the unit holding position T, which also
+// appends k and v to the cache, tinylm.py:308-319), then the 12 consumer warps stream the
+// unit's rows with an online softmax; the CTA folds the warps into one record (m, l, acc) that
+// the next op's staging combines (E_IN_ATTN).  scratch: [E_NCW][4 + dh] f32 (shared).
+template <int DPL>
+PMPD_DEV void ld_halves(const __half* __restrict__ p, bool ok, float (&f)[DPL]) {
+  if (!ok) {
+#pragma unroll
+    for (int j = 0; j < DPL; ++j) f[j] = 0.f;
+    return;
+  }
+  if constexpr (DPL == 1) {
+    f[0] = __half2float(*p);
+  } else if constexpr (DPL == 2) {
+    const float2 v = __half22float2(*reinterpret_cast<const __half2*>(p));
+    f[0] = v.x;
+    f[1] = v.y;
+  } else {
+    constexpr int W = DPL / 2;  // 32-bit words: 2 (uint2) or 4 (uint4)
+    uint32_t w[W];
+    if constexpr (DPL == 4) {
+      const uint2 u = *reinterpret_cast<const uint2*>(p);
+      w[0] = u.x;
+      w[1] = u.y;
+    } else {
+      const uint4 u = *reinterpret_cast<const uint4*>(p);
+      w[0] = u.x;
+      w[1] = u.y;
+      w[2] = u.z;
+      w[3] = u.w;
+    }
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      const float2 v = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+      f[2 * i] = v.x;
+      f[2 * i + 1] = v.y;
+    }
+  }
+}
+
+template <int DPL>
+PMPD_DEV void attn_unit(const EngineOp& op, const float* __restrict__ qkv, int h, int s, int L, float* scratch,
+                        int warp, int lane) {
+  constexpr int DH = 32 * DPL, HALF = DH / 2;
+  const int d = op.n_heads * DH;
+  const int chunk = (L + E_ASPLIT - 1) / E_ASPLIT;
+  const int t0 = s * chunk, t1 = min(L, t0 + chunk);
+  const int pos = L - 1;
+  const bool first = lane < 16;
+  float c[DPL], sn[DPL];
+#pragma unroll
+  for (int j = 0; j < DPL; ++j) {
+    const int jj = (lane * DPL + j) % HALF;
+    c[j] = __ldg(op.cos_t + (int64_t)pos * HALF + jj);
+    sn[j] = __ldg(op.sin_t + (int64_t)pos * HALF + jj);
+  }
+  float qr[DPL];
+#pragma unroll
+  for (int j = 0; j < DPL; ++j) {
+    const float a = __ldcg(qkv + h * DH + lane * DPL + j);
+    const float b = __shfl_xor_sync(0xffffffffu, a, 16);  // RoPE partner dim j +- HALF
+    qr[j] = first ? a * c[j] - b * sn[j] : a * c[j] + b * sn[j];
+  }
+  if (*op.T_dev < op.max_ctx && pos >= t0 && pos < t1 && warp == 0) {
+#pragma unroll
+    for (int j = 0; j < DPL; ++j) {
+      const float a = __ldcg(qkv + d + h * DH + lane * DPL + j);
+      const float b = __shfl_xor_sync(0xffffffffu, a, 16);
+      const float kr = first ? a * c[j] - b * sn[j] : a * c[j] + b * sn[j];
+      op.kc[(int64_t)pos * d + h * DH + lane * DPL + j] = __float2half(kr);
+      op.vc[(int64_t)pos * d + h * DH + lane * DPL + j] = __float2half(__ldcg(qkv + 2 * d + h * DH + lane * DPL + j));
+    }
+  }
+  named_bar_sync(1, E_NCW * 32);  // the appended row is visible to every warp of the CTA
+  const __half* kb = op.kc + h * DH + lane * DPL;
+  const __half* vb = op.vc + h * DH + lane * DPL;
+  float m = -INFINITY, l = 0.f, acc[DPL];
+#pragma unroll
+  for (int j = 0; j < DPL; ++j) acc[j] = 0.f;
+  constexpr int U = 4;
+  for (int tb = t0 + warp; tb < t1; tb += E_NCW * U) {
+    float kf[U][DPL], vf[U][DPL], sc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int t = tb + u * E_NCW;
+      ld_halves<DPL>(kb + (int64_t)t * d, t < t1, kf[u]);
+      ld_halves<DPL>(vb + (int64_t)t * d, t < t1, vf[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float a = 0.f;
+#pragma unroll
+      for (int j = 0; j < DPL; ++j) a = fmaf(qr[j], kf[u][j], a);
+      sc[u] = a;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < U; ++u) sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], o);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (tb + u * E_NCW < t1) {
+        const float x = sc[u] * op.scale;
+        const float mn = fmaxf(m, x);
+        const float corr = __expf(m - mn), pe = __expf(x - mn);
+        l = fmaf(l, corr, pe);
+#pragma unroll
+        for (int j = 0; j < DPL; ++j) acc[j] = fmaf(acc[j], corr, pe * vf[u][j]);
+        m = mn;
+      }
+    }
+  }
+  float* wr = scratch + warp * (4 + DH);
+  if (lane == 0) {
+    wr[0] = m;
+    wr[1] = l;
+  }
+#pragma unroll
+  for (int j = 0; j < DPL; ++j) wr[4 + lane * DPL + j] = acc[j];
+  named_bar_sync(1, E_NCW * 32);
+  float M = -INFINITY;
+#pragma unroll
+  for (int w = 0; w < E_NCW; ++w) M = fmaxf(M, scratch[w * (4 + DH)]);
+  float* rec = op.part + (int64_t)(h * E_ASPLIT + s) * (4 + DH);
+  for (int e = threadIdx.x; e < DH + 2; e += E_NCW * 32) {
+    float v = 0.f;
+    for (int w = 0; w < E_NCW; ++w) {
+      const float mw = scratch[w * (4 + DH)];
+      const float wt = mw == -INFINITY ? 0.f : __expf(mw - M);
+      v = fmaf(e < DH ? scratch[w * (4 + DH) + 4 + e] : scratch[w * (4 + DH) + 1], wt, v);
+    }
+    if (e < DH)
+      rec[4 + e] = v;
+    else if (e == DH)
+      rec[1] = v;  // l
+    else
+      rec[0] = M;  // m
+  }
+  named_bar_sync(1, E_NCW * 32);  // scratch reused by the next unit
+}
+
+__noinline__ __device__ void attn_op(const EngineOp& op, const EngineOp& src, int c, int G, float* scratch, int warp,
+                                    int lane) {
+  const int L = min(*op.T_dev + 1, op.max_ctx);
+  for (int u = c; u < op.n_heads * E_ASPLIT; u += G) {
+    const int h = u / E_ASPLIT, s = u - h * E_ASPLIT;
+    switch (op.d_head) {
+      case 32: attn_unit<1>(op, src.part, h, s, L, scratch, warp, lane); break;
+      case 64: attn_unit<2>(op, src.part, h, s, L, scratch, warp, lane); break;
+      case 128: attn_unit<4>(op, src.part, h, s, L, scratch, warp, lane); break;
+      default: attn_unit<8>(op, src.part, h, s, L, scratch, warp, lane); break;
+    }
+  }
+}
+
+// E_IN_ATTN staging (kept out of line: its 48 live registers of split records would otherwise
+// count against the consumer loop's tile body).  Returns max |x| of the staged f16 row.
+__noinline__ __device__ float stage_attn_input(const EngineOp& op, const EngineOp& src, int kp, __half* xs,
+                                               float* wscratch) {
+  float mx = 0.f;
+      // The whole row (K = d <= 4608) in one L2 round trip: every thread issues the split records
+      // of its groups first, the per-(head, split) softmax weights w = exp(m_s - M_h) /
+      // sum_s exp(m_s - M_h) l_s are computed into xq scratch while those loads are in flight.
+      constexpr int SBA = 3;
+      const int dh = src.d_head;
+      float4 av[SBA][E_ASPLIT];
+#pragma unroll
+      for (int bi = 0; bi < SBA; ++bi) {
+        const int k = 4 * threadIdx.x + bi * 4 * E_NCW * 32;
+        const int hh = k < op.k_real ? k / dh : 0, e = k - hh * dh;
+        const float* rec = src.part + (int64_t)hh * E_ASPLIT * attn_rec(dh) + 4 + e;
+#pragma unroll
+        for (int q = 0; q < E_ASPLIT; ++q)
+          av[bi][q] = k < op.k_real ? __ldcg(reinterpret_cast<const float4*>(rec + q * attn_rec(dh)))
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      float* wts = wscratch;
+      for (int hh = threadIdx.x; hh < src.n_heads; hh += E_NCW * 32) {
+        const float* rec = src.part + (int64_t)hh * E_ASPLIT * attn_rec(dh);
+        float ms[E_ASPLIT], ls[E_ASPLIT], M = -INFINITY;
+#pragma unroll
+        for (int q = 0; q < E_ASPLIT; ++q) {
+          ms[q] = __ldcg(rec + q * attn_rec(dh));
+          ls[q] = __ldcg(rec + q * attn_rec(dh) + 1);
+          M = fmaxf(M, ms[q]);
+        }
+        float den = 0.f;
+#pragma unroll
+        for (int q = 0; q < E_ASPLIT; ++q) {
+          ms[q] = ms[q] == -INFINITY ? 0.f : __expf(ms[q] - M);
+          den = fmaf(ms[q], ls[q], den);
+        }
+        const float id = den > 0.f ? __frcp_rn(den) : 0.f;
+#pragma unroll
+        for (int q = 0; q < E_ASPLIT; ++q) wts[hh * E_ASPLIT + q] = ms[q] * id;
+      }
+      named_bar_sync(1, E_NCW * 32);
+#pragma unroll
+      for (int bi = 0; bi < SBA; ++bi) {
+        const int k = 4 * threadIdx.x + bi * 4 * E_NCW * 32;
+        if (k >= kp) break;
+        float o[4] = {0.f, 0.f, 0.f, 0.f};
+        if (k < op.k_real) {
+          const int hh = k / dh;
+#pragma unroll
+          for (int q = 0; q < E_ASPLIT; ++q) {
+            const float w = wts[hh * E_ASPLIT + q];
+            o[0] = fmaf(w, av[bi][q].x, o[0]);
+            o[1] = fmaf(w, av[bi][q].y, o[1]);
+            o[2] = fmaf(w, av[bi][q].z, o[2]);
+            o[3] = fmaf(w, av[bi][q].w, o[3]);
+          }
+        }
+        const __half2 h01 = __floats2half2_rn(o[0], o[1]), h23 = __floats2half2_rn(o[2], o[3]);
+        *reinterpret_cast<__half2*>(xs + k) = h01;
+        *reinterpret_cast<__half2*>(xs + k + 2) = h23;
+        const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(f01.x), fabsf(f01.y)), fmaxf(fabsf(f23.x), fabsf(f23.y))));
+      }
+  return mx;
+}
+
 // ------------------------------------------------------------------ kernel
+template <bool DEC>
 PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bars& bars, int G, int c,
                             int stage_bytes, int nstage) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tig = lane & 3;
@@ -163,6 +409,18 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
   int seg = 0;      // n-group segment counter (red double buffer)
   for (int oi = 0; oi < a.n_ops; ++oi) {
     const EngineOp& op = a.ops[oi];
+    if (DEC && op.kind == E_ATTN) {
+      if (oi > 0) {
+        if (threadIdx.x == 0) wait_tickets(a.bar, (unsigned)(oi * G));
+        named_bar_sync(1, E_NCW * 32);
+      }
+      attn_op(op, a.ops[op.src], c, G, reinterpret_cast<float*>(smem + kSmX), warp, lane);
+      named_bar_sync(1, E_NCW * 32);
+      // publish (the epilogue skips attention ops): the records above are ordered before this
+      // release by the CTA barrier (cumulativity)
+      if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar) : "memory");
+      continue;
+    }
     const Range r = range_of(op, c, G);
     // ---------------------------------------------------------- stage the input vector
     // k-tiles this CTA touches
@@ -197,6 +455,40 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
     if (a.trace && threadIdx.x == 0) a.trace[((int64_t)c * a.n_ops + oi) * 8 + 0] = gtimer();
     float mx = 0.f;
     const EngineOp* src = op.src >= 0 ? &a.ops[op.src] : nullptr;
+    float inv = 1.f;  // E_IN_RMSNORM: 1 / sqrt(mean(resid^2) + eps) over the whole row
+    if (DEC && op.in_mode == E_IN_RMSNORM) {
+      // one L2 pass: the whole f32 row lands in xs above the f16 staging area (bytes
+      // [2*KT*64, 2*KT*64 + 4*K), checked at set_io) while its sum of squares accumulates; the
+      // k-range is then staged from there without overlapping the f16 writes
+      float* row = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(xs) + 2 * r.KT * kTile);
+      float ss = 0.f;
+      constexpr int RB = 4;
+      for (int k0 = 4 * threadIdx.x; k0 < op.k_real; k0 += 4 * RB * E_NCW * 32) {
+        float4 q[RB];
+#pragma unroll
+        for (int j = 0; j < RB; ++j) {
+          const int k = k0 + j * 4 * E_NCW * 32;
+          q[j] = k < op.k_real ? __ldcg(reinterpret_cast<const float4*>(op.resid + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int j = 0; j < RB; ++j) {
+          const int k = k0 + j * 4 * E_NCW * 32;
+          ss = fmaf(q[j].x, q[j].x, fmaf(q[j].y, q[j].y, fmaf(q[j].z, q[j].z, fmaf(q[j].w, q[j].w, ss))));
+          if (k < op.k_real) *reinterpret_cast<float4*>(row + k) = q[j];
+        }
+      }
+      ss = warp_sum(ss);
+      if (lane == 0) misc[32 + warp] = ss;  // (misc[8..] holds max |x| below)
+      named_bar_sync(1, E_NCW * 32);
+      float tot = 0.f;
+#pragma unroll
+      for (int w = 0; w < E_NCW; ++w) tot += misc[32 + w];
+      inv = rsqrtf(tot * op.eps_inv_k + op.eps);
+    } else if (DEC && op.in_mode == E_IN_ATTN) {
+      mx = stage_attn_input(op, *src, r.KT * kTile, xs, reinterpret_cast<float*>(smem + kSmXq));
+      hi0 = hi1 = 0;  // staged already (the generic loop below runs no iteration)
+      lo0 = lo1 = 0;
+    }
     // Each thread stages groups of 4 consecutive elements, SB groups per batch: all
     // partial-slot loads of a batch are issued before any sum (one L2 round trip per batch).
     constexpr int SB = PMPD_ENGINE_SB;
@@ -204,7 +496,24 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
       const int klo = (seg2 ? lo1 : lo0) * kTile, khi = (seg2 ? hi1 : hi0) * kTile;
       for (int kb = klo + 4 * threadIdx.x; kb < khi; kb += 4 * SB * E_NCW * 32) {
         float v[SB][4];
-        if (!src) {
+        if (DEC && op.in_mode == E_IN_RMSNORM) {
+          float4 rv[SB], gv[SB];
+          const float* row = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(xs) + 2 * r.KT * kTile);
+#pragma unroll
+          for (int bi = 0; bi < SB; ++bi) {
+            const int k = kb + bi * 4 * E_NCW * 32;
+            const bool in = k < khi && k < op.k_real;
+            rv[bi] = in ? *reinterpret_cast<const float4*>(row + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+            gv[bi] = in ? __ldg(reinterpret_cast<const float4*>(op.gain + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int bi = 0; bi < SB; ++bi) {
+            v[bi][0] = rv[bi].x * inv * gv[bi].x;
+            v[bi][1] = rv[bi].y * inv * gv[bi].y;
+            v[bi][2] = rv[bi].z * inv * gv[bi].z;
+            v[bi][3] = rv[bi].w * inv * gv[bi].w;
+          }
+        } else if (!src) {
 #pragma unroll
           for (int bi = 0; bi < SB; ++bi) {
             const int k = kb + bi * 4 * E_NCW * 32;
@@ -249,7 +558,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               float g = r[0][i];
-              if (op.act == 1) g = g / (1.f + __expf(-g)) * r[1][i];
+              if (op.act == 1) g = __fdividef(g, 1.f + __expf(-g)) * r[1][i];
               v[bi][i] = (k + i < op.k_real) ? g : 0.f;
             }
           }
@@ -366,6 +675,9 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
   }
 }
 
+// DEC: the decoder-step op kinds (attention, RMSNorm / attention-combine inputs, residual outputs);
+// the linear-stack program runs the instantiation without them (no extra registers on its path).
+template <bool DEC>
 __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   Bars& bars = *reinterpret_cast<Bars*>(smem + kSmBar);
@@ -406,6 +718,7 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
       uint32_t phase = 0;
       for (int oi = 0; oi < a.n_ops; ++oi) {
         const EngineOp& op = a.ops[oi];
+        if (DEC && op.kind == E_ATTN) continue;  // no weights
         const Range r = range_of(op, c, G);
         int t = r.T0, kt = r.T0 % r.KT;
         while (t < r.T1) {
@@ -438,6 +751,7 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
     int seg = 0;
     for (int oi = 0; oi < a.n_ops; ++oi) {
       const EngineOp& op = a.ops[oi];
+      if (DEC && op.kind == E_ATTN) continue;  // published by the consumers
       const Range r = range_of(op, c, G);
       int t = r.T0, ng = r.T0 / r.KT, kt = r.T0 % r.KT;
       while (t < r.T1) {
@@ -459,7 +773,7 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
           float v = bsum;
 #pragma unroll
           for (int w = 0; w < E_NCW; ++w) v += red[(buf * E_NCW + w) * 64 + nl];
-          atomicAdd(dst + nl, v);
+          atomicAdd(dst + nl, DEC ? v * op.out_alpha : v);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars.red_empty[buf]);
@@ -483,7 +797,7 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
     }
   } else {
     // ------------------------------------------------------------ consumers
-    consumer_loop(p, a, smem, bars, G, c, stage_bytes, nstage);
+    consumer_loop<DEC>(p, a, smem, bars, G, c, stage_bytes, nstage);
   }
   // ---------------------------------------------------------------- final output
   __syncthreads();
@@ -501,6 +815,7 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
   // before the final ticket; the last op's n-groups are zeroed by the CTA that just read them.
   for (int oi = 0; oi < a.n_ops; ++oi) {
     const EngineOp& op = a.ops[oi];
+    if (DEC && (op.kind == E_ATTN || op.keep_out)) continue;  // records are rewritten; the residual stream persists
     for (int ng = c; ng < op.n_tiles; ng += G)
       for (int nl = threadIdx.x; nl < 64; nl += blockDim.x) op.part[(int64_t)ng * 64 + nl] = 0.f;
   }
@@ -570,6 +885,9 @@ int pmpd_engine_make_op(const pmpd_qtensor* t, int32_t src, int32_t src_col, int
   op.max_slots = max_slots;
   op.part = part_dev;
   op.nslots = nslots_dev;
+  op.kind = E_LINEAR;
+  op.in_mode = E_IN_SRC;
+  op.out_alpha = 1.f;
   if ((src_col & 3) || (act_off & 3)) return fail(PMPD_ERR_CONFIG, "engine input offsets must be multiples of 4");
   *static_cast<EngineOp*>(op_host) = op;
   return PMPD_OK;
@@ -578,13 +896,71 @@ int pmpd_engine_make_op(const pmpd_qtensor* t, int32_t src, int32_t src_col, int
 int pmpd_engine_run_traced(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const void* x_in, float* y_out,
                            float y_alpha, uint32_t* bar_dev, int32_t* status_dev, int64_t* trace_dev, void* stream);
 
+int pmpd_engine_op_set_io(void* op_host, int32_t in_mode, const float* resid_dev, const float* gain_dev, float eps,
+                          int32_t keep_out, float out_alpha) {
+  if (!op_host) return fail(PMPD_ERR_CONFIG, "null argument");
+  EngineOp& op = *static_cast<EngineOp*>(op_host);
+  if (op.kind != E_LINEAR) return fail(PMPD_ERR_CONFIG, "set_io applies to linear ops");
+  if (in_mode != E_IN_SRC && in_mode != E_IN_RMSNORM && in_mode != E_IN_ATTN)
+    return fail(PMPD_ERR_CONFIG, "unknown engine input mode %d", in_mode);
+  if (in_mode == E_IN_RMSNORM && (!resid_dev || !gain_dev || (op.k_real & 3) ||
+                                  (reinterpret_cast<uintptr_t>(resid_dev) & 15) ||
+                                  (reinterpret_cast<uintptr_t>(gain_dev) & 15)))
+    return fail(PMPD_ERR_CONFIG, "RMSNorm input needs 16-byte aligned resid/gain and K % 4 == 0");
+  op.in_mode = in_mode;
+  op.resid = resid_dev;
+  op.gain = gain_dev;
+  op.eps = eps;
+  op.eps_inv_k = 1.f / (float)op.k_real;
+  if (in_mode == E_IN_ATTN && op.k_tiles * kTile > 3 * 4 * E_NCW * 32)
+    return fail(PMPD_ERR_CONFIG, "attention-combine input wider than %d", 3 * 4 * E_NCW * 32);
+  if (in_mode == E_IN_RMSNORM && 2 * op.k_tiles * kTile + 4 * op.k_real > 2 * E_XMAX)
+    return fail(PMPD_ERR_CONFIG, "RMSNorm input row too wide for the staging area");
+  op.keep_out = keep_out ? 1 : 0;
+  op.out_alpha = out_alpha;
+  return PMPD_OK;
+}
+
+int pmpd_engine_make_attn_op(int32_t src, int32_t n_heads, int32_t d_head, void* k_cache, void* v_cache,
+                             const float* cos_dev, const float* sin_dev, const int32_t* T_dev, int32_t max_ctx,
+                             float scale, float* records_dev, void* op_host) {
+  if (!op_host || !k_cache || !v_cache || !cos_dev || !sin_dev || !T_dev || !records_dev)
+    return fail(PMPD_ERR_CONFIG, "null argument");
+  if (d_head != 32 && d_head != 64 && d_head != 128 && d_head != 256)
+    return fail(PMPD_ERR_CONFIG, "engine attention needs d_head in {32, 64, 128, 256}");
+  if ((int64_t)n_heads * E_ASPLIT * 4 > 3 * 1024) return fail(PMPD_ERR_CONFIG, "too many heads for the engine");
+  if (src < 0) return fail(PMPD_ERR_CONFIG, "attention op needs a q|k|v source op");
+  EngineOp op{};
+  op.kind = E_ATTN;
+  op.src = src;
+  op.n_heads = n_heads;
+  op.d_head = d_head;
+  op.kc = static_cast<__half*>(k_cache);
+  op.vc = static_cast<__half*>(v_cache);
+  op.cos_t = cos_dev;
+  op.sin_t = sin_dev;
+  op.T_dev = T_dev;
+  op.max_ctx = max_ctx;
+  op.scale = scale;
+  op.part = records_dev;
+  op.keep_out = 1;
+  op.out_alpha = 1.f;
+  *static_cast<EngineOp*>(op_host) = op;
+  return PMPD_OK;
+}
+
+int pmpd_engine_attn_records(int32_t n_heads, int32_t d_head) { return n_heads * E_ASPLIT * (4 + d_head); }
+
 int pmpd_engine_run(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const void* x_in, float* y_out,
                     float y_alpha, uint32_t* bar_dev, int32_t* status_dev, void* stream) {
   return pmpd_engine_run_traced(ops_dev, n_ops, p_dev, x_in, y_out, y_alpha, bar_dev, status_dev, nullptr, stream);
 }
 
-int pmpd_engine_run_traced(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const void* x_in, float* y_out,
-                           float y_alpha, uint32_t* bar_dev, int32_t* status_dev, int64_t* trace_dev, void* stream) {
+}  // extern "C"
+
+namespace {
+int engine_launch(bool dec, const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const void* x_in, float* y_out,
+                  float y_alpha, uint32_t* bar_dev, int32_t* status_dev, int64_t* trace_dev, void* stream) {
   if (n_ops < 1) return fail(PMPD_ERR_CONFIG, "engine program is empty");
   EngineArgs a;
   a.ops = static_cast<const EngineOp*>(ops_dev);
@@ -603,7 +979,8 @@ int pmpd_engine_run_traced(const void* ops_dev, int32_t n_ops, const int32_t* p_
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     smem = optin;
     if (const char* e = getenv("PMPD_ENGINE_SMEM")) smem = atoi(e) < optin ? atoi(e) : optin;
-    cudaFuncSetAttribute(engine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(engine_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(engine_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(num_sms());
@@ -615,9 +992,23 @@ int pmpd_engine_run_traced(const void* ops_dev, int32_t n_ops, const int32_t* p_
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, engine_kernel, a);
+  const cudaError_t e = dec ? cudaLaunchKernelEx(&cfg, engine_kernel<true>, a)
+                            : cudaLaunchKernelEx(&cfg, engine_kernel<false>, a);
   if (e != cudaSuccess) return fail(PMPD_ERR_CUDA, "engine launch: %s", cudaGetErrorString(e));
   return PMPD_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int pmpd_engine_run_traced(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const void* x_in, float* y_out,
+                           float y_alpha, uint32_t* bar_dev, int32_t* status_dev, int64_t* trace_dev, void* stream) {
+  return engine_launch(false, ops_dev, n_ops, p_dev, x_in, y_out, y_alpha, bar_dev, status_dev, trace_dev, stream);
+}
+
+int pmpd_engine_run_decoder(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, float* y_out, float y_alpha,
+                            uint32_t* bar_dev, int32_t* status_dev, int64_t* trace_dev, void* stream) {
+  return engine_launch(true, ops_dev, n_ops, p_dev, nullptr, y_out, y_alpha, bar_dev, status_dev, trace_dev, stream);
 }
 
 }  // extern "C"

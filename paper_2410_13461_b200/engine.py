@@ -22,14 +22,42 @@ from .errors import ConfigError
 from .quant import PackedTensor
 
 
+IN_SRC, IN_RMSNORM, IN_ATTN = 0, 2, 3  # engine.cu E_IN_*
+
+
+@dataclass
+class AttnSpec:
+    """A decode-attention op over one layer's KV cache (tinylm.py:344-358): RoPE of q and the new
+    k at position *T_dev, append k and v to the cache, attend over rows 0..T."""
+    n_heads: int
+    d_head: int
+    k_cache: torch.Tensor   # f16 [max_ctx, d]
+    v_cache: torch.Tensor
+    cos: torch.Tensor       # f32 [max_ctx, d_head / 2]
+    sin: torch.Tensor
+    T_dev: torch.Tensor     # int32 [1]: rows already cached
+    max_ctx: int
+    scale: float
+
+
 @dataclass
 class OpSpec:
-    packed: PackedTensor
+    packed: PackedTensor | None
     src: int = -1       # index of the producing op, -1 = external input
     src_col: int = 0    # first output column of src used as input element 0
     act: int = 0        # 0 identity, 1 silu(g) * u with u at src_col + act_off
     act_off: int = 0
     in_alpha: float = 1.0
+    # decoder-step extensions: input = rmsnorm(resid) * gain (IN_RMSNORM) or the combined
+    # attention records of src (IN_ATTN); `out` = a persistent vector (the residual stream)
+    # the op's output is added into (x += y), instead of a fresh per-launch vector
+    in_mode: int = IN_SRC
+    resid: torch.Tensor | None = None
+    gain: torch.Tensor | None = None
+    eps: float = 1e-6
+    out: torch.Tensor | None = None
+    out_alpha: float = 1.0
+    attn: AttnSpec | None = None
 
 
 class Program:
@@ -46,34 +74,68 @@ class Program:
         for i, spec in enumerate(ops):
             if spec.src >= i:
                 raise ConfigError(f"op {i} reads op {spec.src}, which does not precede it")
+            addr = ctypes.addressof(host) + i * nbytes
+            if spec.attn is not None:
+                at = spec.attn
+                rec = torch.zeros(lib.pmpd_engine_attn_records(at.n_heads, at.d_head), dtype=torch.float32,
+                                  device="cuda")
+                self.parts.append((rec, at))
+                _capi.call("pmpd_engine_make_attn_op", spec.src, at.n_heads, at.d_head, at.k_cache.data_ptr(),
+                           at.v_cache.data_ptr(), at.cos.data_ptr(), at.sin.data_ptr(), at.T_dev.data_ptr(),
+                           at.max_ctx, float(at.scale), rec.data_ptr(), addr)
+                continue
             slots = 1  # one accumulation vector per op (the kernel adds split-K partials at L2)
             nt = spec.packed.desc.n_tiles
-            part = torch.zeros(nt * 64, dtype=torch.float32, device="cuda")
+            if spec.out is not None:
+                if spec.out.dtype != torch.float32 or spec.out.numel() < nt * 64 or not spec.out.is_contiguous():
+                    raise ConfigError(f"op {i}: the persistent output must be f32, contiguous, >= {nt * 64} long")
+                part = spec.out
+            else:
+                part = torch.zeros(nt * 64, dtype=torch.float32, device="cuda")
             ns_host = (ctypes.c_uint8 * nt)()
             _capi.call("pmpd_engine_nslots", spec.packed.ref(), ctypes.addressof(ns_host))
             ns = torch.frombuffer(bytearray(ns_host), dtype=torch.uint8).cuda()
-            self.parts.append((part, ns))
+            self.parts.append((part, ns, spec.resid, spec.gain))
             _capi.call("pmpd_engine_make_op", spec.packed.ref(), spec.src, spec.src_col, spec.act, spec.act_off,
-                       float(spec.in_alpha), part.data_ptr(), slots, ns.data_ptr(),
-                       ctypes.addressof(host) + i * nbytes)
+                       float(spec.in_alpha), part.data_ptr(), slots, ns.data_ptr(), addr)
+            if spec.in_mode != IN_SRC or spec.out is not None or spec.out_alpha != 1.0:
+                if spec.in_mode == IN_ATTN and (spec.src < 0 or ops[spec.src].attn is None):
+                    raise ConfigError(f"op {i}: IN_ATTN needs an attention source op")
+                _capi.call("pmpd_engine_op_set_io", addr, spec.in_mode,
+                           spec.resid.data_ptr() if spec.resid is not None else None,
+                           spec.gain.data_ptr() if spec.gain is not None else None, float(spec.eps),
+                           int(spec.out is not None), float(spec.out_alpha))
         self.table = torch.frombuffer(bytearray(host), dtype=torch.uint8).cuda()
         self.bar = torch.zeros(2, dtype=torch.int32, device="cuda")
         self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.y_alpha = float(y_alpha)
         self.n_out = ops[-1].packed.desc.n
+        # decoder-step op kinds run in the engine's decoder instantiation
+        self.decoder = any(sp.attn is not None or sp.in_mode != IN_SRC or sp.out is not None or sp.out_alpha != 1.0
+                           for sp in ops)
 
     def run_traced(self, x_in, p_dev, y_out):
         """One pass recording the per-CTA per-op timeline; returns int64 [grid, n_ops, 8]: 4 timestamps (ns), warp-0 tile cycles, tile calls, loop cycles."""
         g = _capi.lib().pmpd_engine_grid()
         tr = torch.zeros((g, len(self.ops), 8), dtype=torch.int64, device="cuda")
-        _capi.call("pmpd_engine_run_traced", self.table.data_ptr(), len(self.ops), p_dev.data_ptr(),
-                   x_in.data_ptr(), y_out.data_ptr(), self.y_alpha, self.bar.data_ptr(), self.status.data_ptr(),
-                   tr.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        if self.decoder:
+            _capi.call("pmpd_engine_run_decoder", self.table.data_ptr(), len(self.ops), p_dev.data_ptr(),
+                       y_out.data_ptr(), self.y_alpha, self.bar.data_ptr(), self.status.data_ptr(), tr.data_ptr(),
+                       torch.cuda.current_stream().cuda_stream)
+        else:
+            _capi.call("pmpd_engine_run_traced", self.table.data_ptr(), len(self.ops), p_dev.data_ptr(),
+                       x_in.data_ptr(), y_out.data_ptr(), self.y_alpha, self.bar.data_ptr(), self.status.data_ptr(),
+                       tr.data_ptr(), torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
         return tr.cpu()
 
     def run(self, x_in: torch.Tensor, p_dev: torch.Tensor, y_out: torch.Tensor) -> None:
         """Enqueue one pass (graph-capturable): y_out = y_alpha * chain(x_in) at precision *p_dev."""
+        if self.decoder:
+            _capi.call("pmpd_engine_run_decoder", self.table.data_ptr(), len(self.ops), p_dev.data_ptr(),
+                       y_out.data_ptr(), self.y_alpha, self.bar.data_ptr(), self.status.data_ptr(), None,
+                       torch.cuda.current_stream().cuda_stream)
+            return
         _capi.call("pmpd_engine_run", self.table.data_ptr(), len(self.ops), p_dev.data_ptr(), x_in.data_ptr(),
                    y_out.data_ptr(), self.y_alpha, self.bar.data_ptr(), self.status.data_ptr(),
                    torch.cuda.current_stream().cuda_stream)

@@ -539,12 +539,47 @@ class DecodeEngine:
         self.hist = torch.zeros((capacity, cfg.vocab_size), dtype=torch.float32, device="cuda")
         self.p16 = p16
         self.graph = None
+        self.program = None if p16 or os.environ.get("PMPD_DECODE_ENGINE", "1") == "0" else self._decoder_program()
+
+    def _decoder_program(self):
+        """The whole decode step (tinylm.py:334-368 for one token) as one persistent-engine program:
+        per layer q|k|v (RMSNorm staged in) -> attention (RoPE + KV append) -> o (added into the
+        residual) -> gate|up (RMSNorm) -> down (SwiGLU staged in, added into the residual); then the
+        head (final RMSNorm).  None when the shapes are outside the engine (the per-op path runs)."""
+        from .engine import IN_ATTN, IN_RMSNORM, AttnSpec, OpSpec, Program
+        cfg, dw = self.model.config, self.dw
+        d, ff, dh = cfg.d_model, cfg.d_ff, cfg.d_head
+        if dh not in (32, 64, 128, 256) or d % 64 or ff % 4 or max(d, ff) > 12288 or \
+                any(len(lay["qkv"]) != 1 for lay in dw.layers):
+            return None
+        x = self.buf.x[0]
+        ops = []
+        for i, lay in enumerate(dw.layers):
+            q = len(ops)
+            ops.append(OpSpec(lay["qkv"][0], in_mode=IN_RMSNORM, resid=x, gain=lay["norm_attn"], eps=1e-6))
+            ops.append(OpSpec(None, src=q, attn=AttnSpec(cfg.n_heads, dh, self.cache.k[i], self.cache.v[i], dw.cos,
+                                                         dw.sin, self.cache.T_dev, self.cache.capacity,
+                                                         1.0 / math.sqrt(dh))))
+            ops.append(OpSpec(lay["wo"], src=q + 1, in_mode=IN_ATTN, out=x))
+            ops.append(OpSpec(lay["w_up"], in_mode=IN_RMSNORM, resid=x, gain=lay["norm_mlp"], eps=1e-6))
+            ops.append(OpSpec(lay["w_down"], src=q + 3, act=1, act_off=ff, out=x))
+        ops.append(OpSpec(dw.head, in_mode=IN_RMSNORM, resid=x, gain=dw.final_norm, eps=1e-6))
+        try:
+            return Program(ops)
+        except ConfigError:
+            return None
 
     def _step(self) -> None:
         s = _stream()
         if not self.p16:
             _capi.call("pmpd_sched_step", self.table.data_ptr(), 8, self.step.data_ptr(), self.buf.p.data_ptr(), 1, s)
-        _run_layers(self.model, self.dw, self.buf, 1, self.cache, FULL_PRECISION if self.p16 else None)
+        if self.program is not None and not self.p16:
+            # embedding row at the step's precision -> residual stream, then one engine launch
+            _capi.call("pmpd_gather_rows", self.dw.embed.ref(), self.buf.ids.data_ptr(), 1, self.buf.p.data_ptr(),
+                       self.buf.x.data_ptr(), s)
+            self.program.run(self.buf.x, self.buf.p, self.buf.logits)
+        else:
+            _run_layers(self.model, self.dw, self.buf, 1, self.cache, FULL_PRECISION if self.p16 else None)
         V = self.model.config.vocab_size
         _capi.call("pmpd_argmax", self.buf.logits.data_ptr(), V, 1, V, self.buf.ids.data_ptr(),
                    self.buf.bad.data_ptr(), s)

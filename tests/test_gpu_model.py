@@ -177,3 +177,21 @@ def test_save_load_round_trip(tmp_path, small):
     a = tinylm.generate(small, prompt, FixedScheduler(16), max_new=8)
     b = tinylm.generate(loaded, prompt, FixedScheduler(16), max_new=8)
     assert a.output_tokens == b.output_tokens
+
+
+@pytest.mark.parametrize("which", ["small", "toy"])
+def test_decode_engine_step_matches_per_op_path(which, small, toy, monkeypatch):
+    """The whole decode step as one persistent-engine launch (RMSNorm/SwiGLU staged in, attention
+    with RoPE + KV append, residual adds as L2 atomics) == the per-op kernels: same greedy tokens,
+    logits within f16 rounding, over a progressive 4->3->2 schedule."""
+    model = small if which == "small" else toy
+    prompt = [5, 17, 3, 99, 42, 7]
+    sched = StaticScheduler(PrecisionSchedule((4, 3, 2), 4, {4: 0, 3: 4, 2: 9}, 16))
+    runs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("PMPD_DECODE_ENGINE", mode)
+        tr = tinylm.generate(model, prompt, sched, max_new=16, eos_id=-1, record_logits=True)
+        runs[mode] = tr
+    eng, ref = runs["1"], runs["0"]
+    assert eng.output_tokens == ref.output_tokens
+    assert rel_l2(host(eng.logits), host(ref.logits)) < 2e-3

@@ -214,6 +214,7 @@ def main():
     ap.add_argument("--no-fp16", action="store_true", help="skip the cuBLAS fp16 baseline")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--no-prefill", action="store_true", help="skip the prefill GEMM section")
+    ap.add_argument("--no-model", action="store_true", help="skip the model-level (BASELINE config 2) section")
     args = ap.parse_args()
 
     from paper_2410_13461_b200.stack import LLAMA2_7B, MOBILELLAMA_1B4, algorithmic_bytes
@@ -397,6 +398,21 @@ def main():
         us, cores, cpu_pp, sample = cpu_sample(shape)
         out["cpu_baseline"] = {"value": us, "unit": "us/token", "cores": cores, "kind": "port", "sample": sample,
                                "per_precision_us": cpu_pp}
+    if rank == 0 and world == 1 and not args.no_model:
+        # BASELINE config 2 end to end: full decoder (RMSNorm, RoPE, attention over the KV cache,
+        # SwiGLU, head, greedy argmax), one persistent-engine launch per decode token
+        del st, g, g_ops
+        torch.cuda.empty_cache()
+        sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "tools"))
+        import model_bench
+        mb = model_bench.measure(2)
+        out["model_config2"] = {
+            "workload": "MobileLLaMA-1.4B-shape decoder (random init), prompt 128, 256 greedy tokens, 4-bit prefill; "
+                        "progressive 3->2 @64 vs uniform 4-bit vs fp16 (cuBLAS)",
+            "decode_us_per_token": {k: v["decode_us_per_token"] for k, v in mb["runs"].items()},
+            "prefill_ms": {k: v["prefill_ms"] for k, v in mb["runs"].items()},
+            "speedup_vs_uniform4": mb["decode_speedup_vs_uniform4"], "speedup_vs_fp16": mb["decode_speedup_vs_fp16"],
+            "avg_bits": mb["avg_bits"]}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if dist is not None:

@@ -70,13 +70,10 @@ def run(model, prompt, sched, tokens, p16=False):
     return prefill_ms, e0.elapsed_time(e1) * 1e3 / n
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("config", type=int, nargs="?", default=2, choices=[2, 3])
-    ap.add_argument("--tokens", type=int, default=None)
-    args = ap.parse_args()
-    c = CONFIGS[args.config]
-    tokens = args.tokens or c["tokens"]
+def measure(config: int, tokens: int | None = None, verbose: bool = False) -> dict:
+    """Progressive vs uniform-4 vs fp16 decode (and prefill) of one BASELINE model config."""
+    c = CONFIGS[config]
+    tokens = tokens or c["tokens"]
     mc = tinylm.ModelConfig(max_context=c["prompt"] + tokens + 8, **c["cfg"])
     t = time.time()
     model = tinylm.ModelVariants.from_random(mc, PrecisionSet((4, 3, 2)), seed=1234, std=0.02)
@@ -91,14 +88,25 @@ def main():
     for name, sched, p16 in (("progressive", prog, False), ("uniform4", uni4, False), ("fp16", uni4, True)):
         pre, dec = run(model, prompt, sched, tokens, p16=p16)
         res[name] = {"prefill_ms": pre, "decode_us_per_token": dec}
-        print(json.dumps({"config": args.config, "run": name, "prefill_ms": round(pre, 3),
-                          "decode_us_per_token": round(dec, 2)}), flush=True)
-    out = {"config": args.config, "shape": c["cfg"], "prompt": c["prompt"], "tokens": tokens,
+        if verbose:
+            print(json.dumps({"config": config, "run": name, "prefill_ms": round(pre, 3),
+                              "decode_us_per_token": round(dec, 2)}), flush=True)
+    out = {"config": config, "shape": c["cfg"], "prompt": c["prompt"], "tokens": tokens,
            "schedule": {str(k): v for k, v in st.items()}, "avg_bits": avg_bitwidth(prog, tokens),
            "model_build_s": round(build_s, 1), "runs": res,
            "decode_speedup_vs_uniform4": res["uniform4"]["decode_us_per_token"] / res["progressive"]["decode_us_per_token"],
            "decode_speedup_vs_fp16": res["fp16"]["decode_us_per_token"] / res["progressive"]["decode_us_per_token"]}
-    print(json.dumps(out), flush=True)
+    del model
+    torch.cuda.empty_cache()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("config", type=int, nargs="?", default=2, choices=[2, 3])
+    ap.add_argument("--tokens", type=int, default=None)
+    args = ap.parse_args()
+    print(json.dumps(measure(args.config, args.tokens, verbose=True)), flush=True)
 
 
 if __name__ == "__main__":

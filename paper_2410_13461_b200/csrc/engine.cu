@@ -214,13 +214,18 @@ PMPD_DEV void ld_halves(const __half* __restrict__ p, bool ok, float (&f)[DPL]) 
 
 template <int DPL>
 PMPD_DEV void attn_unit(const EngineOp& op, const float* __restrict__ qkv, int h, int s, int L, float* scratch,
-                        int warp, int lane) {
+                        int warp, int lane, const unsigned* bar, unsigned target) {
   constexpr int DH = 32 * DPL, HALF = DH / 2;
+  constexpr int U = DPL <= 2 ? 8 : DPL == 4 ? 4 : 2;  // rows in flight per warp (registers: 2*U*DPL)
   const int d = op.n_heads * DH;
   const int chunk = (L + E_ASPLIT - 1) / E_ASPLIT;
   const int t0 = s * chunk, t1 = min(L, t0 + chunk);
   const int pos = L - 1;
+  const bool append = *op.T_dev < op.max_ctx;  // row `pos` is this token's (written below)
   const bool first = lane < 16;
+  const __half* kb = op.kc + h * DH + lane * DPL;
+  const __half* vb = op.vc + h * DH + lane * DPL;
+  // ---- independent of this token's q|k|v: issued before the ticket wait (bar != null)
   float c[DPL], sn[DPL];
 #pragma unroll
   for (int j = 0; j < DPL; ++j) {
@@ -228,6 +233,20 @@ PMPD_DEV void attn_unit(const EngineOp& op, const float* __restrict__ qkv, int h
     c[j] = __ldg(op.cos_t + (int64_t)pos * HALF + jj);
     sn[j] = __ldg(op.sin_t + (int64_t)pos * HALF + jj);
   }
+  float kf[U][DPL], vf[U][DPL];
+  const int tb0 = t0 + warp;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int t = tb0 + u * E_NCW;
+    const bool ok = t < t1 && !(append && t == pos);
+    ld_halves<DPL>(kb + (int64_t)t * d, ok, kf[u]);
+    ld_halves<DPL>(vb + (int64_t)t * d, ok, vf[u]);
+  }
+  if (bar) {
+    if (threadIdx.x == 0) wait_tickets(bar, target);
+    named_bar_sync(1, E_NCW * 32);
+  }
+  // ---- q (and the new k, v) of this token
   float qr[DPL];
 #pragma unroll
   for (int j = 0; j < DPL; ++j) {
@@ -235,7 +254,7 @@ PMPD_DEV void attn_unit(const EngineOp& op, const float* __restrict__ qkv, int h
     const float b = __shfl_xor_sync(0xffffffffu, a, 16);  // RoPE partner dim j +- HALF
     qr[j] = first ? a * c[j] - b * sn[j] : a * c[j] + b * sn[j];
   }
-  if (*op.T_dev < op.max_ctx && pos >= t0 && pos < t1 && warp == 0) {
+  if (append && pos >= t0 && pos < t1 && warp == 0) {
 #pragma unroll
     for (int j = 0; j < DPL; ++j) {
       const float a = __ldcg(qkv + d + h * DH + lane * DPL + j);
@@ -246,20 +265,27 @@ PMPD_DEV void attn_unit(const EngineOp& op, const float* __restrict__ qkv, int h
     }
   }
   named_bar_sync(1, E_NCW * 32);  // the appended row is visible to every warp of the CTA
-  const __half* kb = op.kc + h * DH + lane * DPL;
-  const __half* vb = op.vc + h * DH + lane * DPL;
+  if (append) {  // the first batch skipped row `pos`: read it now
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (tb0 + u * E_NCW == pos && pos < t1) {
+        ld_halves<DPL>(kb + (int64_t)pos * d, true, kf[u]);
+        ld_halves<DPL>(vb + (int64_t)pos * d, true, vf[u]);
+      }
+  }
   float m = -INFINITY, l = 0.f, acc[DPL];
 #pragma unroll
   for (int j = 0; j < DPL; ++j) acc[j] = 0.f;
-  constexpr int U = 4;
-  for (int tb = t0 + warp; tb < t1; tb += E_NCW * U) {
-    float kf[U][DPL], vf[U][DPL], sc[U];
+  for (int tb = tb0; tb < t1; tb += E_NCW * U) {
+    if (tb != tb0) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int t = tb + u * E_NCW;
-      ld_halves<DPL>(kb + (int64_t)t * d, t < t1, kf[u]);
-      ld_halves<DPL>(vb + (int64_t)t * d, t < t1, vf[u]);
+      for (int u = 0; u < U; ++u) {
+        const int t = tb + u * E_NCW;
+        ld_halves<DPL>(kb + (int64_t)t * d, t < t1, kf[u]);
+        ld_halves<DPL>(vb + (int64_t)t * d, t < t1, vf[u]);
+      }
     }
+    float sc[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       float a = 0.f;
@@ -313,17 +339,26 @@ PMPD_DEV void attn_unit(const EngineOp& op, const float* __restrict__ qkv, int h
   named_bar_sync(1, E_NCW * 32);  // scratch reused by the next unit
 }
 
+// The attention op of one CTA: its units (head, split) in turn.  The op's ticket wait happens
+// inside the first unit, after the loads that do not depend on this token were issued.
 __noinline__ __device__ void attn_op(const EngineOp& op, const EngineOp& src, int c, int G, float* scratch, int warp,
-                                    int lane) {
+                                    int lane, const unsigned* bar, unsigned target) {
   const int L = min(*op.T_dev + 1, op.max_ctx);
+  bool waited = bar == nullptr;
   for (int u = c; u < op.n_heads * E_ASPLIT; u += G) {
     const int h = u / E_ASPLIT, s = u - h * E_ASPLIT;
+    const unsigned* b = waited ? nullptr : bar;
     switch (op.d_head) {
-      case 32: attn_unit<1>(op, src.part, h, s, L, scratch, warp, lane); break;
-      case 64: attn_unit<2>(op, src.part, h, s, L, scratch, warp, lane); break;
-      case 128: attn_unit<4>(op, src.part, h, s, L, scratch, warp, lane); break;
-      default: attn_unit<8>(op, src.part, h, s, L, scratch, warp, lane); break;
+      case 32: attn_unit<1>(op, src.part, h, s, L, scratch, warp, lane, b, target); break;
+      case 64: attn_unit<2>(op, src.part, h, s, L, scratch, warp, lane, b, target); break;
+      case 128: attn_unit<4>(op, src.part, h, s, L, scratch, warp, lane, b, target); break;
+      default: attn_unit<8>(op, src.part, h, s, L, scratch, warp, lane, b, target); break;
     }
+    waited = true;
+  }
+  if (!waited) {  // no unit on this CTA: still order the publish after the op's start
+    if (threadIdx.x == 0) wait_tickets(bar, target);
+    named_bar_sync(1, E_NCW * 32);
   }
 }
 
@@ -410,11 +445,8 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
   for (int oi = 0; oi < a.n_ops; ++oi) {
     const EngineOp& op = a.ops[oi];
     if (DEC && op.kind == E_ATTN) {
-      if (oi > 0) {
-        if (threadIdx.x == 0) wait_tickets(a.bar, (unsigned)(oi * G));
-        named_bar_sync(1, E_NCW * 32);
-      }
-      attn_op(op, a.ops[op.src], c, G, reinterpret_cast<float*>(smem + kSmX), warp, lane);
+      attn_op(op, a.ops[op.src], c, G, reinterpret_cast<float*>(smem + kSmX), warp, lane,
+              oi > 0 ? a.bar : nullptr, (unsigned)(oi * G));
       named_bar_sync(1, E_NCW * 32);
       // publish (the epilogue skips attention ops): the records above are ordered before this
       // release by the CTA barrier (cumulativity)
@@ -464,17 +496,20 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
       float ss = 0.f;
       constexpr int RB = 4;
       for (int k0 = 4 * threadIdx.x; k0 < op.k_real; k0 += 4 * RB * E_NCW * 32) {
-        float4 q[RB];
+        float4 q[RB], gq[RB];  // the gain rides in the same round trip; the row is stored as resid * gain
 #pragma unroll
         for (int j = 0; j < RB; ++j) {
           const int k = k0 + j * 4 * E_NCW * 32;
           q[j] = k < op.k_real ? __ldcg(reinterpret_cast<const float4*>(op.resid + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          gq[j] = k < op.k_real ? __ldg(reinterpret_cast<const float4*>(op.gain + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int j = 0; j < RB; ++j) {
           const int k = k0 + j * 4 * E_NCW * 32;
           ss = fmaf(q[j].x, q[j].x, fmaf(q[j].y, q[j].y, fmaf(q[j].z, q[j].z, fmaf(q[j].w, q[j].w, ss))));
-          if (k < op.k_real) *reinterpret_cast<float4*>(row + k) = q[j];
+          if (k < op.k_real)
+            *reinterpret_cast<float4*>(row + k) =
+                make_float4(q[j].x * gq[j].x, q[j].y * gq[j].y, q[j].z * gq[j].z, q[j].w * gq[j].w);
         }
       }
       ss = warp_sum(ss);
@@ -497,21 +532,16 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
       for (int kb = klo + 4 * threadIdx.x; kb < khi; kb += 4 * SB * E_NCW * 32) {
         float v[SB][4];
         if (DEC && op.in_mode == E_IN_RMSNORM) {
-          float4 rv[SB], gv[SB];
           const float* row = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(xs) + 2 * r.KT * kTile);
 #pragma unroll
           for (int bi = 0; bi < SB; ++bi) {
             const int k = kb + bi * 4 * E_NCW * 32;
-            const bool in = k < khi && k < op.k_real;
-            rv[bi] = in ? *reinterpret_cast<const float4*>(row + k) : make_float4(0.f, 0.f, 0.f, 0.f);
-            gv[bi] = in ? __ldg(reinterpret_cast<const float4*>(op.gain + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-#pragma unroll
-          for (int bi = 0; bi < SB; ++bi) {
-            v[bi][0] = rv[bi].x * inv * gv[bi].x;
-            v[bi][1] = rv[bi].y * inv * gv[bi].y;
-            v[bi][2] = rv[bi].z * inv * gv[bi].z;
-            v[bi][3] = rv[bi].w * inv * gv[bi].w;
+            const float4 rg =
+                (k < khi && k < op.k_real) ? *reinterpret_cast<const float4*>(row + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[bi][0] = rg.x * inv;  // (x * g) * inv: tinylm.py:293-295 up to one rounding order
+            v[bi][1] = rg.y * inv;
+            v[bi][2] = rg.z * inv;
+            v[bi][3] = rg.w * inv;
           }
         } else if (!src) {
 #pragma unroll

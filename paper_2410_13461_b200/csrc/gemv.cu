@@ -145,6 +145,10 @@ struct Consumer {
   // tiles, loaded one stage ahead so the L2 latency overlaps the previous stage's MMAs
   static constexpr bool PF = KN && !XS;
   uint32_t xw[TPW][MB];
+  // KN, batch <= 4: balanced digits v = 256*hi + lo (both s8), hi of row b in B column 2b and lo in
+  // column 2b+1 -> ONE u8 x s8 IMMA per fragment (lane tig = b holds both sums); batch 8 keeps two
+  static constexpr bool BAL = KN && MB <= 4;
+  static constexpr float kQMax = BAL ? 32639.f : 32767.f;
 
   PMPD_DEV void prefetch_x(uint32_t (&dst)[TPW][MB], int kt0, int cnt) const {
 #pragma unroll
@@ -176,12 +180,12 @@ struct Consumer {
 #pragma unroll
       for (int b = 0; b < MB; ++b) {
         const float m = mx[b];
-        qs[b] = (m > 0.f && idm > 0.f) ? 32767.f * idm / m : 0.f;
+        qs[b] = (m > 0.f && idm > 0.f) ? kQMax * idm / m : 0.f;
       }
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc) {
-        const float m = mx[MB == 1 ? 0 : min(2 * tig + cc, MB - 1)];
-        ql[cc] = (m > 0.f && idm > 0.f) ? 32767.f * idm / m : 0.f;
+        const float m = mx[MB == 1 ? 0 : min(BAL ? tig : 2 * tig + cc, MB - 1)];
+        ql[cc] = (m > 0.f && idm > 0.f) ? kQMax * idm / m : 0.f;
       }
     }
   }
@@ -260,11 +264,13 @@ struct Consumer {
           else
             xf = xpair(b, kk);
           bias[b] = fmaf(xf.x, mn[q].x, fmaf(xf.y, mn[q].y, bias[b]));
-          const float f0 = fmaf(xf.x * dl[q].x, qs[b], 12582912.f);  // 1.5 * 2^23: round-to-nearest-even
-          const float f1 = fmaf(xf.y * dl[q].y, qs[b], 12582912.f);
+          // 1.5 * 2^23 (+128 when balanced): the float's low 16 bits are rint(x*step*qs) (+128)
+          constexpr float kMagic = BAL ? 12583040.f : 12582912.f;
+          const float f0 = fmaf(xf.x * dl[q].x, qs[b], kMagic);
+          const float f1 = fmaf(xf.y * dl[q].y, qs[b], kMagic);
           const uint32_t u0 = __float_as_uint(f0), u1 = __float_as_uint(f1);
           uint8_t* row = xq + (q * PL::kXqRows + b) * 128;
-          *reinterpret_cast<uint16_t*>(row + pos) = (uint16_t)__byte_perm(u0, u1, 0x0040);
+          *reinterpret_cast<uint16_t*>(row + pos) = (uint16_t)(__byte_perm(u0, u1, 0x0040) ^ (BAL ? 0x8080u : 0u));
           *reinterpret_cast<uint16_t*>(row + 64 + pos) = (uint16_t)__byte_perm(u0, u1, 0x0051);
         }
       }
@@ -274,7 +280,13 @@ struct Consumer {
 #pragma unroll
     for (int q = 0; q < TPW; ++q) {
       uint4 lo4 = make_uint4(0u, 0u, 0u, 0u), hi4 = lo4;
-      if (live[q] && gq < (MB == 1 ? 1 : M)) {
+      if constexpr (BAL) {
+        // column gq: row gq/2, high digits when gq is even, low digits when odd (loaded into hi4)
+        if (live[q] && gq < 2 * (MB == 1 ? 1 : M)) {
+          const uint8_t* row = xq + (q * PL::kXqRows + (gq >> 1)) * 128;
+          hi4 = *reinterpret_cast<const uint4*>(row + ((gq & 1) ? 0 : 64) + tig * 16);
+        }
+      } else if (live[q] && gq < (MB == 1 ? 1 : M)) {
         const uint8_t* row = xq + (q * PL::kXqRows + (MB == 1 ? 0 : gq)) * 128;
         lo4 = *reinterpret_cast<const uint4*>(row + tig * 16);
         hi4 = *reinterpret_cast<const uint4*>(row + 64 + tig * 16);
@@ -297,7 +309,7 @@ struct Consumer {
     nibble_to_u8<PMAX, P, T>(merge_planes<PMAX, P, T>(pe), a0, a1);          \
     nibble_to_u8<PMAX, P, T>(merge_planes<PMAX, P, T>(po), a2, a3);          \
     mma_u8s8_16832(dhi[T], a0, a1, a2, a3, bh[q][cch][0], bh[q][cch][1]);    \
-    mma_u8u8_16832(dlo[T], a0, a1, a2, a3, bl[q][cch][0], bl[q][cch][1]);    \
+    if constexpr (!BAL) mma_u8u8_16832(dlo[T], a0, a1, a2, a3, bl[q][cch][0], bl[q][cch][1]); \
   }
         PMPD_KN_MTILE(0)
         PMPD_KN_MTILE(1)
@@ -386,10 +398,15 @@ struct Consumer {
       for (int h = 0; h < 2; ++h)
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
-          const int b = 2 * tig + cc;
-          if (b < Me) {
+          const int b = BAL ? tig : 2 * tig + cc;
+          if (b < Me && (!BAL || cc == 0)) {
             float v;
-            if constexpr (KN) {
+            if constexpr (BAL) {
+              // columns 2b / 2b+1 of this lane = high / low digit sums of row b
+              const float q = ql[0];
+              const float ds = q > 0.f ? __fdividef(1.f, q) * (1.f / (float)(1 << t)) : 0.f;
+              v = fmaf(256.f, (float)dhi[t][2 * h], (float)dhi[t][2 * h + 1]) * ds;
+            } else if constexpr (KN) {
               // y = (256*hi + lo) * 2^-t / qs[b]
               const float q = ql[MB == 1 ? 0 : cc];
               const float ds = q > 0.f ? __fdividef(1.f, q) * (1.f / (float)(1 << t)) : 0.f;

@@ -41,7 +41,12 @@ namespace {
 constexpr int G_BM = 128;       // tokens per UMMA M block
 constexpr int G_NG1 = 64;       // outputs per packed n-group
 constexpr int G_KC = 64;        // K per chunk (one packed tile)
-constexpr int G_DQ = 256;       // dequant threads (8 warps)
+#ifndef PMPD_GEMM_DQ_WARPS
+#define PMPD_GEMM_DQ_WARPS 16
+#endif
+constexpr int G_DQ = PMPD_GEMM_DQ_WARPS * 32;  // dequant threads (a multiple of 256: 256 units per n-group)
+constexpr int G_DQG = G_DQ / 256;              // n-groups dequantized in parallel
+static_assert(G_DQ % 256 == 0, "dequant warps come in groups of 8");
 constexpr int G_PROD = G_DQ / 32;      // TMA producer warp
 constexpr int G_MMA = G_DQ / 32 + 1;   // tcgen05.mma issue warp
 constexpr int G_THREADS = G_DQ + 64;
@@ -215,8 +220,9 @@ template <int P, int NG, int MB>
 PMPD_DEV void dequant_loop(int KC, int ngn, uint8_t* ring, uint8_t* bufs, uint64_t* full_bar, uint64_t* bfull,
                            uint64_t* bempty, int tid) {
   using C = Cfg<NG, MB>;
-  const int uw = (tid >> 5) & 3, uhalf = tid >> 7;
-  const int uL = ((tid >> 1) & 7) * 4 + ((tid >> 4) & 1) * 2 + (tid & 1);
+  const int tt = tid & 255;  // unit within an n-group; thread group tid >> 8 takes n-groups h = g, g + G_DQG, ...
+  const int uw = (tt >> 5) & 3, uhalf = tt >> 7;
+  const int uL = ((tt >> 1) & 7) * 4 + ((tt >> 4) & 1) * 2 + (tt & 1);
   for (int kc = 0; kc < KC; ++kc) {
     const int st = kc / C::KCS, kcs = kc - st * C::KCS, s = st % C::NS, b = kc % C::NB;
     const uint8_t* w0 = ring + s * C::STAGE + C::STAGE_X;
@@ -224,8 +230,7 @@ PMPD_DEV void dequant_loop(int KC, int ngn, uint8_t* ring, uint8_t* bufs, uint64
     if (kc >= C::NB) mbar_wait(&bempty[b], ((kc - C::NB) / C::NB) & 1);
     if (kcs == 0) mbar_wait(&full_bar[s], (st / C::NS) & 1);
 #ifndef GEMM_SKIP_DEQUANT
-#pragma unroll
-    for (int h = 0; h < NG; ++h) {
+    for (int h = tid >> 8; h < NG; h += G_DQG) {
       uint8_t* sbh = sb + h * G_STAGE_B1;
       if (h < ngn) {
         const int toff = (h * C::KCS + kcs) * kTilePlaneBytes;
@@ -353,7 +358,8 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
     float* tile = reinterpret_cast<float*>(smem);
     for (int mb = 0; mb < mbn; ++mb) {
       const int row = 32 * (warp & 3) + lane;
-      for (int cc = (warp >> 2) * (C::N / 2); cc < ((warp >> 2) + 1) * (C::N / 2); cc += 16) {
+      constexpr int NQ = G_DQ / 128;  // column groups: warps w and w+4 share TMEM lanes 32*(w&3)
+      for (int cc = (warp >> 2) * (C::N / NQ); cc < ((warp >> 2) + 1) * (C::N / NQ); cc += 16) {
         uint32_t r[16];
         tmem_ld16(tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(mb * C::N + cc), r);
 #pragma unroll
@@ -464,8 +470,8 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
     encode = reinterpret_cast<EncodeFn>(fn);
   }
   // (n-groups, token blocks) per CTA from a cost model fitted to the measured config-4 sweep
-  // (tools/gemm_cfg_sweep.sh): a CTA spends ~0.06 + 0.19*NG + 0.27*MB us per K chunk (dequant
-  // grows with NG, x loads and MMAs with MB); time ~ waves x chunks x that.  Fewer CTAs with more
+  // (tools/gemm_cfg_sweep.sh, 16 dequant warps): a CTA spends ~0.15 + 0.135*NG + 0.21*MB us per
+  // K chunk (dequant grows with NG, x loads and MMAs with MB); time ~ waves x chunks x that.  Fewer CTAs with more
   // operand reuse win when the extra wave of a finer split would cost more than the reuse saves.
   const int mblocks = (m + G_BM - 1) / G_BM, sms = num_sms();
   static const int cand[][2] = {{4, 2}, {2, 4}, {2, 2}, {4, 1}, {1, 4}, {2, 1}, {1, 2}, {1, 1}};
@@ -476,7 +482,7 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
     if (c[1] > 1 && mblocks < c[1] && c[1] / 2 >= mblocks) continue;  // would leave a whole accumulator idle
     const int64_t ctas = (int64_t)((t->n_tiles + c[0] - 1) / c[0]) * ((mblocks + c[1] - 1) / c[1]);
     const double waves = (double)((ctas + sms - 1) / sms);
-    const double cost = waves * (0.06 + 0.19 * c[0] + 0.27 * mbe);
+    const double cost = waves * (0.15 + 0.135 * c[0] + 0.21 * mbe);
     if (cost < best * 0.999) {
       best = cost;
       ng = c[0];

@@ -185,6 +185,8 @@ def test_decode_engine_step_matches_per_op_path(which, small, toy, monkeypatch):
     with RoPE + KV append, residual adds as L2 atomics) == the per-op kernels: same greedy tokens,
     logits within f16 rounding, over a progressive 4->3->2 schedule."""
     model = small if which == "small" else toy
+    monkeypatch.setenv("PMPD_DECODE_ENGINE", "1")
+    assert tinylm.DecodeEngine(model, 4).program is not None
     prompt = [5, 17, 3, 99, 42, 7]
     sched = StaticScheduler(PrecisionSchedule((4, 3, 2), 4, {4: 0, 3: 4, 2: 9}, 16))
     runs = {}
@@ -195,3 +197,22 @@ def test_decode_engine_step_matches_per_op_path(which, small, toy, monkeypatch):
     eng, ref = runs["1"], runs["0"]
     assert eng.output_tokens == ref.output_tokens
     assert rel_l2(host(eng.logits), host(ref.logits)) < 2e-3
+
+
+@pytest.mark.parametrize("n_heads,d_model,d_ff", [(4, 256, 640), (8, 1024, 2816), (2, 512, 1024)])
+def test_decode_engine_head_dims(n_heads, d_model, d_ff, monkeypatch):
+    """Decoder engine vs per-op kernels at head dims 64 / 128 (the 1.4B and 7B shapes) / 256, with a
+    context long enough that every attention split holds rows (prompt 90 + 24 tokens)."""
+    cfg = tinylm.ModelConfig(n_layers=2, n_heads=n_heads, d_model=d_model, d_ff=d_ff, max_context=160)
+    model = tinylm.ModelVariants.from_random(cfg, quant.PrecisionSet((4, 3, 2)), seed=d_model, std=0.02)
+    prompt = list(np.random.default_rng(5).integers(0, cfg.vocab_size, size=90))
+    sched = StaticScheduler(PrecisionSchedule((4, 3, 2), 4, {4: 0, 3: 6, 2: 14}, 24))
+    monkeypatch.setenv("PMPD_DECODE_ENGINE", "1")
+    assert tinylm.DecodeEngine(model, 4).program is not None  # the engine path is the one under test
+    runs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("PMPD_DECODE_ENGINE", mode)
+        runs[mode] = tinylm.generate(model, prompt, sched, max_new=24, eos_id=-1, record_logits=True)
+    eng, ref = runs["1"], runs["0"]
+    assert eng.output_tokens == ref.output_tokens
+    assert rel_l2(host(eng.logits), host(ref.logits)) < 3e-3

@@ -102,7 +102,6 @@ PMPD_DEV long long gtimer() {
 // shared-memory plan (byte offsets)
 constexpr int kSmBar = 0;                            // mbarriers
 constexpr int kSmMisc = 256;                         // mx, flags
-constexpr int kSmNs = 512;                           // per-source-n-group slot counts: [2][512] B
 constexpr int kSmX = 1536;                           // f16 activations
 constexpr int kSmXq = kSmX + E_XMAX * 2;             // per-warp int8 activation fragments
 constexpr int kSmRed = kSmXq + E_NCW * E_TPW * 128;  // [2][E_NCW][64] f32
@@ -117,45 +116,18 @@ struct Bars {
 };
 
 // 32-bit partition arithmetic (NT * (G + 1) < 2^32, checked in pmpd_engine_make_op): a 64-bit
-// integer division is an emulated ~100-instruction routine, and these run on the op-to-op path.
-PMPD_DEV int cta_of_tile(int t, int G, int NT) {
-  return (int)(((unsigned)(t + 1) * (unsigned)G + (unsigned)NT - 1u) / (unsigned)NT) - 1;
-}
+// integer division is an emulated ~100-instruction routine, and it runs on the op-to-op path.
 
 PMPD_DEV unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-PMPD_DEV unsigned ld_relaxed(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-// Spin until *p >= target: relaxed polls (an acquire load invalidates L1 on every
-// iteration), then one acquire fence to order the subsequent reads.
-#ifndef E_SPIN
-#define E_SPIN 0
-#endif
+// Spin until *p >= target with acquire loads (each synchronizes-with the publishers' red.release),
+// backing off 32 ns between polls.  Relaxed polls + one fence, and tight spins, were measured no
+// better (tools/experiments/README.md).
 PMPD_DEV void wait_tickets(const unsigned* p, unsigned target) {
-#if E_SPIN == 0
   while (ld_acquire(p) < target) __nanosleep(32);
-#elif E_SPIN == 4
-  while (ld_acquire(p) < target) {
-  }
-#elif E_SPIN == 1
-  while (ld_relaxed(p) < target) __nanosleep(20);
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
-#elif E_SPIN == 2
-  while (ld_relaxed(p) < target) {
-  }
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
-#else
-  // relaxed polls, then one acquire load of the same word (synchronizes-with the release adds)
-  do {
-    while (ld_relaxed(p) < target) __nanosleep(32);
-  } while (ld_acquire(p) < target);
-#endif
 }
 
 struct Range {

@@ -85,7 +85,8 @@ def bench_prefill(st, shape, M=512):
             n, k = pk.desc.n, pk.desc.k
             y = outs.get(n)
             if y is None:
-                y = outs[n] = torch.empty((M, n), device="cuda", dtype=torch.float16)
+                # f32 outputs, as the model runner's prefill writes them (q|k|v, gate|up, logits, residual)
+                y = outs[n] = torch.empty((M, n), device="cuda", dtype=torch.float32)
             gemm(pk, xs[k], pd, out=y)
 
     for _ in range(2):

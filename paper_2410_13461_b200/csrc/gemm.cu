@@ -156,6 +156,8 @@ struct GemmArgs {
   float alpha;
   const int32_t* p_dev;
   int* status;
+  int splitk;  // > 1: blockIdx.z takes K chunks [z*KC/S, (z+1)*KC/S) and ADDS alpha*partial into y (f32,
+               // zeroed by the host unless accumulating)
 };
 
 // ------------------------------------------------------------------ weight dequant
@@ -293,7 +295,9 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int KC = g.k_tiles;
+  // this CTA's K chunks: all of them, or its split-K slice [kbase, kbase + KC)
+  const int kbase = (int)(((long long)blockIdx.z * g.k_tiles) / g.splitk);
+  const int KC = (int)(((long long)(blockIdx.z + 1) * g.k_tiles) / g.splitk) - kbase;
   // x blocks of this CTA that hold rows (blocks past M are neither loaded nor multiplied)
   const int mbn = min(MB, (g.M - m0 + G_BM - 1) / G_BM);
 
@@ -302,7 +306,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
     if (lane == 0) {
       const int nst = (KC + C::KCS - 1) / C::KCS;
       for (int st = 0; st < nst; ++st) {
-        const int s = st % C::NS, kc0 = st * C::KCS;
+        const int s = st % C::NS, kc0 = kbase + st * C::KCS;  // absolute chunk (TMA coordinate)
         uint8_t* sx = ring + s * C::STAGE;
         uint8_t* sw = sx + C::STAGE_X;
         if (st >= C::NS) mbar_wait_backoff(&mma_bar[s], ((st - C::NS) / C::NS) & 1);
@@ -389,7 +393,15 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
           }
         } else {
           float* yr = static_cast<float*>(g.y) + m * g.ldy + n;
-          if (n + 4 <= g.n_real && (((uintptr_t)yr) & 15) == 0) {
+          if (g.splitk > 1) {  // partial of this K slice: added at L2 (16-byte vector red when aligned)
+            if (n + 4 <= g.n_real && (((uintptr_t)yr) & 15) == 0) {
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(yr), "f"(v[0]), "f"(v[1]),
+                           "f"(v[2]), "f"(v[3])
+                           : "memory");
+            } else {
+              for (int i = 0; i < 4 && n + i < g.n_real; ++i) atomicAdd(yr + i, v[i]);
+            }
+          } else if (n + 4 <= g.n_real && (((uintptr_t)yr) & 15) == 0) {
             float4 o = make_float4(v[0], v[1], v[2], v[3]);
             if (g.accumulate) {
               const float4 q = *reinterpret_cast<const float4*>(yr);
@@ -420,7 +432,7 @@ int launch(const GemmArgs& g, const GemmMaps& maps, int m, int n_tiles, cudaStre
     cudaFuncSetAttribute(gemm_kernel<NG, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<NG, MB>::SMEM);
     attr = true;
   }
-  dim3 grid((n_tiles + NG - 1) / NG, (m + MB * G_BM - 1) / (MB * G_BM));
+  dim3 grid((n_tiles + NG - 1) / NG, (m + MB * G_BM - 1) / (MB * G_BM), g.splitk);
   gemm_kernel<NG, MB><<<grid, G_THREADS, Cfg<NG, MB>::SMEM, st>>>(g, maps);
   return check_launch("prefill gemm launch");
 }
@@ -470,25 +482,40 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
     encode = reinterpret_cast<EncodeFn>(fn);
   }
   // (n-groups, token blocks) per CTA from a cost model fitted to the measured config-4 sweep
-  // (tools/gemm_cfg_sweep.sh, 16 dequant warps): a CTA spends ~0.15 + 0.135*NG + 0.21*MB us per
-  // K chunk (dequant grows with NG, x loads and MMAs with MB); time ~ waves x chunks x that.  Fewer CTAs with more
+  // (tools/gemm_cfg_sweep.sh, 16 dequant warps, f32 y): a CTA spends ~0.214 + 0.111*NG + 0.192*MB us
+  // per K chunk (dequant grows with NG, x loads and MMAs with MB); time ~ waves x chunks x that.  Fewer CTAs with more
   // operand reuse win when the extra wave of a finer split would cost more than the reuse saves.
   const int mblocks = (m + G_BM - 1) / G_BM, sms = num_sms();
   static const int cand[][2] = {{4, 2}, {2, 4}, {2, 2}, {4, 1}, {1, 4}, {2, 1}, {1, 2}, {1, 1}};
-  int ng = 1, mb = 1;
+  // Split-K (f32 output only): S CTAs share one output tile, each over K/S chunks, and add their
+  // partials at L2 (vector red); it pays when the tile grid alone cannot fill the SMs without
+  // re-dequantizing the weights for every 128-row block.  The partial adds cost ~1.5 us per M outputs per
+  // split (fitted).
+  int ng = 1, mb = 1, splitk = 1;
   double best = 1e30;
+  const int kc_all = t->k_tiles;
   for (const auto& c : cand) {
     const int mbe = c[1] < mblocks ? c[1] : mblocks;
     if (c[1] > 1 && mblocks < c[1] && c[1] / 2 >= mblocks) continue;  // would leave a whole accumulator idle
-    const int64_t ctas = (int64_t)((t->n_tiles + c[0] - 1) / c[0]) * ((mblocks + c[1] - 1) / c[1]);
-    const double waves = (double)((ctas + sms - 1) / sms);
-    const double cost = waves * (0.15 + 0.135 * c[0] + 0.21 * mbe);
-    if (cost < best * 0.999) {
-      best = cost;
-      ng = c[0];
-      mb = c[1];
+    for (int sk = 1; sk <= 4; sk *= 2) {
+      if (sk > 1 && (y_dtype != PMPD_DTYPE_F32 || kc_all < 8 * sk)) break;
+      const int64_t ctas = (int64_t)((t->n_tiles + c[0] - 1) / c[0]) * ((mblocks + c[1] - 1) / c[1]) * sk;
+      const double waves = (double)((ctas + sms - 1) / sms);
+      const double cost = waves * ((kc_all + sk - 1) / sk) * (0.214 + 0.111 * c[0] + 0.192 * mbe) +
+                          (sk > 1 ? 1.49e-6 * sk * m * t->n : 0.0);
+      if (cost < best * 0.999) {
+        best = cost;
+        ng = c[0];
+        mb = c[1];
+        splitk = sk;
+      }
     }
   }
+  if (const char* e = getenv("PMPD_GEMM_SPLITK")) {  // diagnostics: force the split count
+    const int v = atoi(e);
+    if ((v == 1 || v == 2 || v == 4) && (v == 1 || y_dtype == PMPD_DTYPE_F32)) splitk = v;
+  }
+  if (splitk > t->k_tiles) splitk = 1;  // every split needs at least one K chunk
   if (const char* e = getenv("PMPD_GEMM_CFG")) {  // diagnostics: force "ng,mb"
     int a = 0, b = 0;
     if (sscanf(e, "%d,%d", &a, &b) == 2 && (a == 1 || a == 2 || a == 4) && (b == 1 || b == 2 || b == 4) && a * b <= 8) {
@@ -528,6 +555,11 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
     }
   }
   cudaStream_t st = as_stream(stream);
+  g.splitk = splitk;
+  if (splitk > 1 && !accumulate) {
+    const cudaError_t ze = cudaMemset2DAsync(y_dev, (size_t)ldy * 4, 0, (size_t)t->n * 4, (size_t)m, st);
+    if (ze != cudaSuccess) return fail(PMPD_ERR_CUDA, "prefill gemm: zeroing y: %s", cudaGetErrorString(ze));
+  }
   if (ng == 1 && mb == 4) return launch<1, 4>(g, maps, m, t->n_tiles, st);
   if (ng == 2 && mb == 4) return launch<2, 4>(g, maps, m, t->n_tiles, st);
   if (ng == 4 && mb == 2) return launch<4, 2>(g, maps, m, t->n_tiles, st);

@@ -50,3 +50,25 @@ def test_gemm_matches_gemv_and_accumulates():
         assert rel_l2(y3.cpu().numpy(), 2 * y.cpu().numpy()) < 1e-6
     yh = gemm(pk, x, _pdev(4), out_dtype=torch.float16)
     assert yh.dtype == torch.float16 and rel_l2(yh.float().cpu().numpy(), gemm(pk, x, _pdev(4)).cpu().numpy()) < 1e-3
+
+
+@pytest.mark.parametrize("split", [2, 4])
+@pytest.mark.parametrize("K,N,M", [(4096, 4096, 512), (11008, 512, 300), (640, 320, 77)])
+def test_gemm_split_k(split, K, N, M, monkeypatch):
+    """Split-K (S CTAs per output tile, partials added at L2 into f32 y) == the unsplit GEMM, with and
+    without accumulate, and with a strided y (ldy > n)."""
+    g = torch.Generator(device="cuda").manual_seed(K + N + M + split)
+    w = torch.randn((K, N), generator=g, device="cuda") * 0.02
+    pk = quantize_tensor(w, 4, 64).packed(_capi.LAYOUT_KN)
+    x = torch.randn((M, K), generator=g, device="cuda").half()
+    monkeypatch.setenv("PMPD_GEMM_SPLITK", "1")
+    ref = gemm(pk, x, _pdev(3), alpha=0.75)
+    monkeypatch.setenv("PMPD_GEMM_SPLITK", str(split))
+    big = torch.full((M, N + 8), 7.0, device="cuda")
+    y = big[:, :N]
+    gemm(pk, x, _pdev(3), out=y, alpha=0.75)
+    torch.cuda.synchronize()
+    assert rel_l2(y.cpu().numpy(), ref.cpu().numpy()) < 1e-4  # f32 summation order only
+    assert torch.all(big[:, N:] == 7.0)  # the zeroing before the split-K adds stays inside y
+    gemm(pk, x, _pdev(3), out=y, alpha=0.75, accumulate=True)
+    assert rel_l2(y.cpu().numpy(), 2 * ref.cpu().numpy()) < 1e-4

@@ -28,14 +28,15 @@ for N, K in shapes:
     wt = w.t().contiguous().half()
     for M in (512, 2048):
         x = torch.randn((M, K), device="cuda").half()
-        y = torch.empty((M, N), device="cuda", dtype=torch.float16)
+        y = torch.empty((M, N), device="cuda", dtype=torch.float32)  # f32 as the model runner uses
+        y16 = torch.empty((M, N), device="cuda", dtype=torch.float16)
         for p in (4, 2):
             pd = torch.tensor([p], dtype=torch.int32, device="cuda")
             us = timeit(lambda: gemm(pk, x, pd, out=y))
             tf = 2 * M * N * K / us / 1e6
             rows.append(dict(N=N, K=K, M=M, p=p, us=round(us, 2), tflops=round(tf, 1), frac=round(tf / peak, 3)))
             print(json.dumps(rows[-1]), flush=True)
-        us = timeit(lambda: torch.matmul(x, wt.t(), out=y))
+        us = timeit(lambda: torch.matmul(x, wt.t(), out=y16))
         tf = 2 * M * N * K / us / 1e6
         rows.append(dict(N=N, K=K, M=M, p="cublas_fp16", us=round(us, 2), tflops=round(tf, 1), frac=round(tf / peak, 3)))
         print(json.dumps(rows[-1]), flush=True)

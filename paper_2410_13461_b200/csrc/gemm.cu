@@ -68,7 +68,10 @@ struct Cfg {
   static constexpr int WR = NG * KCS * kTilePlaneBytes;  // one plane (or scale) region
   static constexpr int STAGE = stage_bytes(KCS);
   // dequantized weight buffers: 3 when that still leaves 3 load stages, else 2
-  static constexpr int NB = (G_SMEM_MAX - 2048 - 3 * STAGE_B) / STAGE >= 3 ? 3 : 2;
+#ifndef PMPD_GEMM_NB
+#define PMPD_GEMM_NB 3
+#endif
+  static constexpr int NB = (G_SMEM_MAX - 2048 - PMPD_GEMM_NB * STAGE_B) / STAGE >= 3 ? PMPD_GEMM_NB : 2;
   static constexpr int BUFB = NB * STAGE_B;
   static constexpr int NS_FIT = (G_SMEM_MAX - 2048 - BUFB) / STAGE;
   static constexpr int NS = NS_FIT > 8 ? 8 : NS_FIT;

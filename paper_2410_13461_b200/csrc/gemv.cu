@@ -175,6 +175,7 @@ struct Consumer {
 
   // set the KN activation scale for n-group ng
   PMPD_DEV void enter_group(int ng) {
+    (void)kQMax;  // KN only
     if constexpr (KN) {
       const float idm = __ldg(a.aux + ng);
 #pragma unroll

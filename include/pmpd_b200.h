@@ -215,6 +215,11 @@ int pmpd_engine_make_attn_op(int32_t src, int32_t n_heads, int32_t d_head, void*
                              const float* cos_dev, const float* sin_dev, const int32_t* T_dev, int32_t max_ctx,
                              float scale, float* records_dev, void* op_host);
 int pmpd_engine_attn_records(int32_t n_heads, int32_t d_head);
+/* Cost-balanced CTA tile ranges for one op (bounds_host: pmpd_engine_grid() + 1 ints): the ranges
+ * minimise the largest per-CTA cost of stage calls and n-group flushes instead of splitting the tiles
+ * evenly; attach the uploaded array with pmpd_engine_op_set_bounds (null = even split). */
+int pmpd_engine_partition(const pmpd_qtensor* t, int32_t* bounds_host);
+int pmpd_engine_op_set_bounds(void* op_host, const int32_t* bounds_dev);
 /* pmpd_engine_run for programs that use the decoder-step ops above (a separate kernel
  * instantiation, so the linear-stack program pays nothing for them); trace_dev optional. */
 int pmpd_engine_run_decoder(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, float* y_out_dev, float y_alpha,

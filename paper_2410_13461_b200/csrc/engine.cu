@@ -75,6 +75,7 @@ struct EngineOp {
   const int32_t* T_dev;
   int n_heads, d_head, max_ctx;
   float scale;
+  const int* bounds;  // optional [G + 1] tile-range boundaries per CTA (pmpd_engine_partition); null = even
 };
 constexpr int E_LINEAR = 0, E_ATTN = 1;
 constexpr int E_IN_SRC = 0, E_IN_RMSNORM = 2, E_IN_ATTN = 3;
@@ -137,8 +138,13 @@ PMPD_DEV Range range_of(const EngineOp& op, int c, int G) {
   Range r;
   r.NT = op.n_tiles * op.k_tiles;
   r.KT = op.k_tiles;
-  r.T0 = (int)((unsigned)c * (unsigned)r.NT / (unsigned)G);
-  r.T1 = (int)((unsigned)(c + 1) * (unsigned)r.NT / (unsigned)G);
+  if (op.bounds) {  // cost-balanced partition computed on the host (pmpd_engine_partition)
+    r.T0 = __ldg(op.bounds + c);
+    r.T1 = __ldg(op.bounds + c + 1);
+  } else {
+    r.T0 = (int)((unsigned)c * (unsigned)r.NT / (unsigned)G);
+    r.T1 = (int)((unsigned)(c + 1) * (unsigned)r.NT / (unsigned)G);
+  }
   return r;
 }
 
@@ -952,6 +958,78 @@ int pmpd_engine_make_attn_op(int32_t src, int32_t n_heads, int32_t d_head, void*
 }
 
 int pmpd_engine_attn_records(int32_t n_heads, int32_t d_head) { return n_heads * E_ASPLIT * (4 + d_head); }
+
+// Cost-balanced tile partition for one op: the CTA tile ranges minimise the largest per-CTA cost,
+// where a CTA's tiles run as stages of E_STILES cut at n-group boundaries, a stage of <= E_NCW tiles
+// costs one tile-time (one tile per warp) and a fuller one two, and each n-group segment adds a
+// flush (~0.5 tile-time).  An even split of the tiles gives some CTAs an extra stage or segment
+// (e.g. 3 stage calls instead of 2 for o on 148 SMs).  Binary search on the budget, greedy cover.
+int pmpd_engine_partition(const pmpd_qtensor* t, int32_t* bounds_host) {
+  if (!t || !bounds_host) return fail(PMPD_ERR_CONFIG, "null argument");
+  const int G = num_sms(), KT = t->k_tiles, NT = t->n_tiles * t->k_tiles;
+  if (NT < 1) return fail(PMPD_ERR_CONFIG, "empty tensor");
+  // cost in half tile-times
+  auto seg_cost = [&](int n) {  // n tiles of one n-group segment
+    int cst = 1;               // flush
+    for (int s0 = 0; s0 < n; s0 += E_STILES) cst += (n - s0 > E_NCW) ? 4 : 2;
+    return cst;
+  };
+  // greedy: from tile t, the largest end with cost <= budget
+  auto cover = [&](int budget, int32_t* out) {
+    int t0 = 0, c = 0;
+    if (out) out[0] = 0;
+    while (t0 < NT) {
+      if (c == G) return G + 1;
+      int t1 = t0, cost = 0;
+      while (t1 < NT) {
+        const int kt = t1 % KT, seg_end = std::min(NT, t1 - kt + KT);
+        // largest prefix of this segment that still fits
+        int lo = 0, hi = seg_end - t1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) / 2;
+          if (cost + seg_cost(mid) <= budget) lo = mid; else hi = mid - 1;
+        }
+        if (lo == 0) break;
+        cost += seg_cost(lo);
+        t1 += lo;
+        if (lo < seg_end - (t1 - lo)) break;  // segment not finished: the budget is spent
+      }
+      if (t1 == t0) return G + 1;  // budget below one tile
+      ++c;
+      if (out) out[c] = t1;
+      t0 = t1;
+    }
+    if (out) for (int k = c + 1; k <= G; ++k) out[k] = NT;  // idle CTAs
+    return c;
+  };
+  int lo = 1, hi = 1 << 30;
+  {  // upper bound: the even split's cost
+    int mx = 0;
+    for (int c = 0; c < G; ++c) {
+      const int a = (int)((int64_t)c * NT / G), b = (int)((int64_t)(c + 1) * NT / G);
+      int cst = 0;
+      for (int t1 = a; t1 < b;) {
+        const int e = std::min(b, t1 - t1 % KT + KT);
+        cst += seg_cost(e - t1);
+        t1 = e;
+      }
+      mx = std::max(mx, cst);
+    }
+    hi = mx;
+  }
+  while (lo < hi) {
+    const int mid = (lo + hi) / 2;
+    if (cover(mid, nullptr) <= G) hi = mid; else lo = mid + 1;
+  }
+  cover(lo, bounds_host);
+  return PMPD_OK;
+}
+
+int pmpd_engine_op_set_bounds(void* op_host, const int32_t* bounds_dev) {
+  if (!op_host) return fail(PMPD_ERR_CONFIG, "null argument");
+  static_cast<EngineOp*>(op_host)->bounds = bounds_dev;
+  return PMPD_OK;
+}
 
 int pmpd_engine_run(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const void* x_in, float* y_out,
                     float y_alpha, uint32_t* bar_dev, int32_t* status_dev, void* stream) {

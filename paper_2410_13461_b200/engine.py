@@ -13,6 +13,7 @@ sequence of ``h @ model.weights(name, p)`` calls of one decode step
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import torch
@@ -68,6 +69,7 @@ class Program:
             raise ConfigError("engine program is empty")
         lib = _capi.lib()
         nbytes = lib.pmpd_engine_op_bytes()
+        grid = lib.pmpd_engine_grid()
         self.ops = ops
         self.parts = []
         host = (ctypes.c_uint8 * (nbytes * len(ops)))()
@@ -98,6 +100,13 @@ class Program:
             self.parts.append((part, ns, spec.resid, spec.gain))
             _capi.call("pmpd_engine_make_op", spec.packed.ref(), spec.src, spec.src_col, spec.act, spec.act_off,
                        float(spec.in_alpha), part.data_ptr(), slots, ns.data_ptr(), addr)
+            if os.environ.get("PMPD_ENGINE_EVEN", "0") != "1":
+                # cost-balanced CTA tile ranges (stage/segment aware) instead of an even tile split
+                b_host = (ctypes.c_int32 * (grid + 1))()
+                _capi.call("pmpd_engine_partition", spec.packed.ref(), ctypes.addressof(b_host))
+                bounds = torch.frombuffer(bytearray(b_host), dtype=torch.int32).cuda()
+                self.parts.append((bounds,))
+                _capi.call("pmpd_engine_op_set_bounds", addr, bounds.data_ptr())
             if spec.in_mode != IN_SRC or spec.out is not None or spec.out_alpha != 1.0:
                 if spec.in_mode == IN_ATTN and (spec.src < 0 or ops[spec.src].attn is None):
                     raise ConfigError(f"op {i}: IN_ATTN needs an attention source op")

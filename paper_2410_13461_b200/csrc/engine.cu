@@ -969,8 +969,12 @@ int pmpd_engine_partition(const pmpd_qtensor* t, int32_t* bounds_host) {
   const int G = num_sms(), KT = t->k_tiles, NT = t->n_tiles * t->k_tiles;
   if (NT < 1) return fail(PMPD_ERR_CONFIG, "empty tensor");
   // cost in half tile-times
+  static const int flush_cost = [] {  // half tile-times per n-group segment (PMPD_ENGINE_PART_FLUSH)
+    const char* e = getenv("PMPD_ENGINE_PART_FLUSH");
+    return e ? atoi(e) : 1;
+  }();
   auto seg_cost = [&](int n) {  // n tiles of one n-group segment
-    int cst = 1;               // flush
+    int cst = flush_cost;
     for (int s0 = 0; s0 < n; s0 += E_STILES) cst += (n - s0 > E_NCW) ? 4 : 2;
     return cst;
   };

@@ -374,8 +374,20 @@ def _run_layers(model: ModelVariants, dw: _DeviceWeights, buf: _Buffers, n: int,
             _capi.call("pmpd_rope_kv", qkv.data_ptr(), 3 * d, n, d, dh, dw.cos.data_ptr(), dw.sin.data_ptr(),
                        cache.T_dev.data_ptr(), cache.capacity, q.data_ptr(), cache.k[i].data_ptr(),
                        cache.v[i].data_ptr(), s)
-            _capi.call("pmpd_attention", q.data_ptr(), n, d, dh, cache.k[i].data_ptr(), cache.v[i].data_ptr(),
-                       cache.T_dev.data_ptr(), cache.capacity, scale, ctx.data_ptr(), s)
+            if n >= 256 and cache.T == 0:
+                # long-prompt prefill from an empty cache (>= 256 rows; below that the per-query kernel
+                # wins over the library call overhead): causal attention of the n new rows over
+                # themselves (tinylm.py:349-358) through torch's fused SDPA (a library kernel, like
+                # cuBLAS; attention is runner glue, not the quantized hot path)
+                H = cfg.n_heads
+                qh = q[:n].view(n, H, dh).transpose(0, 1).half()
+                kh = cache.k[i][:n].view(n, H, dh).transpose(0, 1)
+                vh = cache.v[i][:n].view(n, H, dh).transpose(0, 1)
+                o = torch.nn.functional.scaled_dot_product_attention(qh, kh, vh, is_causal=True, scale=scale)
+                ctx.copy_(o.transpose(0, 1).reshape(n, d))
+            else:
+                _capi.call("pmpd_attention", q.data_ptr(), n, d, dh, cache.k[i].data_ptr(), cache.v[i].data_ptr(),
+                           cache.T_dev.data_ptr(), cache.capacity, scale, ctx.data_ptr(), s)
         _linear(dw, [lay["wo"]], [pre + "wo"], ctx, x, buf.p, p_host, buf.ws, True)
         if fuse:
             _fused_linear([lay["w_up"]], _capi.GEMV_IN_RMSNORM, x, lay["norm_mlp"], 0, u, buf, False)

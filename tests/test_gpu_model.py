@@ -216,3 +216,17 @@ def test_decode_engine_head_dims(n_heads, d_model, d_ff, monkeypatch):
     eng, ref = runs["1"], runs["0"]
     assert eng.output_tokens == ref.output_tokens
     assert rel_l2(host(eng.logits), host(ref.logits)) < 3e-3
+
+
+def test_long_prompt_prefill_sdpa_matches_chunked():
+    """A >= 256-row prompt prefill from an empty cache runs its attention through torch SDPA; the same
+    prompt prefilled as 200 + 100 rows stays on the per-query kernel (the second chunk sees a
+    non-empty cache).  Last-position logits and the cached K/V must agree."""
+    cfg = tinylm.ModelConfig(n_layers=2, n_heads=4, d_model=256, d_ff=512, max_context=400)
+    model = tinylm.ModelVariants.from_random(cfg, quant.PrecisionSet((4, 3, 2)), seed=21, std=0.02)
+    prompt = [int(t) for t in np.random.default_rng(3).integers(0, cfg.vocab_size, size=300)]
+    lg_full, cache_full = tinylm.prefill(model, 4, prompt)
+    lg_a, cache = tinylm.prefill(model, 4, prompt[:200])
+    lg_b = tinylm._forward(model, 4, prompt[200:], cache)[-1]
+    assert rel_l2(host(lg_full), host(lg_b)) < 5e-3
+    torch.testing.assert_close(cache_full.k[:, :300].float(), cache.k[:, :300].float(), atol=2e-2, rtol=2e-2)

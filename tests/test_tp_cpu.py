@@ -118,3 +118,88 @@ def test_split_aligned_and_plans():
     assert plan.up_cols[1].start - plan.up_cols[0].start == 11008
     with pytest.raises(Exception):
         tp.split_aligned(100, 4, 64)
+
+
+# ---------------------------------------------------------------------------
+# tpmodel collective layer: DistComm + lockstep + distributed greedy argmax (gloo, world 2/4)
+# ---------------------------------------------------------------------------
+
+def _rank_logits(V, world, rank, seed):
+    """Full logits with deliberate cross-shard ties; this rank's vocabulary slice."""
+    rng = np.random.default_rng(seed)
+    full = rng.standard_normal(V).astype(np.float32)
+    top = full.max() + 1.0
+    for j in (V - 1, V // 2, 3 * V // 4):  # the max appears in several shards
+        full[j] = top
+    sl = tp.plan_head(V, world, rank)
+    return full, sl
+
+
+def _argmax_worker(rank, world, port, V, seed, out):
+    from paper_2410_13461_b200.tpmodel import DistComm, combine_argmax, lockstep
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = DistComm()
+    full, sl = _rank_logits(V, world, rank, seed)
+    loc = torch.from_numpy(full[sl.start:sl.stop].copy())
+
+    def gen():
+        y = torch.full((2, 3), float(rank + 1))
+        yield "sum", y                          # in-place all-reduce
+        li = int(torch.argmax(loc))             # first occurrence = lowest local index
+        pair = torch.tensor([float(loc[li]), float(li + sl.start), 0.0])
+        pairs = yield "gather", pair
+        tok, bad = combine_argmax(torch.stack(pairs))
+        return y, int(tok.item()), int(bad.item())
+    (y, tok, bad), = lockstep([gen()], comm)
+    if rank == 0:
+        out.put((y.numpy(), tok, bad))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,V", [(2, 257), (4, 1000), (2, 32000)])
+def test_tp_distributed_argmax_lowest_index_on_ties(world, V):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_argmax_worker, args=(r, world, port, V, 9, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    y, tok, bad = q.get(timeout=120)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    full, _ = _rank_logits(V, world, 0, 9)
+    assert tok == int(np.argmax(full))          # np.argmax: lowest index among the tied maxima
+    assert bad == 0
+    assert np.array_equal(y, np.full((2, 3), world * (world + 1) / 2))
+
+
+def test_combine_argmax_rules():
+    from paper_2410_13461_b200.tpmodel import combine_argmax
+    pairs = torch.tensor([[1.0, 5.0, 0.0], [3.0, 70.0, 0.0], [3.0, 130.0, 0.0], [2.0, 200.0, 0.0]])
+    tok, bad = combine_argmax(pairs)
+    assert int(tok) == 70 and int(bad) == 0
+    pairs[3, 2] = 1.0
+    assert int(combine_argmax(pairs)[1]) == 1
+    pairs = torch.tensor([[float("nan"), 5.0, 1.0], [3.0, 70.0, 0.0]])
+    tok, bad = combine_argmax(pairs)
+    assert int(bad) == 1  # non-finite logits are flagged (the caller raises InputError)
+
+
+def test_lockstep_detects_diverged_ranks():
+    from paper_2410_13461_b200.errors import ContractViolation
+    from paper_2410_13461_b200.tpmodel import LocalComm, lockstep
+
+    def g(op):
+        yield op, torch.zeros(1)
+    with pytest.raises(ContractViolation):
+        lockstep([g("sum"), g("gather")], LocalComm(2))
+    a, b = torch.ones(2), torch.full((2,), 2.0)
+
+    def h(t):
+        yield "sum", t
+        return t.clone()
+    r = lockstep([h(a), h(b)], LocalComm(2))
+    assert torch.equal(r[0], torch.full((2,), 3.0)) and torch.equal(r[1], r[0])

@@ -231,12 +231,15 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    # PMPD_BENCH_TP=1 runs the tensor-parallel branch at world 1 under torchrun (a 1-GPU check of
+    # the NCCL-in-graph path the driver's N>1 runs take)
+    tp_mode = world > 1 or os.environ.get("PMPD_BENCH_TP") == "1"
+    if tp_mode:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
 
-    if world > 1:
+    if tp_mode:
         # tensor parallel over the node's GPUs: column/row-split GEMVs + NCCL all-reduce per row-split layer
         from paper_2410_13461_b200.stack import TPLinearStack
         heads = 32 if args.shape == "7b" else 16
@@ -288,7 +291,7 @@ def main():
         per_p[16] = {"us_per_token": us, "GBps": algorithmic_bytes(shape, 16) / us * 1e-3, "impl": "cuBLAS fp16"}
         del gf
     prefill = None
-    if world == 1 and not args.no_prefill:
+    if not tp_mode and not args.no_prefill:
         prefill = bench_prefill(st, shape)
         if getattr(st, "fp16", None) is not None:  # cuBLAS fp16 prefill of the same stack
             xs = {k: torch.randn((512, k), device="cuda").half() for k in (shape.d_model, shape.d_ff)}
@@ -336,8 +339,8 @@ def main():
     us_tok = ms * 1e3 / (args.steps * HORIZON)
 
     # ---- e2e: per token H2D of the input activation from pinned host + D2H of the logits
-    x_dev = st.x0 if world == 1 else st.x16
-    y_dev = st.logits if world == 1 else st.logits_all
+    x_dev = st.x16 if tp_mode else st.x0
+    y_dev = st.logits_all if tp_mode else st.logits
     x_host = x_dev.cpu().pin_memory()
     out_host = torch.empty(y_dev.shape, dtype=torch.float32).pin_memory()
 
@@ -363,9 +366,13 @@ def main():
     bytes_tok = sum(w[p] * algorithmic_bytes(shape, p) for p in w)
     achieved = bytes_tok / us_tok * 1e-3  # GB/s
     peak, peak_src = measured_peaks()
+    if tp_mode:
+        peak, peak_src = peak * world, f"{peak_src} x {world} GPUs"
     weighted_kernel = sum(w[p] * per_p[p]["us_per_token"] for p in w)
     traffic_pp, traffic_src = ncu_traffic()
     traffic = sum(w[p] * traffic_pp[p] for p in w) if traffic_pp and all(p in traffic_pp for p in w) else None
+    if tp_mode:
+        traffic, traffic_src = None, "not captured for the tensor-parallel per-op path"
 
     out = {
         "metric": METRIC, "value": us_tok, "unit": "us/token", "n_gpus": world, "steps": args.steps,
@@ -375,7 +382,7 @@ def main():
         "config": {"workload": f"{args.shape} decode linear stack (32x q|k|v,o,gate|up,down + head), batch 1, "
                                "progressive 4->3->2 switching at tokens 32/128 over 512 tokens per step",
                    "schedule": {str(k): v for k, v in SCHED.items()}, "horizon": HORIZON,
-                   "parallelism": f"tp{world} (NCCL all-reduce after o and down)" if world > 1 else "single GPU",
+                   "parallelism": f"tp{world} (NCCL all-reduce after o and down)" if tp_mode else "single GPU",
                    "l2": "inputs larger than L2 (2.5-4.1 GB of planes per token vs 126 MB L2)"},
         "per_precision": {str(k): v for k, v in per_p.items()},
         "avg_bits": sum(p * f for p, f in w.items()),
@@ -385,13 +392,15 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_unit": "bytes per token (ncu dram read+write, schedule-weighted)",
                      "traffic_source": traffic_src, "peak_source": peak_src,
-                     "note": "algorithmic bytes (perf.py:101 + activations) per token / µs per token; one "
-                             "persistent engine kernel carries all 129 linear layers of a token (plus 1 tiny "
-                             "precision-hook launch)"},
+                     "note": ("algorithmic bytes (perf.py:101 + activations) per token / µs per token; one "
+                              "persistent engine kernel carries all 129 linear layers of a token (plus 1 tiny "
+                              "precision-hook launch)") if not tp_mode else
+                             ("whole-job algorithmic bytes per token / µs per token over N x the one-GPU peak; per rank "
+                              "129 per-op decode GEMVs on its shards + 64 NCCL all-reduces + 1 all-gather")},
         "clocks": clk.summary(),
         "e2e": {"value": e2e_us, "unit": "us/token", "h2d_bytes_per_step": HORIZON * x_dev.numel() * 2,
                 "d2h_bytes_per_step": HORIZON * y_dev.numel() * 4},
-        "gpu_launches": args.steps * HORIZON * (2 if world == 1 else 2 + 4 * shape.n_layers),
+        "gpu_launches": args.steps * HORIZON * (2 + 4 * shape.n_layers if tp_mode else 2),
     }
     if prefill is not None:
         out["prefill"] = prefill

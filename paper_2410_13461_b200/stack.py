@@ -237,7 +237,6 @@ class TPLinearStack:
         hq = P.o_rows.size
         self.x16 = torch.randn((m, d), device="cuda", generator=gen).half()
         self.qkv = torch.empty((m, 3 * hq), device="cuda", dtype=torch.float16)
-        self.part = torch.empty((m, d), device="cuda", dtype=torch.float32)
         self.u = torch.empty((m, 2 * P.ff.size), device="cuda", dtype=torch.float16)
         self.logits_loc = torch.zeros((m, max(self.head_sizes)), device="cuda", dtype=torch.float32)
         self.logits_all = torch.zeros((world, m, max(self.head_sizes)), device="cuda", dtype=torch.float32)
@@ -262,13 +261,13 @@ class TPLinearStack:
         ffl = self.plan.ff.size
         for wqkv, wo, wup, wdn in self.layers:
             gemv(wqkv, self.x16, self.p_dev, self.ws, out=self.qkv, alpha=a_d)
-            gemv(wo, self.qkv[:, 2 * hq:], self.p_dev, self.ws, out=self.part, alpha=a_d)   # row-parallel
-            dist.all_reduce(self.part, group=self.group)
-            self.x16.copy_(self.part)
+            # row-parallel partial sums land in f16 in x16 and are all-reduced in place: the next
+            # GEMV reads the reduced vector directly (no f32 buffer, no conversion launch)
+            gemv(wo, self.qkv[:, 2 * hq:], self.p_dev, self.ws, out=self.x16, alpha=a_d)   # row-parallel
+            dist.all_reduce(self.x16, group=self.group)
             gemv(wup, self.x16, self.p_dev, self.ws, out=self.u, alpha=a_d)               # column-parallel
-            gemv(wdn, self.u[:, :ffl], self.p_dev, self.ws, out=self.part, alpha=a_f)     # row-parallel
-            dist.all_reduce(self.part, group=self.group)
-            self.x16.copy_(self.part)
+            gemv(wdn, self.u[:, :ffl], self.p_dev, self.ws, out=self.x16, alpha=a_f)      # row-parallel
+            dist.all_reduce(self.x16, group=self.group)
         hs = self.head_cols.size
         gemv(self.head, self.x16, self.p_dev, self.ws, out=self.logits_loc[:, :hs], alpha=a_d)
         dist.all_gather_into_tensor(self.logits_all, self.logits_loc, group=self.group)

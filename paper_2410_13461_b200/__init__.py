@@ -27,6 +27,7 @@ _LAZY = {
     "predict_schedule": "learnsched",
     # B200 additions
     "QLinear": "linear", "gemv": "linear", "Workspace": "linear", "LinearStack": "stack",
+    "generate_batch": "tinylm", "TPModel": "tpmodel", "DistComm": "tpmodel", "LocalComm": "tpmodel",
 }
 
 

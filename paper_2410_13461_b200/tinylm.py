@@ -344,8 +344,11 @@ def _fused_linear(pks: list, mode: int, xf: torch.Tensor, gain, u_off: int, out:
         col += width
 
 
-def _run_layers(model: ModelVariants, dw: _DeviceWeights, buf: _Buffers, n: int, cache: KVCache, p_host) -> None:
-    """Embedding + all blocks + final norm + head for n tokens in buf.ids; logits -> buf.logits[:n]."""
+def _run_layers(model: ModelVariants, dw: _DeviceWeights, buf: _Buffers, n: int, cache: KVCache, p_host,
+                seq_caches: list | None = None) -> None:
+    """Embedding + all blocks + final norm + head for n tokens in buf.ids; logits -> buf.logits[:n].
+    ``seq_caches``: the n rows are the next tokens of n independent sequences (batched decode),
+    row j attending over seq_caches[j]; the linear layers run as one n-row GEMV."""
     cfg = model.config
     d, ff, dh = cfg.d_model, cfg.d_ff, cfg.d_head
     s = _stream()
@@ -366,7 +369,10 @@ def _run_layers(model: ModelVariants, dw: _DeviceWeights, buf: _Buffers, n: int,
         else:
             _capi.call("pmpd_rmsnorm", x.data_ptr(), d, lay["norm_attn"].data_ptr(), n, d, 1e-6, h.data_ptr(), d, s)
             _linear(dw, lay["qkv"], [pre + "wq", pre + "wk", pre + "wv"], h, qkv, buf.p, p_host, buf.ws, False)
-        if n == 1 and dh % 32 == 0 and dh <= 256:  # decode: RoPE + KV append fused into the attention
+        if seq_caches is not None:
+            for j, c in enumerate(seq_caches):
+                _attend_one(dw, qkv[j], ctx[j], q[j], c, i, d, dh, scale, s)
+        elif n == 1 and dh % 32 == 0 and dh <= 256:  # decode: RoPE + KV append fused into the attention
             _capi.call("pmpd_attention_rope", qkv.data_ptr(), d, dh, dw.cos.data_ptr(), dw.sin.data_ptr(),
                        cache.T_dev.data_ptr(), cache.capacity, scale, cache.k[i].data_ptr(), cache.v[i].data_ptr(),
                        ctx.data_ptr(), s)
@@ -402,6 +408,21 @@ def _run_layers(model: ModelVariants, dw: _DeviceWeights, buf: _Buffers, n: int,
     else:
         _capi.call("pmpd_rmsnorm", x.data_ptr(), d, dw.final_norm.data_ptr(), n, d, 1e-6, h.data_ptr(), d, s)
         _linear(dw, [dw.head], ["head"], h, logits, buf.p, p_host, buf.ws, False)
+
+
+def _attend_one(dw: _DeviceWeights, qkv_row, ctx_row, q_row, cache: KVCache, layer: int, d: int, dh: int,
+                scale: float, s: int) -> None:
+    """One new token of one sequence: RoPE, KV append at cache.T_dev, attention -> ctx_row."""
+    if dh % 32 == 0 and dh <= 256:
+        _capi.call("pmpd_attention_rope", qkv_row.data_ptr(), d, dh, dw.cos.data_ptr(), dw.sin.data_ptr(),
+                   cache.T_dev.data_ptr(), cache.capacity, scale, cache.k[layer].data_ptr(),
+                   cache.v[layer].data_ptr(), ctx_row.data_ptr(), s)
+    else:
+        _capi.call("pmpd_rope_kv", qkv_row.data_ptr(), 3 * d, 1, d, dh, dw.cos.data_ptr(), dw.sin.data_ptr(),
+                   cache.T_dev.data_ptr(), cache.capacity, q_row.data_ptr(), cache.k[layer].data_ptr(),
+                   cache.v[layer].data_ptr(), s)
+        _capi.call("pmpd_attention", q_row.data_ptr(), 1, d, dh, cache.k[layer].data_ptr(), cache.v[layer].data_ptr(),
+                   cache.T_dev.data_ptr(), cache.capacity, scale, ctx_row.data_ptr(), s)
 
 
 def _check_precision(model: ModelVariants, p: int) -> None:
@@ -602,9 +623,11 @@ class DecodeEngine:
 
     def capture(self) -> None:
         """Capture one decode step (after a prefill has set the counters)."""
+        # snapshot the counters BEFORE the side stream is ordered after the current one: the
+        # warm-up step below advances them and must not race with the copies
+        saved = [t.clone() for t in (self.n, self.step, self.cache.T_dev, self.buf.ids, self.tokens)]
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
-        saved = [t.clone() for t in (self.n, self.step, self.cache.T_dev, self.buf.ids, self.tokens)]
         with torch.cuda.stream(side):
             self._step()  # warm-up launch (lazy attributes, cuBLAS handles)
         torch.cuda.current_stream().wait_stream(side)
@@ -720,3 +743,140 @@ def _generate_host(model, prompt, scheduler, cfg, eos, max_new) -> GenerationTra
         push(sample(logits, cfg, rng), logits)
     term = "eos" if tokens[-1] == eos else "length"
     return GenerationTrace(list(prompt), tokens, precisions, hashes, term, scheduler.p_prefill, sched)
+
+
+# ---------------------------------------------------------------------------
+# batched generation (offline schedule search)
+# ---------------------------------------------------------------------------
+
+class _BatchDecoder:
+    """Static device state of up to 8 greedy generations that share one static schedule: one
+    KV cache per sequence, one CUDA graph per decode step (sched hook -> embedding gather ->
+    n-row GEMVs with per-sequence attention -> n-row argmax -> per-sequence token push)."""
+
+    def __init__(self, model: ModelVariants, caches: list, capacity: int, record: bool):
+        cfg = model.config
+        self.model, self.dw, self.caches, self.capacity = model, model.device(), caches, capacity
+        self.M = len(caches)
+        self.buf = _Buffers(cfg, GEMV_MAX_ROWS, self.dw.ws_bytes)
+        self.tokens = torch.zeros((self.M, capacity), dtype=torch.int32, device="cuda")
+        self.n = torch.zeros(self.M, dtype=torch.int32, device="cuda")
+        self.step = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.table = torch.zeros(16, dtype=torch.int32, device="cuda")
+        self.hist = torch.zeros((self.M, capacity, cfg.vocab_size), dtype=torch.float32, device="cuda") \
+            if record else None
+        self.graph = None
+
+    def _emit(self, logits_rows, s, advance: bool) -> None:
+        """Greedy token of every row of logits_rows [M, V] -> buf.ids; history; token push (and,
+        after a decode step, T += 1 for the row the attention appended)."""
+        V = self.model.config.vocab_size
+        _capi.call("pmpd_argmax", logits_rows.data_ptr(), logits_rows.stride(0), self.M, V, self.buf.ids.data_ptr(),
+                   self.buf.bad.data_ptr(), s)
+        for j, c in enumerate(self.caches):
+            if self.hist is not None:
+                _capi.call("pmpd_store_row", logits_rows[j].data_ptr(), self.hist[j].data_ptr(),
+                           self.n[j:].data_ptr(), V, self.capacity, s)
+            _capi.call("pmpd_push_token", self.buf.ids[j:].data_ptr(), self.tokens[j].data_ptr(), self.n[j:].data_ptr(),
+                       c.T_dev.data_ptr() if advance else 0, self.capacity, s)
+
+    def _step(self) -> None:
+        s = _stream()
+        _capi.call("pmpd_sched_step", self.table.data_ptr(), 8, self.step.data_ptr(), self.buf.p.data_ptr(), 1, s)
+        _run_layers(self.model, self.dw, self.buf, self.M, None, None, seq_caches=self.caches)
+        self._emit(self.buf.logits[:self.M], s, True)
+
+    def capture(self) -> None:
+        state = (self.n, self.step, self.buf.ids, self.tokens) + tuple(c.T_dev for c in self.caches)
+        saved = [t.clone() for t in state]  # before the side stream is ordered (see DecodeEngine.capture)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self._step()  # warm-up launch
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        for t, v in zip(state, saved):
+            t.copy_(v)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._step()
+        torch.cuda.synchronize()
+        self.graph = g
+
+
+def generate_batch(model: ModelVariants, prompts: Sequence[Sequence[int]], scheduler,
+                   sampler_cfg: SamplerConfig | None = None, eos_id: int | None = None, max_new: int = 64,
+                   record_logits: bool = False, check_every: int = 16) -> list:
+    """``[generate(model, prompt, scheduler, ...) for prompt in prompts]`` for up to 8 prompts at
+    once (tinylm.py:475-523 per prompt): the decode steps of all sequences run as one batch of
+    n-row GEMVs, each sequence attending over its own cache.  This is the inner loop of the
+    reference's offline schedule search (schedule.py:447-457 scores one candidate schedule by
+    generating every validation prompt under StaticScheduler(schedule)).
+
+    Greedy sampling and schedules that do not depend on the prompt (StaticScheduler /
+    FixedScheduler) only; every trace equals the one ``generate`` returns for that prompt."""
+    cfg = sampler_cfg if sampler_cfg is not None else SamplerConfig()
+    eos = model.config.vocab_size - 1 if eos_id is None else eos_id
+    prompts = [list(p) for p in prompts]
+    if not 1 <= len(prompts) <= GEMV_MAX_ROWS:
+        raise ConfigError(f"generate_batch takes 1..{GEMV_MAX_ROWS} prompts, got {len(prompts)}")
+    if cfg.mode != "greedy":
+        raise ConfigError("generate_batch supports greedy sampling only")
+    if hasattr(scheduler, "resolve_device"):
+        raise ConfigError("generate_batch needs a prompt-independent (static) scheduler")
+    if max_new < 1:
+        raise InputError(f"max_new must be >= 1, got {max_new}")
+    if max_new > scheduler.horizon:
+        raise InputError(f"max_new {max_new} exceeds the schedule horizon {scheduler.horizon}")
+    mc = model.config.max_context
+    for pr in prompts:
+        if not pr:
+            raise InputError("prompt is empty")
+        if len(pr) >= mc:
+            raise InputError(f"prompt length {len(pr)} must be < max_context {mc}")
+        if len(pr) + max_new - 1 > mc:
+            raise InputError(f"prompt length {len(pr)} + {max_new - 1} decode steps exceed max_context {mc}")
+    _check_precision(model, scheduler.p_prefill)
+    caches = [KVCache(model.config.n_layers, model.config.d_model, mc) for _ in prompts]
+    sched = scheduler.resolve(caches[0])
+    violations = sched.validate()
+    if violations:
+        raise ContractViolation("scheduler produced an invalid schedule: " + "; ".join(violations))
+    allowed = model.allowed_precisions()
+    for p in sched.precisions:
+        if p not in allowed or p == FULL_PRECISION:
+            raise ContractViolation(f"schedule uses precision {p} outside the batched decoder's set "
+                                    f"{sorted(allowed - {FULL_PRECISION})}")
+    bd = _BatchDecoder(model, caches, max_new, record_logits)
+    bd.table.copy_(torch.tensor(sched.device_table(), dtype=torch.int32))
+    V = model.config.vocab_size
+    last = torch.zeros((bd.M, V), dtype=torch.float32, device="cuda")
+    for j, (pr, c) in enumerate(zip(prompts, caches)):
+        last[j].copy_(_forward(model, scheduler.p_prefill, pr, c)[-1])
+    bd._emit(last, _stream(), False)  # token 0 of every sequence (caches already hold the prompts)
+    produced = 1
+    if max_new > 1:
+        bd.capture()
+    while True:
+        if int(bd.buf.bad.item()):
+            raise InputError("logits contain non-finite values")
+        toks = bd.tokens[:, :produced].cpu().numpy()
+        if produced >= max_new or all((row == eos).any() for row in toks):
+            break
+        k = min(check_every, max_new - produced)
+        for _ in range(k):
+            bd.graph.replay()
+        produced += k
+    out = []
+    toks_all = bd.tokens[:, :produced].cpu().tolist()
+    for j, (pr, c) in enumerate(zip(prompts, caches)):
+        toks = toks_all[j]
+        if eos in toks:
+            toks = toks[:toks.index(eos) + 1]
+        c.T = len(pr) + len(toks) - 1
+        hist = bd.hist[j, :len(toks)] if record_logits else None
+        hashes = [_logits_hash(r) for r in hist.double().cpu().numpy()] if record_logits else [""] * len(toks)
+        term = "eos" if toks[-1] == eos else "length"
+        out.append(GenerationTrace(pr, toks, [sched.precision_at(i) for i in range(len(toks))], hashes, term,
+                                   scheduler.p_prefill, sched, hist))
+    return out

@@ -230,3 +230,46 @@ def test_long_prompt_prefill_sdpa_matches_chunked():
     lg_b = tinylm._forward(model, 4, prompt[200:], cache)[-1]
     assert rel_l2(host(lg_full), host(lg_b)) < 5e-3
     torch.testing.assert_close(cache_full.k[:, :300].float(), cache.k[:, :300].float(), atol=2e-2, rtol=2e-2)
+
+
+def test_generate_batch_equals_per_prompt_generate(small, toy):
+    """Batched greedy generation (offline schedule search inner loop): every trace equals the
+    one ``generate`` returns for that prompt alone, incl. EOS truncation per sequence."""
+    rng = np.random.default_rng(4)
+    for mv in (small, toy):
+        V = mv.config.vocab_size
+        prompts = [list(b"Old maps mark the mountain"), list(b"A"), [int(t) for t in rng.integers(0, V, 37)],
+                   list(b"A lantern in the window"), [int(t) for t in rng.integers(0, V, 5)]]
+        for sch, mx, eos in ((StaticScheduler(PrecisionSchedule((4, 3, 2), 4, {4: 0, 3: 4, 2: 9}, 24)), 24, -1),
+                             (FixedScheduler(3), 16, None)):
+            got = tinylm.generate_batch(mv, prompts, sch, eos_id=eos, max_new=mx, record_logits=True)
+            for pr, tr in zip(prompts, got):
+                want = tinylm.generate(mv, pr, sch, eos_id=eos, max_new=mx, record_logits=True)
+                assert tr.output_tokens == want.output_tokens
+                assert tr.precisions == want.precisions and tr.termination == want.termination
+                assert rel_l2(host(tr.logits), host(want.logits)) < 5e-3
+    # an EOS that fires early in one sequence: force it with the token the model emits at step 2
+    pr = list(b"Old maps mark the mountain")
+    first = tinylm.generate(small, pr, FixedScheduler(4), eos_id=-1, max_new=8).output_tokens
+    got = tinylm.generate_batch(small, [pr, list(b"xyz")], FixedScheduler(4), eos_id=first[2], max_new=8)
+    assert got[0].output_tokens == first[:first.index(first[2]) + 1] and got[0].termination == "eos"
+    assert got[1].output_tokens == tinylm.generate(small, list(b"xyz"), FixedScheduler(4), eos_id=first[2],
+                                                   max_new=8).output_tokens
+    with pytest.raises(ConfigError):
+        tinylm.generate_batch(small, [pr] * 9, FixedScheduler(4), max_new=4)
+    with pytest.raises(InputError):
+        tinylm.generate_batch(small, [pr, []], FixedScheduler(4), max_new=4)
+
+
+def test_decode_capture_leaves_counters_unchanged(small):
+    """Capturing a decode step runs one warm-up step on a side stream; the counters it advances
+    (step, tokens produced, cache length) must be restored exactly (a snapshot taken after the
+    side stream was ordered raced with that warm-up and shifted every precision switch by one)."""
+    for _ in range(3):
+        eng = tinylm.DecodeEngine(small, 16)
+        eng.step.fill_(5)
+        eng.n.fill_(2)
+        eng.cache.T_dev.fill_(9)
+        eng.capture()
+        torch.cuda.synchronize()
+        assert (int(eng.step), int(eng.n), int(eng.cache.T_dev)) == (5, 2, 9)

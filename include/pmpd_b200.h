@@ -265,6 +265,15 @@ int pmpd_attention_rope(const float* qkv_dev, int32_t d, int32_t d_head, const f
                         const int32_t* T_dev, int32_t max_ctx, float scale, void* k_cache_dev, void* v_cache_dev,
                         void* out_dev, void* stream);
 
+/* Batched decode: m independent sequences, one new token each.  Row i of qkv_dev (stride ldqkv
+ * >= 3d) is sequence i's q|k|v; its cache is k_cache_dev / v_cache_dev + i * seq_stride halfs
+ * ([max_ctx][d] f16 rows) with length T_dev[i]; same math per sequence as pmpd_attention_rope.
+ * Output row i (stride d).  Replaces a per-sequence loop of pmpd_attention_rope calls. */
+int pmpd_attention_rope_batch(const float* qkv_dev, int32_t ldqkv, int32_t m, int32_t d, int32_t d_head,
+                              const float* cos_dev, const float* sin_dev, const int32_t* T_dev, int32_t max_ctx,
+                              float scale, void* k_cache_dev, void* v_cache_dev, int64_t seq_stride, void* out_dev,
+                              void* stream);
+
 /* out (f16) = silu(u[:, :ff]) * u[:, ff:] (tinylm.py:362-364). */
 int pmpd_silu_mul(const float* u_dev, int32_t ldu, int32_t m, int32_t ff, void* out_dev, int32_t ldo, void* stream);
 

@@ -66,6 +66,7 @@ SIGNATURES = {
     "pmpd_rope_kv": [_P, _I, _I, _I, _I, _P, _P, _P, _I, _P, _P, _P, _P],
     "pmpd_attention": [_P, _I, _I, _I, _P, _P, _P, _I, _F, _P, _P],
     "pmpd_attention_rope": [_P, _I, _I, _P, _P, _P, _I, _F, _P, _P, _P, _P],
+    "pmpd_attention_rope_batch": [_P, _I, _I, _I, _I, _P, _P, _P, _I, _F, _P, _P, _L, _P, _P],
     "pmpd_silu_mul": [_P, _I, _I, _I, _P, _I, _P],
     "pmpd_argmax": [_P, _I, _I, _I, _P, _P, _P],
     "pmpd_add_i32": [_P, _I, _P],

@@ -176,7 +176,8 @@ template <int DPL, bool ROPE>
 __global__ void __cluster_dims__(kSplit, 1, 1) __launch_bounds__(kAttnWarps * 32)
     attention_split_kernel(const float* __restrict__ q, int d, __half* __restrict__ kc, __half* __restrict__ vc,
                            const int32_t* __restrict__ T_dev, int max_ctx, float scale, __half* __restrict__ out,
-                           const float* __restrict__ cos_t, const float* __restrict__ sin_t) {
+                           const float* __restrict__ cos_t, const float* __restrict__ sin_t, int ldq = 0,
+                           int64_t sstride = 0) {
   constexpr int DH = 32 * DPL;
   __shared__ float w_ml[kAttnWarps][2];
   __shared__ float w_acc[kAttnWarps][DH];
@@ -187,7 +188,15 @@ __global__ void __cluster_dims__(kSplit, 1, 1) __launch_bounds__(kAttnWarps * 32
   const int qh = blockIdx.x / kSplit, H = d / DH;
   const int i = qh / H, h = qh - i * H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int L = min(*T_dev + i + 1, max_ctx);
+  // ROPE: i is a sequence (one new token each, its own cache at kc + i * sstride and length T_dev[i]);
+  // otherwise i is the i-th of m causal queries over one cache
+  const int Ti = ROPE ? T_dev[i] : *T_dev;
+  const int L = ROPE ? min(Ti + 1, max_ctx) : min(Ti + i + 1, max_ctx);
+  if constexpr (ROPE) {
+    q += (int64_t)i * ldq;
+    kc += (int64_t)i * sstride;
+    vc += (int64_t)i * sstride;
+  }
   const int chunk = (L + kSplit - 1) / kSplit;
   const int t0 = rank * chunk, t1 = min(L, t0 + chunk);
 
@@ -196,7 +205,7 @@ __global__ void __cluster_dims__(kSplit, 1, 1) __launch_bounds__(kAttnWarps * 32
 #pragma unroll
     for (int j = 0; j < DPL; ++j) qr[j] = q[(int64_t)i * d + h * DH + lane * DPL + j];
   } else {
-    // i == 0; position T = L - 1 (the row being appended)
+    // position T = L - 1 (the row being appended)
     constexpr int HALF = DH / 2;
     const int pos = L - 1;
     const bool first = lane < 16;
@@ -216,7 +225,7 @@ __global__ void __cluster_dims__(kSplit, 1, 1) __launch_bounds__(kAttnWarps * 32
       }
     };
     rot(q, qr);
-    if (*T_dev < max_ctx && pos >= t0 && pos < t1 && warp == 0) {
+    if (Ti < max_ctx && pos >= t0 && pos < t1 && warp == 0) {
       float kr[DPL];
       rot(q + d, kr);
 #pragma unroll
@@ -576,37 +585,47 @@ int pmpd_attention(const float* q, int32_t m, int32_t d, int32_t d_head, const v
   return check_launch("pmpd_attention");
 }
 
-int pmpd_attention_rope(const float* qkv, int32_t d, int32_t d_head, const float* cos_t, const float* sin_t,
-                        const int32_t* T_dev, int32_t max_ctx, float scale, void* k_cache, void* v_cache, void* out,
-                        void* stream) {
+int pmpd_attention_rope_batch(const float* qkv, int32_t ldqkv, int32_t m, int32_t d, int32_t d_head,
+                              const float* cos_t, const float* sin_t, const int32_t* T_dev, int32_t max_ctx,
+                              float scale, void* k_cache, void* v_cache, int64_t seq_stride, void* out,
+                              void* stream) {
   if (d % d_head || d_head % 32 || d_head > 256) return fail(PMPD_ERR_CONFIG, "bad head geometry for the fused path");
-  if ((reinterpret_cast<uintptr_t>(k_cache) & 15) || (reinterpret_cast<uintptr_t>(v_cache) & 15))
-    return fail(PMPD_ERR_INPUT, "KV cache must be 16-byte aligned");
-  const dim3 grid((unsigned)((d / d_head) * kSplit));
+  if (m < 1 || ldqkv < 3 * d) return fail(PMPD_ERR_CONFIG, "bad batch geometry (m >= 1, ldqkv >= 3d)");
+  if ((reinterpret_cast<uintptr_t>(k_cache) & 15) || (reinterpret_cast<uintptr_t>(v_cache) & 15) || (seq_stride & 7))
+    return fail(PMPD_ERR_INPUT, "KV caches must be 16-byte aligned");
+  const dim3 grid((unsigned)(m * (d / d_head) * kSplit));
   auto kc = static_cast<__half*>(k_cache);
   auto vc = static_cast<__half*>(v_cache);
   auto o = static_cast<__half*>(out);
+  const auto st = as_stream(stream);
   switch (d_head) {
     case 32:
-      attention_split_kernel<1, true><<<grid, kAttnWarps * 32, 0, as_stream(stream)>>>(qkv, d, kc, vc, T_dev, max_ctx,
-                                                                                        scale, o, cos_t, sin_t);
+      attention_split_kernel<1, true><<<grid, kAttnWarps * 32, 0, st>>>(qkv, d, kc, vc, T_dev, max_ctx, scale, o, cos_t,
+                                                                         sin_t, ldqkv, seq_stride);
       break;
     case 64:
-      attention_split_kernel<2, true><<<grid, kAttnWarps * 32, 0, as_stream(stream)>>>(qkv, d, kc, vc, T_dev, max_ctx,
-                                                                                        scale, o, cos_t, sin_t);
+      attention_split_kernel<2, true><<<grid, kAttnWarps * 32, 0, st>>>(qkv, d, kc, vc, T_dev, max_ctx, scale, o, cos_t,
+                                                                         sin_t, ldqkv, seq_stride);
       break;
     case 128:
-      attention_split_kernel<4, true><<<grid, kAttnWarps * 32, 0, as_stream(stream)>>>(qkv, d, kc, vc, T_dev, max_ctx,
-                                                                                        scale, o, cos_t, sin_t);
+      attention_split_kernel<4, true><<<grid, kAttnWarps * 32, 0, st>>>(qkv, d, kc, vc, T_dev, max_ctx, scale, o, cos_t,
+                                                                         sin_t, ldqkv, seq_stride);
       break;
     case 256:
-      attention_split_kernel<8, true><<<grid, kAttnWarps * 32, 0, as_stream(stream)>>>(qkv, d, kc, vc, T_dev, max_ctx,
-                                                                                        scale, o, cos_t, sin_t);
+      attention_split_kernel<8, true><<<grid, kAttnWarps * 32, 0, st>>>(qkv, d, kc, vc, T_dev, max_ctx, scale, o, cos_t,
+                                                                         sin_t, ldqkv, seq_stride);
       break;
     default:
       return fail(PMPD_ERR_CONFIG, "head dim %d not supported by the fused path", d_head);
   }
-  return check_launch("pmpd_attention_rope");
+  return check_launch("pmpd_attention_rope_batch");
+}
+
+int pmpd_attention_rope(const float* qkv, int32_t d, int32_t d_head, const float* cos_t, const float* sin_t,
+                        const int32_t* T_dev, int32_t max_ctx, float scale, void* k_cache, void* v_cache, void* out,
+                        void* stream) {
+  return pmpd_attention_rope_batch(qkv, 3 * d, 1, d, d_head, cos_t, sin_t, T_dev, max_ctx, scale, k_cache, v_cache, 0,
+                                   out, stream);
 }
 
 int pmpd_silu_mul(const float* u, int32_t ldu, int32_t m, int32_t ff, void* out, int32_t ldo, void* stream) {

@@ -282,6 +282,21 @@ class KVCache:
         self.T = 0
         self.T_dev.zero_()
 
+    @classmethod
+    def batch(cls, n: int, n_layers: int, width: int, capacity: int) -> list:
+        """n caches carved from one allocation ([n][layers][capacity][width] f16 K and V, lengths
+        int32[n]) so a batched decode step attends over all of them in one launch."""
+        k = torch.zeros((n, n_layers, capacity, width), dtype=torch.float16, device="cuda")
+        v = torch.zeros_like(k)
+        T = torch.zeros(n, dtype=torch.int32, device="cuda")
+        out = []
+        for j in range(n):
+            c = cls.__new__(cls)
+            c.k, c.v, c.T_dev, c.T = k[j], v[j], T[j:j + 1], 0
+            c.group = (k, v, T, j)
+            out.append(c)
+        return out
+
 
 # ---------------------------------------------------------------------------
 # forward pass
@@ -370,8 +385,17 @@ def _run_layers(model: ModelVariants, dw: _DeviceWeights, buf: _Buffers, n: int,
             _capi.call("pmpd_rmsnorm", x.data_ptr(), d, lay["norm_attn"].data_ptr(), n, d, 1e-6, h.data_ptr(), d, s)
             _linear(dw, lay["qkv"], [pre + "wq", pre + "wk", pre + "wv"], h, qkv, buf.p, p_host, buf.ws, False)
         if seq_caches is not None:
-            for j, c in enumerate(seq_caches):
-                _attend_one(dw, qkv[j], ctx[j], q[j], c, i, d, dh, scale, s)
+            g = getattr(seq_caches[0], "group", None)
+            if g is not None and dh % 32 == 0 and dh <= 256 and \
+                    all(getattr(c, "group", (None,))[0] is g[0] and c.group[3] == j for j, c in enumerate(seq_caches)):
+                # caches carved from one allocation (KVCache.batch): every sequence in one launch
+                kb, vb, Tb, _ = g
+                _capi.call("pmpd_attention_rope_batch", qkv.data_ptr(), qkv.stride(0), n, d, dh, dw.cos.data_ptr(),
+                           dw.sin.data_ptr(), Tb.data_ptr(), kb.shape[2], scale, kb[0, i].data_ptr(),
+                           vb[0, i].data_ptr(), kb.stride(0), ctx.data_ptr(), s)
+            else:
+                for j, c in enumerate(seq_caches):
+                    _attend_one(dw, qkv[j], ctx[j], q[j], c, i, d, dh, scale, s)
         elif n == 1 and dh % 32 == 0 and dh <= 256:  # decode: RoPE + KV append fused into the attention
             _capi.call("pmpd_attention_rope", qkv.data_ptr(), d, dh, dw.cos.data_ptr(), dw.sin.data_ptr(),
                        cache.T_dev.data_ptr(), cache.capacity, scale, cache.k[i].data_ptr(), cache.v[i].data_ptr(),
@@ -837,7 +861,7 @@ def generate_batch(model: ModelVariants, prompts: Sequence[Sequence[int]], sched
         if len(pr) + max_new - 1 > mc:
             raise InputError(f"prompt length {len(pr)} + {max_new - 1} decode steps exceed max_context {mc}")
     _check_precision(model, scheduler.p_prefill)
-    caches = [KVCache(model.config.n_layers, model.config.d_model, mc) for _ in prompts]
+    caches = KVCache.batch(len(prompts), model.config.n_layers, model.config.d_model, mc)
     sched = scheduler.resolve(caches[0])
     violations = sched.validate()
     if violations:

@@ -456,6 +456,19 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
       const int ngp = r.T0 / r.KT + i;
       idm_pre[i] = (r.T1 > r.T0 && ngp < op.n_tiles) ? __ldg(op.aux + ngp) : 0.f;
     }
+    // RMSNorm input of a row that fits one pass (K <= 4 * RN * 384): the gain is static, so its
+    // loads are issued before the grid wait and only the residual's round trip is on the op path
+    constexpr int RN = 4, RN_K = 4 * RN * E_NCW * 32;
+    const bool rms1 = DEC && op.in_mode == E_IN_RMSNORM && op.k_real <= RN_K;
+    float4 gpre[RN];
+    if (DEC) {
+#pragma unroll
+      for (int j = 0; j < RN; ++j) {
+        const int k = 4 * threadIdx.x + j * 4 * E_NCW * 32;
+        gpre[j] = rms1 && k < op.k_real ? __ldg(reinterpret_cast<const float4*>(op.gain + k))
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
     if (oi > 0) {
       // every op starts after ALL CTAs published ALL earlier ops (the ticket count is only a
       // safe completion test for a strict op-by-op order)
@@ -466,7 +479,42 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
     float mx = 0.f;
     const EngineOp* src = op.src >= 0 ? &a.ops[op.src] : nullptr;
     float inv = 1.f;  // E_IN_RMSNORM: 1 / sqrt(mean(resid^2) + eps) over the whole row
-    if (DEC && op.in_mode == E_IN_RMSNORM) {
+    if (DEC && rms1) {
+      // one pass: resid * gain stays in registers while the sum of squares is reduced, then the
+      // whole normalised row is written to xs as f16 (max |x| over the row, not just the k-range)
+      float4 rg[RN];
+      float ss = 0.f;
+#pragma unroll
+      for (int j = 0; j < RN; ++j) {
+        const int k = 4 * threadIdx.x + j * 4 * E_NCW * 32;
+        const float4 q = k < op.k_real ? __ldcg(reinterpret_cast<const float4*>(op.resid + k))
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        ss = fmaf(q.x, q.x, fmaf(q.y, q.y, fmaf(q.z, q.z, fmaf(q.w, q.w, ss))));
+        rg[j] = make_float4(q.x * gpre[j].x, q.y * gpre[j].y, q.z * gpre[j].z, q.w * gpre[j].w);
+      }
+      ss = warp_sum(ss);
+      if (lane == 0) misc[32 + warp] = ss;
+      named_bar_sync(1, E_NCW * 32);
+      float tot = 0.f;
+#pragma unroll
+      for (int w = 0; w < E_NCW; ++w) tot += misc[32 + w];
+      inv = rsqrtf(tot * op.eps_inv_k + op.eps);
+#pragma unroll
+      for (int j = 0; j < RN; ++j) {
+        const int k = 4 * threadIdx.x + j * 4 * E_NCW * 32;
+        if (k < r.KT * kTile) {
+          // (x * g) * inv: tinylm.py:293-295 up to one rounding order; zero past k_real
+          const __half2 h01 = __floats2half2_rn(rg[j].x * inv, rg[j].y * inv);
+          const __half2 h23 = __floats2half2_rn(rg[j].z * inv, rg[j].w * inv);
+          *reinterpret_cast<__half2*>(xs + k) = h01;
+          *reinterpret_cast<__half2*>(xs + k + 2) = h23;
+          const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+          mx = fmaxf(mx, fmaxf(fmaxf(fabsf(f01.x), fabsf(f01.y)), fmaxf(fabsf(f23.x), fabsf(f23.y))));
+        }
+      }
+      hi0 = hi1 = 0;  // staged already
+      lo0 = lo1 = 0;
+    } else if (DEC && op.in_mode == E_IN_RMSNORM) {
       // one L2 pass: the whole f32 row lands in xs above the f16 staging area (bytes
       // [2*KT*64, 2*KT*64 + 4*K), checked at set_io) while its sum of squares accumulates; the
       // k-range is then staged from there without overlapping the f16 writes

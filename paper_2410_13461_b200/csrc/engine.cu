@@ -342,9 +342,13 @@ __noinline__ __device__ void attn_op(const EngineOp& op, const EngineOp& src, in
 
 // E_IN_ATTN staging (kept out of line: its 48 live registers of split records would otherwise
 // count against the consumer loop's tile body).  Returns max |x| of the staged f16 row.
-__noinline__ __device__ float stage_attn_input(const EngineOp& op, const EngineOp& src, int kp, __half* xs,
-                                               float* wscratch) {
+__noinline__ __device__ float stage_attn_input(const EngineOp& op, const EngineOp& src, int lo0, int hi0, int lo1,
+                                               int hi1, __half* xs, float* wscratch) {
   float mx = 0.f;
+  // only this CTA's k-tile ranges [lo0, hi0) and [lo1, hi1) are staged (the tiles read nothing
+  // else): element u of the concatenated ranges maps to k = kof(u)
+  const int len0 = (hi0 - lo0) * kTile, lr = len0 + (hi1 - lo1) * kTile;
+  auto kof = [&](int u) { return u < len0 ? lo0 * kTile + u : lo1 * kTile + (u - len0); };
       // The whole row (K = d <= 4608) in one L2 round trip: every thread issues the split records
       // of its groups first, the per-(head, split) softmax weights w = exp(m_s - M_h) /
       // sum_s exp(m_s - M_h) l_s are computed into xq scratch while those loads are in flight.
@@ -353,7 +357,8 @@ __noinline__ __device__ float stage_attn_input(const EngineOp& op, const EngineO
       float4 av[SBA][E_ASPLIT];
 #pragma unroll
       for (int bi = 0; bi < SBA; ++bi) {
-        const int k = 4 * threadIdx.x + bi * 4 * E_NCW * 32;
+        const int u = 4 * threadIdx.x + bi * 4 * E_NCW * 32;
+        const int k = u < lr ? kof(u) : op.k_real;
         const int hh = k < op.k_real ? k / dh : 0, e = k - hh * dh;
         const float* rec = src.part + (int64_t)hh * E_ASPLIT * attn_rec(dh) + 4 + e;
 #pragma unroll
@@ -384,8 +389,9 @@ __noinline__ __device__ float stage_attn_input(const EngineOp& op, const EngineO
       named_bar_sync(1, E_NCW * 32);
 #pragma unroll
       for (int bi = 0; bi < SBA; ++bi) {
-        const int k = 4 * threadIdx.x + bi * 4 * E_NCW * 32;
-        if (k >= kp) break;
+        const int u = 4 * threadIdx.x + bi * 4 * E_NCW * 32;
+        if (u >= lr) break;
+        const int k = kof(u);
         float o[4] = {0.f, 0.f, 0.f, 0.f};
         if (k < op.k_real) {
           const int hh = k / dh;
@@ -546,7 +552,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
       for (int w = 0; w < E_NCW; ++w) tot += misc[32 + w];
       inv = rsqrtf(tot * op.eps_inv_k + op.eps);
     } else if (DEC && op.in_mode == E_IN_ATTN) {
-      mx = stage_attn_input(op, *src, r.KT * kTile, xs, reinterpret_cast<float*>(smem + kSmXq));
+      mx = stage_attn_input(op, *src, lo0, hi0, lo1, hi1, xs, reinterpret_cast<float*>(smem + kSmXq));
       hi0 = hi1 = 0;  // staged already (the generic loop below runs no iteration)
       lo0 = lo1 = 0;
     }

@@ -153,19 +153,27 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU baselines (oracle port)
-def cpu_sample(shape, seconds_budget=20.0):
-    """Reference CPU path (oracle restatement of dequantize + x @ W in float64, quant.py:199-215 +
-    tinylm.py:341) timed on a bounded sample: 4096x4096 KN matrices at p=4/3/2 on all host cores,
-    extrapolated per weight to the whole 7B linear stack and weighted by the schedule."""
+def cpu_setup():
+    """Untimed inputs of the CPU sample: one quantized 4096x4096 KN matrix per host core."""
     import numpy as np
-    from concurrent.futures import ThreadPoolExecutor
     from oracle import quant as oq
 
     cores = max(1, min(os.cpu_count() or 1, 16))
     rng = np.random.default_rng(0)
     K = N = 4096
     qts = [oq.quantize((0.02 * rng.standard_normal((K, N))).astype(np.float32), 4, 64) for _ in range(cores)]
-    x = rng.standard_normal((1, K))
+    return qts, rng.standard_normal((1, K)), cores
+
+
+def cpu_sample(shape, setup=None):
+    """Reference CPU path (oracle restatement of dequantize + x @ W in float64, quant.py:199-215 +
+    tinylm.py:341) timed on a bounded sample: 4096x4096 KN matrices at p=4/3/2 on all host cores,
+    extrapolated per weight to the whole 7B linear stack and weighted by the schedule."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import quant as oq
+
+    qts, x, cores = setup if setup is not None else cpu_setup()
+    K = N = 4096
     per_p = {}
     for p in (4, 3, 2):
         def work(qt):
@@ -182,22 +190,36 @@ def cpu_sample(shape, seconds_budget=20.0):
                              f"extrapolated per weight to {shape.weights_per_token} weights/token, schedule-weighted"
 
 
+def arm_config(args, world: int, tp_mode: bool) -> dict:
+    """The workload config both arms report (ours and --impl reference)."""
+    return {"workload": f"{args.shape} decode linear stack (32x q|k|v,o,gate|up,down + head), batch 1, "
+                        "progressive 4->3->2 switching at tokens 32/128 over 512 tokens per step",
+            "schedule": {str(k): v for k, v in SCHED.items()}, "horizon": HORIZON,
+            "parallelism": f"tp{world} (NCCL all-reduce after o and down)" if tp_mode else "single GPU",
+            "l2": "inputs larger than L2 (2.5-4.1 GB of planes per token vs 126 MB L2)"}
+
+
 def run_reference(args, shape):
     """--impl reference: the reference's CPU algorithm (oracle port) on the box's host cores."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    vals, per_p, cores, sample = [], {}, 1, ""
+    vals, walls, per_p, cores, sample = [], [], {}, 1, ""
+    setup = cpu_setup()  # quantization of the sample matrices is not part of a step
     for i in range(args.warmup + args.steps):
-        us, cores, per_p, sample = cpu_sample(shape)
+        t = time.perf_counter()
+        us, cores, per_p, sample = cpu_sample(shape, setup)
         if i >= args.warmup:
             vals.append(us)
+            walls.append(time.perf_counter() - t)
     v = statistics.mean(vals)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "us/token", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.shape} decode linear stack, batch 1, progressive 4->3->2 @32/128 over 512"},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(walls) * 1e3,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (N(0,0.02^2) weights, seeded)",
+        "config": arm_config(args, world, world > 1),
         "cpu_baseline": {"value": v, "unit": "us/token", "cores": cores, "kind": "port", "sample": sample,
                          "per_precision_us": per_p},
         "e2e": {"value": v, "unit": "us/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -379,11 +401,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "fp16",
         "data": "synthetic (N(0,0.02^2) weights, seeded; device-quantized bit-exactly to nested 4/3/2-bit)",
-        "config": {"workload": f"{args.shape} decode linear stack (32x q|k|v,o,gate|up,down + head), batch 1, "
-                               "progressive 4->3->2 switching at tokens 32/128 over 512 tokens per step",
-                   "schedule": {str(k): v for k, v in SCHED.items()}, "horizon": HORIZON,
-                   "parallelism": f"tp{world} (NCCL all-reduce after o and down)" if tp_mode else "single GPU",
-                   "l2": "inputs larger than L2 (2.5-4.1 GB of planes per token vs 126 MB L2)"},
+        "config": arm_config(args, world, tp_mode),
         "per_precision": {str(k): v for k, v in per_p.items()},
         "avg_bits": sum(p * f for p, f in w.items()),
         "speedup_vs_uniform4": per_p[4]["us_per_token"] / us_tok,

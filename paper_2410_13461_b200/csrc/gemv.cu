@@ -801,7 +801,10 @@ int launch_grid(const pmpd_qtensor* t, int m) {
     const char* e = getenv("PMPD_GEMV_SPLITK");  // diagnostics: 1 forces the split-K grid
     mode = e ? atoi(e) : 0;
   }
-  if (mode != 1 && (t->n_tiles <= sms || (m <= 2 && t->n_tiles <= 2 * sms))) return t->n_tiles;
+  // batch >= 4 on long K (>= 128 k-tiles): the per-CTA tile count of the n-group grid makes it
+  // compute-bound; the split-K grid is ~10 % faster there (tools/gemv_grid_sweep.py, 11008x4096)
+  const bool long_k = m >= 4 && t->k_tiles >= 128;
+  if (mode != 1 && !long_k && (t->n_tiles <= sms || (m <= 2 && t->n_tiles <= 2 * sms))) return t->n_tiles;
   return grid_for(t);
 }
 

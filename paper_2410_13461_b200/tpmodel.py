@@ -334,7 +334,7 @@ class TPModel:
 
     # -- generation ------------------------------------------------------------
     def generate(self, prompt: Sequence[int], scheduler, eos_id: int | None = None, max_new: int = 64,
-                 record_logits: bool = False, check_every: int = 16) -> GenerationTrace:
+                 record_logits: bool = False, check_every: int = 16, graph: bool = True) -> GenerationTrace:
         """Greedy generation under the scheduler's precision switching (tinylm.py:475-523): the
         per-token precision comes from the device hook, the token from the distributed argmax,
         both on device; the host reads tokens back every ``check_every`` steps for EOS."""
@@ -369,6 +369,28 @@ class TPModel:
         if hist is not None:
             hist[0].copy_(logits)
         produced = 1
+
+        def step():
+            self._decode_token(bufs, tables, steps, tokens, counts, cap, hist)
+        if graph and max_new > 1:
+            # one CUDA graph per decode step on every local rank (NCCL collectives are captured
+            # too); the warm-up step's counter updates are undone before capturing
+            state = [steps[i] for i in range(len(steps))] + tokens + counts + [b.ids for b in bufs] + \
+                [b.bad for b in bufs] + [c.T_dev for c in self.caches]
+            saved = [t.clone() for t in state]
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                step()
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize()
+            for t, v in zip(state, saved):
+                t.copy_(v)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step()
+            torch.cuda.synchronize()
+            step = g.replay
         while True:
             if int(bufs[0].bad.item()):
                 raise InputError("logits contain non-finite values")
@@ -376,7 +398,7 @@ class TPModel:
             if eos in toks or produced >= max_new:
                 break
             for _ in range(min(check_every, max_new - produced)):
-                self._decode_token(bufs, tables, steps, tokens, counts, cap, hist, produced)
+                step()
                 produced += 1
         toks = tokens[0][:produced].cpu().tolist()
         if eos in toks:
@@ -390,7 +412,7 @@ class TPModel:
         return GenerationTrace(list(prompt), toks, [sched.precision_at(j) for j in range(len(toks))], hashes, term,
                                scheduler.p_prefill, sched, hist[:len(toks)] if record_logits else None)
 
-    def _decode_token(self, bufs, tables, steps, tokens, counts, cap, hist, row) -> None:
+    def _decode_token(self, bufs, tables, steps, tokens, counts, cap, hist) -> None:
         """One greedy decode step on every local rank: sched hook -> sharded forward -> local
         argmax -> (value, index) exchange -> token push (all on device)."""
         s = _stream()
@@ -414,8 +436,9 @@ class TPModel:
                 return torch.cat([pt[:, :sl.size] for pt, sl in zip(full, w.vocab)], dim=1)
             return None
         out = lockstep([gen(w, b) for w, b in zip(self.w, bufs)], self.comm)
-        if hist is not None:
-            hist[row].copy_(out[0][0])
+        if hist is not None:  # row = tokens produced so far (device counter: graph-capturable)
+            full = out[0].contiguous()
+            _capi.call("pmpd_store_row", full.data_ptr(), hist.data_ptr(), counts[0].data_ptr(), full.shape[1], cap, s)
         for b, tk, nn, c in zip(bufs, tokens, counts, self.caches):
             _capi.call("pmpd_push_token", b.ids.data_ptr(), tk.data_ptr(), nn.data_ptr(), c.T_dev.data_ptr(), cap, s)
 

@@ -408,13 +408,14 @@ def _run_layers(model: ModelVariants, dw: _DeviceWeights, buf: _Buffers, n: int,
                 # long-prompt prefill from an empty cache (>= 256 rows; below that the per-query kernel
                 # wins over the library call overhead): causal attention of the n new rows over
                 # themselves (tinylm.py:349-358) through torch's fused SDPA (a library kernel, like
-                # cuBLAS; attention is runner glue, not the quantized hot path)
+                # cuBLAS; attention is runner glue, not the quantized hot path).  4-D (batch, heads,
+                # rows, dh) inputs: with 3-D ones SDPA has no fused kernel and falls back to f32 math
                 H = cfg.n_heads
-                qh = q[:n].view(n, H, dh).transpose(0, 1).half()
-                kh = cache.k[i][:n].view(n, H, dh).transpose(0, 1)
-                vh = cache.v[i][:n].view(n, H, dh).transpose(0, 1)
+                qh = q[:n].view(n, H, dh).transpose(0, 1).half().unsqueeze(0)
+                kh = cache.k[i][:n].view(n, H, dh).transpose(0, 1).unsqueeze(0)
+                vh = cache.v[i][:n].view(n, H, dh).transpose(0, 1).unsqueeze(0)
                 o = torch.nn.functional.scaled_dot_product_attention(qh, kh, vh, is_causal=True, scale=scale)
-                ctx.copy_(o.transpose(0, 1).reshape(n, d))
+                ctx.copy_(o[0].transpose(0, 1).reshape(n, d))
             else:
                 _capi.call("pmpd_attention", q.data_ptr(), n, d, dh, cache.k[i].data_ptr(), cache.v[i].data_ptr(),
                            cache.T_dev.data_ptr(), cache.capacity, scale, ctx.data_ptr(), s)

@@ -125,11 +125,11 @@ def _layers(w: TPWeights, buf: _Buffers, n: int, cache: KVCache, T0: int):
                        cache.v[i].data_ptr(), s)
             if n >= 256 and T0 == 0:  # long prompt from an empty cache: library SDPA (as tinylm)
                 H = w.heads
-                qh = q.view(n, H, dh).transpose(0, 1).half()
-                kh = cache.k[i][:n].view(n, H, dh).transpose(0, 1)
-                vh = cache.v[i][:n].view(n, H, dh).transpose(0, 1)
+                qh = q.view(n, H, dh).transpose(0, 1).half().unsqueeze(0)
+                kh = cache.k[i][:n].view(n, H, dh).transpose(0, 1).unsqueeze(0)
+                vh = cache.v[i][:n].view(n, H, dh).transpose(0, 1).unsqueeze(0)
                 o = torch.nn.functional.scaled_dot_product_attention(qh, kh, vh, is_causal=True, scale=scale)
-                ctx.copy_(o.transpose(0, 1).reshape(n, dq))
+                ctx.copy_(o[0].transpose(0, 1).reshape(n, dq))
             else:
                 _capi.call("pmpd_attention", q.data_ptr(), n, dq, dh, cache.k[i].data_ptr(), cache.v[i].data_ptr(),
                            cache.T_dev.data_ptr(), cache.capacity, scale, ctx.data_ptr(), s)

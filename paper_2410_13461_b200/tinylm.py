@@ -348,6 +348,10 @@ def _linear(dw: _DeviceWeights, pks: list, name16: list, x16: torch.Tensor, out:
 _FUSE_DECODE = os.environ.get("PMPD_FUSE_DECODE", "0") == "1"  # fused norm/SwiGLU GEMVs: measured slower, off
 
 
+# prefill rows from which causal self-attention over an empty cache goes through torch SDPA
+_SDPA_MIN_ROWS = int(os.environ.get("PMPD_SDPA_MIN_ROWS", "256"))
+
+
 def _fused_linear(pks: list, mode: int, xf: torch.Tensor, gain, u_off: int, out: torch.Tensor, buf: _Buffers,
                   accumulate: bool) -> None:
     """out (+)= op(xf) @ W_p with op = RMSNorm*gain or SwiGLU fused into the decode GEMV staging."""
@@ -404,7 +408,7 @@ def _run_layers(model: ModelVariants, dw: _DeviceWeights, buf: _Buffers, n: int,
             _capi.call("pmpd_rope_kv", qkv.data_ptr(), 3 * d, n, d, dh, dw.cos.data_ptr(), dw.sin.data_ptr(),
                        cache.T_dev.data_ptr(), cache.capacity, q.data_ptr(), cache.k[i].data_ptr(),
                        cache.v[i].data_ptr(), s)
-            if n >= 256 and cache.T == 0:
+            if n >= _SDPA_MIN_ROWS and cache.T == 0:
                 # long-prompt prefill from an empty cache (>= 256 rows; below that the per-query kernel
                 # wins over the library call overhead): causal attention of the n new rows over
                 # themselves (tinylm.py:349-358) through torch's fused SDPA (a library kernel, like

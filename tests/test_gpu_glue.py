@@ -99,3 +99,18 @@ def test_attention_rope_matches_two_kernels(dh, H, T):
     assert (k1.float() - k2.float()).abs().max().item() <= 1e-3 * k1.float().abs().max().item()
     rel = ((out1.float() - out2.float()).norm() / out1.float().norm()).item()
     assert rel < 2e-3, rel
+
+
+@pytest.mark.parametrize("m,ff,pad", [(1, 5632, 0), (512, 11008, 0), (3, 13, 1), (7, 96, 3)])
+def test_silu_mul_matches_torch(m, ff, pad):
+    """out = f16(silu(u[:, :ff]) * u[:, ff:]) (tinylm.py:362-364), vectorised and ragged/unaligned rows."""
+    from paper_2410_13461_b200 import _capi
+    ldu = 2 * ff + pad
+    u = torch.randn(m, ldu, device="cuda") * 3
+    out = torch.zeros(m, ff + pad, dtype=torch.float16, device="cuda")
+    _capi.call("pmpd_silu_mul", u.data_ptr(), ldu, m, ff, out.data_ptr(), ff + pad, torch.cuda.current_stream().cuda_stream)
+    g, up = u[:, :ff].double(), u[:, ff:2 * ff].double()
+    want = g / (1 + torch.exp(-g)) * up
+    got = out[:, :ff].double()
+    assert torch.allclose(got, want, rtol=2e-3, atol=2e-3)
+    assert torch.all(out[:, ff:] == 0)

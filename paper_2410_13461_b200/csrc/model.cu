@@ -64,12 +64,34 @@ __global__ void rmsnorm_kernel(const float* __restrict__ x, int ldx, const float
 // cos/sin: [max_ctx][d_head/2] tables computed in float64 on the host.
 __global__ void rope_kv_kernel(const float* __restrict__ qkv, int ldq, int d, int dh, const float* __restrict__ cos_t,
                                const float* __restrict__ sin_t, const int32_t* __restrict__ T_dev, int max_ctx,
-                               float* __restrict__ q_out, __half* __restrict__ kc, __half* __restrict__ vc) {
+                               float* __restrict__ q_out, __half* __restrict__ kc, __half* __restrict__ vc,
+                               int vec2) {
   const int i = blockIdx.x;  // token
   const int pos = *T_dev + i;
   if (pos >= max_ctx) return;
   const float* row = qkv + (int64_t)i * ldq;
   const int half = dh >> 1;
+  if (vec2) {
+    // two adjacent rotation pairs (j, j + 1) per thread: float2 loads/stores, half2 cache writes
+    for (int e = 2 * threadIdx.x; e < d / 2; e += 2 * blockDim.x) {
+      const int h = e / half, j = e - h * half;
+      const float2 c = *reinterpret_cast<const float2*>(cos_t + (int64_t)pos * half + j);
+      const float2 s = *reinterpret_cast<const float2*>(sin_t + (int64_t)pos * half + j);
+      const int a = h * dh + j, b = a + half;
+      const float2 q1 = *reinterpret_cast<const float2*>(row + a), q2 = *reinterpret_cast<const float2*>(row + b);
+      *reinterpret_cast<float2*>(q_out + (int64_t)i * d + a) = make_float2(q1.x * c.x - q2.x * s.x, q1.y * c.y - q2.y * s.y);
+      *reinterpret_cast<float2*>(q_out + (int64_t)i * d + b) = make_float2(q2.x * c.x + q1.x * s.x, q2.y * c.y + q1.y * s.y);
+      const float2 k1 = *reinterpret_cast<const float2*>(row + d + a), k2 = *reinterpret_cast<const float2*>(row + d + b);
+      *reinterpret_cast<__half2*>(kc + (int64_t)pos * d + a) =
+          __floats2half2_rn(k1.x * c.x - k2.x * s.x, k1.y * c.y - k2.y * s.y);
+      *reinterpret_cast<__half2*>(kc + (int64_t)pos * d + b) =
+          __floats2half2_rn(k2.x * c.x + k1.x * s.x, k2.y * c.y + k1.y * s.y);
+      const float2 v1 = *reinterpret_cast<const float2*>(row + 2 * d + a), v2 = *reinterpret_cast<const float2*>(row + 2 * d + b);
+      *reinterpret_cast<__half2*>(vc + (int64_t)pos * d + a) = __floats2half2_rn(v1.x, v1.y);
+      *reinterpret_cast<__half2*>(vc + (int64_t)pos * d + b) = __floats2half2_rn(v2.x, v2.y);
+    }
+    return;
+  }
   for (int e = threadIdx.x; e < d / 2; e += blockDim.x) {
     const int h = e / half, j = e - h * half;
     const float c = cos_t[(int64_t)pos * half + j], s = sin_t[(int64_t)pos * half + j];
@@ -549,8 +571,13 @@ int pmpd_rope_kv(const float* qkv, int32_t ldq, int32_t m, int32_t d, int32_t d_
                  const float* sin_t, const int32_t* T_dev, int32_t max_ctx, float* q_out, void* k_cache,
                  void* v_cache, void* stream) {
   if (d_head % 2 || d % d_head) return fail(PMPD_ERR_CONFIG, "bad head geometry");
+  // float2 / half2 path: rotation pairs come in adjacent twos (d_head % 4 == 0) and every row is 8-byte aligned
+  const int vec2 = d_head % 4 == 0 && ldq % 2 == 0 && d % 2 == 0 && (reinterpret_cast<uintptr_t>(qkv) & 7) == 0 &&
+                   (reinterpret_cast<uintptr_t>(q_out) & 7) == 0 && (reinterpret_cast<uintptr_t>(cos_t) & 7) == 0 &&
+                   (reinterpret_cast<uintptr_t>(sin_t) & 7) == 0 && (reinterpret_cast<uintptr_t>(k_cache) & 3) == 0 &&
+                   (reinterpret_cast<uintptr_t>(v_cache) & 3) == 0;
   rope_kv_kernel<<<m, kBlock, 0, as_stream(stream)>>>(qkv, ldq, d, d_head, cos_t, sin_t, T_dev, max_ctx, q_out,
-                                                      (__half*)k_cache, (__half*)v_cache);
+                                                      (__half*)k_cache, (__half*)v_cache, vec2);
   return check_launch("pmpd_rope_kv");
 }
 

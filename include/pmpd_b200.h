@@ -220,6 +220,13 @@ int pmpd_engine_attn_records(int32_t n_heads, int32_t d_head);
  * evenly; attach the uploaded array with pmpd_engine_op_set_bounds (null = even split). */
 int pmpd_engine_partition(const pmpd_qtensor* t, int32_t* bounds_host);
 int pmpd_engine_op_set_bounds(void* op_host, const int32_t* bounds_dev);
+/* Counted accumulation (linear-stack programs run by pmpd_engine_run): the op's output is
+ * acc_dev = u64 [2][n_tiles * 64] zero-initialised words, each holding [63:56] the number of CTAs
+ * that added into it and [55:0] the sum of their partials as 2^-24 fixed point (offset binary),
+ * so split-K sums are bit-reproducible and self-validating; nslots_dev[n_tiles] = contributors
+ * per n-group under the op's bounds, n_contrib = CTAs with a nonempty range.  bar_dev of the run
+ * then holds 3 + n_ops u32 (tickets, done, launch epoch, per-op hint counters), zeroed once. */
+int pmpd_engine_op_set_counted(void* op_host, void* acc_dev, const uint8_t* nslots_dev, int32_t n_contrib);
 /* pmpd_engine_run for programs that use the decoder-step ops above (a separate kernel
  * instantiation, so the linear-stack program pays nothing for them); trace_dev optional. */
 int pmpd_engine_run_decoder(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, float* y_out_dev, float y_alpha,

@@ -13,13 +13,19 @@
 //     mma.sync m16n8k32 (u8 x {s8,u8}) against an int16 two-digit activation
 //     operand, int32 accumulation (see gemv.cu for the arithmetic);
 //   * an epilogue warp reduces the consumer warps' per-n-group partials and
-//     adds them (f32 atomics, performed at L2) into the op's output vector,
-//     then publishes the op's completion on a grid-wide counter;
-//   * the next op's consumers wait on that counter (acquire) and read one f32
-//     per input element into an f16 activation vector in shared memory.  The
-//     order of the split-K additions is not fixed, so the low bits of a result
-//     may differ between runs (the per-op GEMV keeps a deterministic order);
-//   * after the final output every CTA re-zeroes its slice of the vectors.
+//     adds them into the op's output vector at L2;
+//   * the next op's consumers stage one value per input element into an f16
+//     activation vector in shared memory.
+// Linear-stack programs (engine_kernel<false>) use COUNTED fixed-point
+// accumulation: every output element is a u64 word whose top 8 bits count the
+// contributing CTAs and whose low 56 bits sum the contributions as 2^-24
+// fixed point (offset binary).  Integer addition is associative, so the result
+// is bit-identical whatever order the split-K partials arrive in, and the word
+// itself tells a consumer when all contributors have landed: no release fence,
+// no grid-wide ticket on the op-to-op path (a relaxed per-op counter is only a
+// polling hint).  Vectors alternate between two parity sets per launch; each
+// CTA zeroes its slice of the idle set as it goes.  Decoder-step programs
+// (engine_kernel<true>) keep f32 L2 atomics and a release/acquire ticket.
 // Co-residency of all CTAs is guaranteed by a cooperative launch.
 #include <cuda_fp16.h>
 
@@ -76,11 +82,59 @@ struct EngineOp {
   int n_heads, d_head, max_ctx;
   float scale;
   const int* bounds;  // optional [G + 1] tile-range boundaries per CTA (pmpd_engine_partition); null = even
+  // ---- counted accumulation (linear-stack programs, pmpd_engine_op_set_counted)
+  unsigned long long* acc;  // u64 [2][n_tiles * 64]: parity sets of counted fixed-point sums
+  int n_contrib;            // CTAs with a nonempty tile range (each adds 1 to the op's hint counter)
 };
 constexpr int E_LINEAR = 0, E_ATTN = 1;
 constexpr int E_IN_SRC = 0, E_IN_RMSNORM = 2, E_IN_ATTN = 3;
 constexpr int E_ASPLIT = 4;  // context splits per head in the attention op
 PMPD_DEV int attn_rec(int dh) { return 4 + dh; }  // record: m, l, pad, pad, acc[dh] (16-byte aligned acc)
+
+// ---- counted fixed-point words: [63:56] contributors, [55:0] sum of (rint(v * 2^24) + 2^47)
+constexpr int kCntShift = 56;
+constexpr unsigned long long kValMask = (1ull << kCntShift) - 1;
+constexpr long long kFixOff = 1ll << 47;       // per-contribution offset: keeps every addend >= 0
+constexpr float kFixScale = 16777216.f;        // 2^24
+constexpr float kFixUnscale = 5.9604644775390625e-8f;  // 2^-24
+constexpr float kFixMax = 8388608.f;           // |v| < 2^23 keeps rint(v * 2^24) inside +-2^47
+// Contribution word of one partial; a non-finite or out-of-range partial still counts (so no
+// consumer waits forever) but adds zero and flags the status word.
+PMPD_DEV unsigned long long fix_encode(float v, int* status) {
+  long long q = 0;
+  if (fabsf(v) < kFixMax)
+    q = __float2ll_rn(v * kFixScale);
+  else if (status)
+    atomicExch(status, PMPD_ERR_INPUT);
+  return (1ull << kCntShift) + (unsigned long long)(q + kFixOff);
+}
+PMPD_DEV int fix_count(unsigned long long w) { return (int)(w >> kCntShift); }
+// value of a complete word with `cnt` contributions: one rounding of the exact sum to f32
+PMPD_DEV float fix_decode(unsigned long long w, int cnt) {
+  const long long t = (long long)(w & kValMask) - (long long)cnt * kFixOff;
+  return __ll2float_rn(t) * kFixUnscale;
+}
+PMPD_DEV void ld_relaxed_u64x2(const unsigned long long* p, unsigned long long& a, unsigned long long& b) {
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+PMPD_DEV unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+PMPD_DEV void red_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+PMPD_DEV unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Poll the op's hint counter until every contributing CTA has issued its additions (a hint:
+// the words themselves are validated by their counts).
+PMPD_DEV void wait_hint(const unsigned* p, unsigned target) {
+  while ((int)(ld_relaxed_u32(p) - target) < 0) __nanosleep(32);
+}
 
 struct EngineArgs {
   const EngineOp* ops;
@@ -89,7 +143,8 @@ struct EngineArgs {
   const __half* x_in;  // input of op 0 (f16)
   float* y_out;        // output of the last op (f32), y_alpha * reduced partials
   float y_alpha;
-  unsigned* bar;       // [0]: op-completion tickets, [1]: CTAs done (self-resetting)
+  unsigned* bar;       // [0]: op-completion tickets, [1]: CTAs done (self-resetting), [2]: launch epoch,
+                       // [3 + i]: op i's hint counter (counted programs)
   int* status;
   long long* trace;    // optional timeline [G][n_ops][4] (globaltimer ns), null = off
 };
@@ -146,6 +201,23 @@ PMPD_DEV Range range_of(const EngineOp& op, int c, int G) {
     r.T1 = (int)((unsigned)(c + 1) * (unsigned)r.NT / (unsigned)G);
   }
   return r;
+}
+
+// L2 prefetch of this CTA's packed tiles of op `op` (active planes + scale blocks).  The smem
+// ring holds less than an op's share of the weights, so while the consumers wait at an op
+// boundary the ring is full and the TMA stream would stall; prefetching PMPD_ENGINE_PF ops ahead
+// into the 126 MB L2 keeps HBM streaming through the op-to-op exchanges, and the ring then
+// refills from L2.
+#ifndef PMPD_ENGINE_PF
+#define PMPD_ENGINE_PF 0  // measured slower at 1-4 ops ahead (round 2): the engine is sync-bound, not stream-bound
+#endif
+PMPD_DEV void prefetch_op(const EngineOp& op, int c, int G, int p) {
+  if (op.kind != E_LINEAR) return;
+  const Range r = range_of(op, c, G);
+  if (r.T1 <= r.T0) return;
+  const uint32_t n = (uint32_t)(r.T1 - r.T0) * kTilePlaneBytes;
+  for (int j = 0; j < p; ++j) bulk_prefetch_l2(op.planes + j * op.plane_bytes + (int64_t)r.T0 * kTilePlaneBytes, n);
+  bulk_prefetch_l2(op.scales + (int64_t)r.T0 * kTileScaleBytes, (uint32_t)(r.T1 - r.T0) * kTileScaleBytes);
 }
 
 // ------------------------------------------------------------------ attention op
@@ -416,7 +488,8 @@ __noinline__ __device__ float stage_attn_input(const EngineOp& op, const EngineO
 // ------------------------------------------------------------------ kernel
 template <bool DEC>
 PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bars& bars, int G, int c,
-                            int stage_bytes, int nstage) {
+                            int stage_bytes, int nstage, unsigned epoch) {
+  const int par = (int)(epoch & 1u);  // counted programs: parity set of this launch
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tig = lane & 3;
   __half* xs = reinterpret_cast<__half*>(smem + kSmX);
   uint8_t* xq = smem + kSmXq + warp * E_TPW * 128;
@@ -475,10 +548,17 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
                                         : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
-    if (oi > 0) {
+    if (DEC && oi > 0) {
       // every op starts after ALL CTAs published ALL earlier ops (the ticket count is only a
       // safe completion test for a strict op-by-op order)
       if (threadIdx.x == 0) wait_tickets(a.bar, (unsigned)(oi * G));
+      named_bar_sync(1, E_NCW * 32);
+    }
+    if (!DEC && op.src >= 0 && r.T1 > r.T0) {
+      // counted: wait (relaxed) until every contributor of the source op has issued its
+      // additions; the staging below validates each word's count, so this only avoids polling
+      // the data lines while they are still being produced
+      if (threadIdx.x == 0) wait_hint(a.bar + 3 + op.src, (epoch + 1u) * (unsigned)a.ops[op.src].n_contrib);
       named_bar_sync(1, E_NCW * 32);
     }
     if (a.trace && threadIdx.x == 0) a.trace[((int64_t)c * a.n_ops + oi) * 8 + 0] = gtimer();
@@ -587,6 +667,50 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
             } else {
 #pragma unroll
               for (int i = 0; i < 4; ++i) v[bi][i] = (k + i < op.k_real) ? __half2float(a.x_in[k + i]) : 0.f;
+            }
+          }
+        } else if (!DEC) {
+          // counted source: one u64 word per element; every word's contributor count is checked
+          // against the source n-group's (static) contributor number, re-reading the batch until
+          // all have landed (rare after the hint wait).  silu(g) * u reads the two halves in turn.
+          const unsigned long long* sa = src->acc + (long long)par * src->n_tiles * kTile;
+          for (int which = 0; which < (op.act == 1 ? 2 : 1); ++which) {
+            unsigned long long w[SB][4];
+            int want[SB];
+#pragma unroll
+            for (int bi = 0; bi < SB; ++bi) {
+              const int k = kb + bi * 4 * E_NCW * 32;
+              want[bi] = k < khi ? (int)__ldg(src->nslots + ((op.src_col + which * op.act_off + k) >> 6)) : 0;
+            }
+            for (;;) {
+#pragma unroll
+              for (int bi = 0; bi < SB; ++bi) {
+                const int k = kb + bi * 4 * E_NCW * 32;
+                const int n = op.src_col + which * op.act_off + k;
+                if (k < khi) {
+                  ld_relaxed_u64x2(sa + n, w[bi][0], w[bi][1]);
+                  ld_relaxed_u64x2(sa + n + 2, w[bi][2], w[bi][3]);
+                } else {
+                  w[bi][0] = w[bi][1] = w[bi][2] = w[bi][3] = 0ull;
+                }
+              }
+              bool ok = true;
+#pragma unroll
+              for (int bi = 0; bi < SB; ++bi)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) ok = ok && fix_count(w[bi][i]) == want[bi];
+              if (ok) break;
+              __nanosleep(64);
+            }
+#pragma unroll
+            for (int bi = 0; bi < SB; ++bi) {
+              const int k = kb + bi * 4 * E_NCW * 32;
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float x = fix_decode(w[bi][i], want[bi]) * op.in_alpha;
+                const float g = which == 0 ? x : __fdividef(v[bi][i], 1.f + __expf(-v[bi][i])) * x;
+                v[bi][i] = (k + i < op.k_real) ? g : 0.f;
+              }
             }
           }
         } else {
@@ -750,6 +874,8 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
     if (threadIdx.x == 0 && c == 0) atomicExch(a.status, PMPD_ERR_CONTRACT);
     p = p < 1 ? 1 : 4;
   }
+  // launch epoch (counted programs): advanced by the last CTA to finish, read by all at start
+  const unsigned epoch = DEC ? 0u : ld_relaxed_u32(a.bar + 2);
   const int stage_bytes = E_STILES * (p + 1) * kTilePlaneBytes;
   uint32_t dyn_bytes;
   asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn_bytes));
@@ -778,8 +904,10 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
       const uint64_t pol = policy_evict_first();
       int slot = 0, used = 0;
       uint32_t phase = 0;
+      for (int oi = 1; oi < PMPD_ENGINE_PF && oi < a.n_ops; ++oi) prefetch_op(a.ops[oi], c, G, p);
       for (int oi = 0; oi < a.n_ops; ++oi) {
         const EngineOp& op = a.ops[oi];
+        if (PMPD_ENGINE_PF > 0 && oi + PMPD_ENGINE_PF < a.n_ops) prefetch_op(a.ops[oi + PMPD_ENGINE_PF], c, G, p);
         if (DEC && op.kind == E_ATTN) continue;  // no weights
         const Range r = range_of(op, c, G);
         int t = r.T0, kt = r.T0 % r.KT;
@@ -810,6 +938,7 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
     // ------------------------------------------------------------ epilogue
     float* red = reinterpret_cast<float*>(smem + kSmRed);
     float* redb = reinterpret_cast<float*>(smem + kSmRedb);
+    const int par = (int)(epoch & 1u);
     int seg = 0;
     for (int oi = 0; oi < a.n_ops; ++oi) {
       const EngineOp& op = a.ops[oi];
@@ -827,15 +956,20 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
         float bsum = 0.f;
 #pragma unroll
         for (int w = 0; w < E_NCW; ++w) bsum += redb[buf * E_NCW + w];
-        // split-K: every CTA holding tiles of n-group ng adds its partial at L2
+        // split-K: every CTA holding tiles of n-group ng adds its partial at L2 (counted
+        // fixed point in linear-stack programs, f32 in decoder programs)
         float* dst = op.part + (int64_t)ng * 64;
+        unsigned long long* dsta = DEC ? nullptr : op.acc + ((long long)par * op.n_tiles + ng) * 64;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int nl = lane + 32 * h;
           float v = bsum;
 #pragma unroll
           for (int w = 0; w < E_NCW; ++w) v += red[(buf * E_NCW + w) * 64 + nl];
-          atomicAdd(dst + nl, DEC ? v * op.out_alpha : v);
+          if (DEC)
+            atomicAdd(dst + nl, v * op.out_alpha);
+          else
+            red_relaxed_u64(dsta + nl, fix_encode(v, a.status));
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars.red_empty[buf]);
@@ -848,7 +982,17 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
         }
       }
       __syncwarp();  // lane 0's release covers the warp's partial stores (cumulativity)
-      if (lane == 0) {
+      if (!DEC) {
+        // counted: a relaxed hint (the words carry their own completion), then zero this CTA's
+        // slice of the op's idle parity set for the next launch
+        if (lane == 0 && r.T1 > r.T0) {
+          asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar + 3 + oi) : "memory");
+          if (a.trace) a.trace[((int64_t)c * a.n_ops + oi) * 8 + 3] = gtimer();
+        }
+        const long long len = (long long)op.n_tiles * 64;
+        unsigned long long* other = op.acc + (long long)(par ^ 1) * len;
+        for (long long i = len * c / G + lane, e = len * (c + 1) / G; i < e; i += 32) other[i] = 0ull;
+      } else if (lane == 0) {
         // A CTA with no tiles in op oi must not publish it before every CTA has
         // published ops < oi: the ticket count is a completion test only if tickets
         // of op oi never precede the completion of op oi-1.
@@ -859,11 +1003,36 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
     }
   } else {
     // ------------------------------------------------------------ consumers
-    consumer_loop<DEC>(p, a, smem, bars, G, c, stage_bytes, nstage);
+    consumer_loop<DEC>(p, a, smem, bars, G, c, stage_bytes, nstage, epoch);
   }
   // ---------------------------------------------------------------- final output
   __syncthreads();
   const EngineOp& last = a.ops[a.n_ops - 1];
+  if constexpr (!DEC) {
+    // counted: CTA c finalizes n-groups c, c + G, ... of the last op from their complete words
+    const int par = (int)(epoch & 1u);
+    if (threadIdx.x == 0) wait_hint(a.bar + 3 + a.n_ops - 1, (epoch + 1u) * (unsigned)last.n_contrib);
+    __syncthreads();
+    const unsigned long long* la = last.acc + (long long)par * last.n_tiles * 64;
+    for (int ng = c; ng < last.n_tiles; ng += G) {
+      const int want = __ldg(last.nslots + ng);
+      for (int nl = threadIdx.x; nl < 64; nl += blockDim.x) {
+        const int n = ng * 64 + nl;
+        unsigned long long w = ld_relaxed_u64(la + n);
+        while (fix_count(w) != want) {
+          __nanosleep(64);
+          w = ld_relaxed_u64(la + n);
+        }
+        if (n < last.n_real) a.y_out[n] = a.y_alpha * fix_decode(w, want);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(a.bar + 1, 1u) == (unsigned)(G - 1)) {
+      a.bar[1] = 0;
+      a.bar[2] = epoch + 1u;  // read by the next launch (kernel boundary orders it)
+    }
+    return;
+  }
   if (threadIdx.x == 0) wait_tickets(a.bar, (unsigned)(a.n_ops * G));
   __syncthreads();
   for (int ng = c; ng < last.n_tiles; ng += G) {
@@ -1080,6 +1249,18 @@ int pmpd_engine_partition(const pmpd_qtensor* t, int32_t* bounds_host) {
     if (cover(mid, nullptr) <= G) hi = mid; else lo = mid + 1;
   }
   cover(lo, bounds_host);
+  return PMPD_OK;
+}
+
+int pmpd_engine_op_set_counted(void* op_host, void* acc_dev, const uint8_t* nslots_dev, int32_t n_contrib) {
+  if (!op_host || !acc_dev || !nslots_dev) return fail(PMPD_ERR_CONFIG, "null argument");
+  if (reinterpret_cast<uintptr_t>(acc_dev) & 15) return fail(PMPD_ERR_CONFIG, "counted accumulators must be 16-byte aligned");
+  if (n_contrib < 1 || n_contrib > num_sms()) return fail(PMPD_ERR_CONFIG, "bad contributor count %d", n_contrib);
+  EngineOp& op = *static_cast<EngineOp*>(op_host);
+  if (op.kind != E_LINEAR) return fail(PMPD_ERR_CONFIG, "counted accumulation applies to linear ops");
+  op.acc = static_cast<unsigned long long*>(acc_dev);
+  op.nslots = nslots_dev;
+  op.n_contrib = n_contrib;
   return PMPD_OK;
 }
 

@@ -16,9 +16,10 @@
 //   * producer warp (one lane): TMA -- one 64 k x 128 row box of x per token block (2-D tensor
 //     map, zero-filled past the last row) and the chunk's NG packed tiles as stored (planes
 //     0..p-1 + scale blocks, 1-D bulk copies).
-//   * 8 dequant warps: bucket indices -> f16 via exponent magic (two per LOP3), then
-//     hfma2(k, step, min) in f16 (the reference dequantize, quant.py:199-215, with f16 operands;
-//     pmpd_dequant keeps the bit-exact f32 form), W^T [n][k] (conflict-free swizzled 8 B stores); fence.proxy.async (their own smem stores only: every load is async-proxy TMA);
+//   * 16 dequant warps: bucket indices -> the reference's dequantized weight in f32,
+//     fmaf(k, step, min) (bit-exact with quant.py:199-215), rounded once to f16 (FADD2/FFMA2 on
+//     two weights per instruction), W^T [n][k] (conflict-free swizzled 8 B stores);
+//     fence.proxy.async (their own smem stores only: every load is async-proxy TMA);
 //     then one thread issues MB x 4 tcgen05.mma.cta_group::1.kind::f16 (M128 N64*NG K16, f32
 //     accumulators in TMEM) and tcgen05.commit frees the stage.  Each dequantized weight tile
 //     feeds MB*128 tokens and each x box NG*64 outputs; (NG, MB) are chosen per launch to
@@ -164,6 +165,31 @@ struct GemmArgs {
 };
 
 // ------------------------------------------------------------------ weight dequant
+// Packed f32x2 arithmetic (sm_100 FADD2 / FFMA2: each lane is an IEEE fma.rn / add.rn).
+PMPD_DEV float2 add2(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "add.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+PMPD_DEV float2 fma2(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("{\n\t.reg .b64 a, b, c, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\tmov.b64 c, {%6, %7};\n\t"
+      "fma.rn.f32x2 d, a, b, c;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+// Bytes j0, j0+1 of w hold bucket indices k (< 256): f16x2 of fmaf(k, step, min), rounded once.
+PMPD_DEV uint32_t bucket_pair_f16(uint32_t w, int j0, float2 step, float2 mn) {
+  const float2 kf = add2(make_float2(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540 + j0)),
+                                     __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7541 + j0))),
+                         make_float2(-8388608.f, -8388608.f));  // 2^23 + k - 2^23 = k, exact
+  const float2 v = fma2(kf, step, mn);
+  const __half2 h = __floats2half2_rn(v.x, v.y);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
 // Thread (L, w, half) decodes m-tiles 2*half, 2*half+1 of word w of lane chunk L of the chunk's
 // packed tile (16 codes, layout.cuh kn_tile_coord) and writes W^T[n][k] in f16.
 template <int P>
@@ -176,36 +202,28 @@ PMPD_DEV void dequant_unit(const uint8_t* pl, int pstride, const uint8_t* scl, i
   const float* sc = reinterpret_cast<const float*>(scl);
   const float4 d4 = *reinterpret_cast<const float4*>(sc + kb);
   const float4 m4 = *reinterpret_cast<const float4*>(sc + 64 + kb);
-  // f16 step / min pairs of (kb, kb+1) and (kb+2, kb+3): the GEMM computes in f16 (the f32
-  // reference dequantize stays bit-exact in pmpd_dequant; here one f16 rounding of each operand)
-  const __half2 d01 = __floats2half2_rn(d4.x, d4.y), d23 = __floats2half2_rn(d4.z, d4.w);
-  const __half2 m01 = __floats2half2_rn(m4.x, m4.y), m23 = __floats2half2_rn(m4.z, m4.w);
+  // Each weight is the reference's dequantized value in f32, fmaf(k, step, min) (bit-exact with
+  // float32(dequantize(qt, p)), quant.py:199-215), rounded ONCE to f16 for the tensor core: the
+  // same operand precision as the fp16 baseline.  (Rounding step and min to f16 first puts one
+  // shared error on all 64 weights of a group; through a model that bias reached 2e-2 logits
+  // error on an ill-conditioned step, tools/prefill_rounding_probe.py.)  Two weights per
+  // instruction: k -> f32 by the 2^23 exponent magic, then FADD2 / FFMA2 / F2FP.PACK.
+  const float2 d01 = make_float2(d4.x, d4.y), d23 = make_float2(d4.z, d4.w);
+  const float2 m01 = make_float2(m4.x, m4.y), m23 = make_float2(m4.z, m4.w);
   constexpr uint32_t kLoaded = ((1u << 4) - 1) & ~((1u << (4 - P)) - 1);
   constexpr uint32_t kConst = (P < 4) ? (1u << (4 - P - 1)) : 0u;
-  // low nibble under exponent 25 = 1024 + k, high nibble under exponent 21 = 64 + k (both exact)
-  const __half2 c1024 = __floats2half2_rn(1024.f, 1024.f), c64 = __floats2half2_rn(64.f, 64.f);
+  constexpr uint32_t kl = kLoaded * 0x01010101u, kc = kConst * 0x01010101u;
   const uint32_t pe[4] = {pw[0], pw[1], pw[2], pw[3]};
 #define PMPD_G_T(T)                                                                                  \
   {                                                                                                  \
     uint32_t u = merge_planes<4, P, T>(pe);                                                          \
     u = T ? rotr32(u, T) : u; /* nibble slot s = bucket index of row 16T+gq+8(s&1), k = kb+(s>>1) */ \
-    const uint32_t kl = kLoaded * 0x00010001u, kc = kConst * 0x00010001u;                            \
-    const uint32_t p01 = __byte_perm(u, 0u, 0x4140), p23 = __byte_perm(u, 0u, 0x4342);               \
-    const uint32_t e01 = lop3_and_or(p01, kl, kc | 0x64006400u);                                     \
-    const uint32_t e23 = lop3_and_or(p23, kl, kc | 0x64006400u);                                     \
-    const uint32_t o01 = lop3_and_or(p01, kl << 4, (kc << 4) | 0x54005400u);                         \
-    const uint32_t o23 = lop3_and_or(p23, kl << 4, (kc << 4) | 0x54005400u);                         \
-    const __half2 we01 = __hfma2(__hsub2(*reinterpret_cast<const __half2*>(&e01), c1024), d01, m01); \
-    const __half2 we23 = __hfma2(__hsub2(*reinterpret_cast<const __half2*>(&e23), c1024), d23, m23); \
-    const __half2 wo01 = __hfma2(__hsub2(*reinterpret_cast<const __half2*>(&o01), c64), d01, m01);   \
-    const __half2 wo23 = __hfma2(__hsub2(*reinterpret_cast<const __half2*>(&o23), c64), d23, m23);   \
-    uint2 ve, vo;                                                                                    \
-    ve.x = *reinterpret_cast<const uint32_t*>(&we01);                                                \
-    ve.y = *reinterpret_cast<const uint32_t*>(&we23);                                                \
-    vo.x = *reinterpret_cast<const uint32_t*>(&wo01);                                                \
-    vo.y = *reinterpret_cast<const uint32_t*>(&wo23);                                                \
-    *reinterpret_cast<uint2*>(sb + sw128_off(16 * T + gq, kb)) = ve;                                 \
-    *reinterpret_cast<uint2*>(sb + sw128_off(16 * T + gq + 8, kb)) = vo;                             \
+    const uint32_t ev = lop3_and_or(u, kl, kc);          /* byte j = bucket index (row gq, kb+j) */  \
+    const uint32_t od = lop3_and_or(u >> 4, kl, kc);     /* byte j = bucket index (row gq+8, kb+j) */\
+    const uint32_t ve0 = bucket_pair_f16(ev, 0, d01, m01), ve1 = bucket_pair_f16(ev, 2, d23, m23);   \
+    const uint32_t vo0 = bucket_pair_f16(od, 0, d01, m01), vo1 = bucket_pair_f16(od, 2, d23, m23);   \
+    *reinterpret_cast<uint2*>(sb + sw128_off(16 * T + gq, kb)) = make_uint2(ve0, ve1);               \
+    *reinterpret_cast<uint2*>(sb + sw128_off(16 * T + gq + 8, kb)) = make_uint2(vo0, vo1);           \
   }
   if (half == 0) {
     PMPD_G_T(0)

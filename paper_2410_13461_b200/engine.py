@@ -3,10 +3,11 @@ decode token in one cooperative kernel, with the weight stream never waiting on 
 
 A ``Program`` is a chain of GEMV ops over KN-packed tensors; op ``i`` consumes
 ``in_alpha * y_src[src_col:...]`` (optionally ``silu(g) * u``) of an earlier
-op, or the external f16 input for ``src = -1``.  Each op's output is an f32
-vector in HBM into which the CTAs sharing an n-group add their split-K partials
-(L2 atomics; summation order not fixed); the last op's output, scaled by
-``y_alpha``, lands in ``y_out``.  The kernel re-zeroes the vectors on exit.  The reference path this replaces is the
+op, or the external f16 input for ``src = -1``.  The CTAs sharing an n-group
+add their split-K partials into the op's output vector at L2: in a linear-stack
+program as counted 2^-24 fixed-point u64 words (deterministic, self-validating:
+no grid-wide ticket between ops), in a decoder program as f32 (order not fixed).
+The last op's output, scaled by ``y_alpha``, lands in ``y_out``.  The reference path this replaces is the
 sequence of ``h @ model.weights(name, p)`` calls of one decode step
 (pkg/src/pmpd/tinylm.py:341-368).
 """
@@ -72,6 +73,10 @@ class Program:
         grid = lib.pmpd_engine_grid()
         self.ops = ops
         self.parts = []
+        # decoder-step op kinds run in the engine's decoder instantiation (f32 accumulation + ticket);
+        # plain chains use counted fixed-point accumulation
+        self.decoder = any(sp.attn is not None or sp.in_mode != IN_SRC or sp.out is not None or sp.out_alpha != 1.0
+                           for sp in ops)
         host = (ctypes.c_uint8 * (nbytes * len(ops)))()
         for i, spec in enumerate(ops):
             if spec.src >= i:
@@ -100,13 +105,38 @@ class Program:
             self.parts.append((part, ns, spec.resid, spec.gain))
             _capi.call("pmpd_engine_make_op", spec.packed.ref(), spec.src, spec.src_col, spec.act, spec.act_off,
                        float(spec.in_alpha), part.data_ptr(), slots, ns.data_ptr(), addr)
-            if os.environ.get("PMPD_ENGINE_EVEN", "0") != "1":
+            desc = spec.packed.desc
+            if spec.src >= 0 and ops[spec.src].packed is not None:
+                width = spec.src_col + (spec.act_off if spec.act == 1 else 0) + desc.k_tiles * 64
+                if width > ops[spec.src].packed.desc.n_tiles * 64:
+                    raise ConfigError(f"op {i} reads past the end of op {spec.src}'s output")
+            even = os.environ.get("PMPD_ENGINE_EVEN", "0") == "1"
+            b_host = (ctypes.c_int32 * (grid + 1))()
+            if even:
+                ntl = desc.n_tiles * desc.k_tiles
+                for c in range(grid + 1):
+                    b_host[c] = c * ntl // grid
+            else:
                 # cost-balanced CTA tile ranges (stage/segment aware) instead of an even tile split
-                b_host = (ctypes.c_int32 * (grid + 1))()
                 _capi.call("pmpd_engine_partition", spec.packed.ref(), ctypes.addressof(b_host))
-                bounds = torch.frombuffer(bytearray(b_host), dtype=torch.int32).cuda()
-                self.parts.append((bounds,))
-                _capi.call("pmpd_engine_op_set_bounds", addr, bounds.data_ptr())
+            bounds = torch.frombuffer(bytearray(b_host), dtype=torch.int32).cuda()
+            self.parts.append((bounds,))
+            _capi.call("pmpd_engine_op_set_bounds", addr, bounds.data_ptr())
+            if not self.decoder:
+                # counted accumulation: contributors per n-group from the partition, two parity sets
+                kt, cnt, contrib = desc.k_tiles, [0] * desc.n_tiles, 0
+                for c in range(grid):
+                    t0, t1 = b_host[c], b_host[c + 1]
+                    if t1 > t0:
+                        contrib += 1
+                        for ng in range(t0 // kt, (t1 - 1) // kt + 1):
+                            cnt[ng] += 1
+                if max(cnt) > 255 or min(cnt) < 1:
+                    raise ConfigError(f"op {i}: n-group contributor counts outside 1..255")
+                acc = torch.zeros(2 * desc.n_tiles * 64, dtype=torch.int64, device="cuda")
+                cs = torch.tensor(cnt, dtype=torch.uint8, device="cuda")
+                self.parts.append((acc, cs))
+                _capi.call("pmpd_engine_op_set_counted", addr, acc.data_ptr(), cs.data_ptr(), contrib)
             if spec.in_mode != IN_SRC or spec.out is not None or spec.out_alpha != 1.0:
                 if spec.in_mode == IN_ATTN and (spec.src < 0 or ops[spec.src].attn is None):
                     raise ConfigError(f"op {i}: IN_ATTN needs an attention source op")
@@ -115,13 +145,10 @@ class Program:
                            spec.gain.data_ptr() if spec.gain is not None else None, float(spec.eps),
                            int(spec.out is not None), float(spec.out_alpha))
         self.table = torch.frombuffer(bytearray(host), dtype=torch.uint8).cuda()
-        self.bar = torch.zeros(2, dtype=torch.int32, device="cuda")
+        self.bar = torch.zeros(3 + len(ops), dtype=torch.int32, device="cuda")
         self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.y_alpha = float(y_alpha)
         self.n_out = ops[-1].packed.desc.n
-        # decoder-step op kinds run in the engine's decoder instantiation
-        self.decoder = any(sp.attn is not None or sp.in_mode != IN_SRC or sp.out is not None or sp.out_alpha != 1.0
-                           for sp in ops)
 
     def run_traced(self, x_in, p_dev, y_out):
         """One pass recording the per-CTA per-op timeline; returns int64 [grid, n_ops, 8]: 4 timestamps (ns), warp-0 tile cycles, tile calls, loop cycles."""

@@ -1,4 +1,5 @@
-"""Time the 7B linear stack per token: per-op GEMV chain vs persistent engine (graph replays)."""
+"""Time the 7B linear stack per token through the persistent engine (graph replays); with
+``--per-op`` also the per-op GEMV chain.  PMPD_LIB selects a library variant."""
 import os
 import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -7,7 +8,8 @@ from paper_2410_13461_b200.stack import LLAMA2_7B, LinearStack, algorithmic_byte
 
 st = LinearStack(LLAMA2_7B, seed=1)
 st.build_engine()
-for name, fn in (("per-op", st.token), ("engine", st.token_engine)):
+fns = (("per-op", st.token), ("engine", st.token_engine)) if "--per-op" in sys.argv else (("engine", st.token_engine),)
+for name, fn in fns:
     g = st.capture(fn)
     for p in (4, 3, 2):
         st.set_schedule({p: 0})

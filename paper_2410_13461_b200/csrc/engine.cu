@@ -92,6 +92,15 @@ constexpr int E_ASPLIT = 4;  // context splits per head in the attention op
 PMPD_DEV int attn_rec(int dh) { return 4 + dh; }  // record: m, l, pad, pad, acc[dh] (16-byte aligned acc)
 
 // ---- counted fixed-point words: [63:56] contributors, [55:0] sum of (rint(v * 2^24) + 2^47)
+#ifndef PMPD_ENGINE_NOHINT
+#define PMPD_ENGINE_NOHINT 1       // 0: consumers first wait for the relaxed per-op hint counter (measured slower)
+#endif
+#ifndef PMPD_ENGINE_RETRY_NS
+#define PMPD_ENGINE_RETRY_NS 32    // back-off between re-reads of incomplete words
+#endif
+#ifndef PMPD_ENGINE_HINT_RELEASE
+#define PMPD_ENGINE_HINT_RELEASE 0 // 1: the hint add is a release (orders the data adds before it)
+#endif
 constexpr int kCntShift = 56;
 constexpr unsigned long long kValMask = (1ull << kCntShift) - 1;
 constexpr long long kFixOff = 1ll << 47;       // per-contribution offset: keeps every addend >= 0
@@ -554,7 +563,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
       if (threadIdx.x == 0) wait_tickets(a.bar, (unsigned)(oi * G));
       named_bar_sync(1, E_NCW * 32);
     }
-    if (!DEC && op.src >= 0 && r.T1 > r.T0) {
+    if (!DEC && !PMPD_ENGINE_NOHINT && op.src >= 0 && r.T1 > r.T0) {
       // counted: wait (relaxed) until every contributor of the source op has issued its
       // additions; the staging below validates each word's count, so this only avoids polling
       // the data lines while they are still being produced
@@ -700,7 +709,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
 #pragma unroll
                 for (int i = 0; i < 4; ++i) ok = ok && fix_count(w[bi][i]) == want[bi];
               if (ok) break;
-              __nanosleep(64);
+              if (PMPD_ENGINE_RETRY_NS) __nanosleep(PMPD_ENGINE_RETRY_NS);
             }
 #pragma unroll
             for (int bi = 0; bi < SB; ++bi) {
@@ -986,7 +995,10 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
         // counted: a relaxed hint (the words carry their own completion), then zero this CTA's
         // slice of the op's idle parity set for the next launch
         if (lane == 0 && r.T1 > r.T0) {
-          asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar + 3 + oi) : "memory");
+          if (PMPD_ENGINE_HINT_RELEASE)
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar + 3 + oi) : "memory");
+          else
+            asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar + 3 + oi) : "memory");
           if (a.trace) a.trace[((int64_t)c * a.n_ops + oi) * 8 + 3] = gtimer();
         }
         const long long len = (long long)op.n_tiles * 64;

@@ -229,6 +229,36 @@ PMPD_DEV void prefetch_op(const EngineOp& op, int c, int G, int p) {
   bulk_prefetch_l2(op.scales + (int64_t)r.T0 * kTileScaleBytes, (uint32_t)(r.T1 - r.T0) * kTileScaleBytes);
 }
 
+// Rolling L2 prefetch (PMPD_ENGINE_PFT tiles ahead of the TMA loads, issued in step with them):
+// the cursor (pop, pt) walks this CTA's tiles op by op; pt < 0 = start of op pop's range.
+#ifndef PMPD_ENGINE_PFT
+#define PMPD_ENGINE_PFT 0
+#endif
+PMPD_DEV void pf_advance(const EngineOp* ops, int n_ops, int c, int G, int p, int& pop, int& pt, int n) {
+  while (n > 0 && pop < n_ops) {
+    const EngineOp& op = ops[pop];
+    if (op.kind != E_LINEAR) {
+      ++pop;
+      pt = -1;
+      continue;
+    }
+    const Range r = range_of(op, c, G);
+    if (pt < r.T0) pt = r.T0;
+    const int m = min(n, r.T1 - pt);
+    if (m > 0) {
+      const uint32_t nb = (uint32_t)m * kTilePlaneBytes;
+      for (int j = 0; j < p; ++j) bulk_prefetch_l2(op.planes + j * op.plane_bytes + (int64_t)pt * kTilePlaneBytes, nb);
+      bulk_prefetch_l2(op.scales + (int64_t)pt * kTileScaleBytes, (uint32_t)m * kTileScaleBytes);
+      pt += m;
+      n -= m;
+    }
+    if (pt >= r.T1) {
+      ++pop;
+      pt = -1;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ attention op
 // One decode query over the KV cache of one layer (tinylm.py:344-358), as engine work units
 // (head h, split s): RoPE of q (and of the new k, by the unit holding position T, which also
@@ -914,6 +944,8 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
       int slot = 0, used = 0;
       uint32_t phase = 0;
       for (int oi = 1; oi < PMPD_ENGINE_PF && oi < a.n_ops; ++oi) prefetch_op(a.ops[oi], c, G, p);
+      int pf_op = 0, pf_t = -1;
+      if (PMPD_ENGINE_PFT > 0) pf_advance(a.ops, a.n_ops, c, G, p, pf_op, pf_t, PMPD_ENGINE_PFT);
       for (int oi = 0; oi < a.n_ops; ++oi) {
         const EngineOp& op = a.ops[oi];
         if (PMPD_ENGINE_PF > 0 && oi + PMPD_ENGINE_PF < a.n_ops) prefetch_op(a.ops[oi + PMPD_ENGINE_PF], c, G, p);
@@ -932,6 +964,7 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
                             &bars.full[slot], pol);
           bulk_g2s_stream(st + p * E_STILES * kTilePlaneBytes, op.scales + (int64_t)t * kTileScaleBytes,
                           cnt * kTileScaleBytes, &bars.full[slot], pol);
+          if (PMPD_ENGINE_PFT > 0) pf_advance(a.ops, a.n_ops, c, G, p, pf_op, pf_t, cnt);
           kt += cnt;
           if (kt == r.KT) kt = 0;
           t = end;

@@ -185,12 +185,15 @@ int pmpd_sched_step(const int32_t* sched_dev, int32_t n_prec, int32_t* step_dev,
  * persistent kernel (replaces the per-layer h @ weights(name, p) calls of a
  * reference decode step, tinylm.py:341-368).  A program is a device array of
  * opaque op records (pmpd_engine_op_bytes() each) built with
- * pmpd_engine_make_op; op i reads the f16 vector in_alpha * (output of op src)
- * [src_col ...] (act 0) or silu(g)*u (act 1), or x_in for src = -1, and
- * writes split-K partials to part_dev ([n_tiles][max_slots][64] f32); the last
- * op's output is reduced into y_out (f32) scaled by y_alpha.  bar_dev: two
- * zero-initialised uint32 (self-resetting).  Weights are streamed at the
- * precision *p_dev (planes 0..p-1 only). */
+ * pmpd_engine_make_op + pmpd_engine_op_set_bounds + pmpd_engine_op_set_counted;
+ * op i reads the f16 vector in_alpha * (output of op src)[src_col ...] (act 0)
+ * or silu(g)*u (act 1), or x_in for src = -1.  Split-K partials are added into
+ * counted fixed-point words (see pmpd_engine_op_set_counted): deterministic,
+ * and complete when their contributor count is reached, so ops follow each other
+ * without a grid barrier.  The last op's output lands in y_out (f32) scaled by
+ * y_alpha.  bar_dev: 3 + 2 * n_ops zero-initialised uint32 (epoch and counters,
+ * kept across launches).  Weights are streamed at the precision *p_dev (planes
+ * 0..p-1 only).  part_dev / max_slots of pmpd_engine_make_op are unused (ABI). */
 int pmpd_engine_op_bytes(void);
 int pmpd_engine_grid(void);
 int pmpd_engine_max_slots(const pmpd_qtensor* t);
@@ -201,19 +204,20 @@ int pmpd_engine_make_op(const pmpd_qtensor* t, int32_t src, int32_t src_col, int
                         void* op_host);
 /* Decoder-step ops (a whole batch-1 decode step in one engine launch; tinylm.py:334-368):
  *   pmpd_engine_op_set_io: after pmpd_engine_make_op, switch the op's input to
- *     in_mode 2 = RMSNorm(resid) * gain over the whole f32 row (tinylm.py:293-295, 337/345/349) or
- *     in_mode 3 = the combined records of the attention op `src`, and/or make `part` a persistent
- *     vector (keep_out = 1: the residual stream; the op's output is ADDED into it, x += ctx @ Wo /
- *     x += a @ W_down, tinylm.py:359/364), scaled by out_alpha.
+ *     in_mode 2 = RMSNorm(residual stream) * gain over the whole row (tinylm.py:293-295,
+ *     337/345/349) or in_mode 3 = the combined records of the attention op `src`; keep_out = 1
+ *     makes the op a residual op (its output is ADDED into the residual stream, x += ctx @ Wo /
+ *     x += a @ W_down, tinylm.py:359/364), scaled by out_alpha.  resid_dev is unused (the stream
+ *     is an argument of pmpd_engine_run_decoder).
  *   pmpd_engine_make_attn_op: attention over one layer's f16 KV cache for the new token: q|k|v =
- *     the f32 output of op `src`; RoPE at position T = *T_dev (cos/sin [max_ctx][d_head/2]);
- *     k, v appended to row T; records_dev holds pmpd_engine_attn_records() f32.
+ *     the output of op `src`; RoPE at position T = *T_dev (cos/sin [max_ctx][d_head/2]);
+ *     k, v appended to row T; records_dev = u64 [2][pmpd_engine_attn_records()].
  *     d_head in {32, 64, 128, 256}. */
 int pmpd_engine_op_set_io(void* op_host, int32_t in_mode, const float* resid_dev, const float* gain_dev, float eps,
                           int32_t keep_out, float out_alpha);
 int pmpd_engine_make_attn_op(int32_t src, int32_t n_heads, int32_t d_head, void* k_cache_dev, void* v_cache_dev,
                              const float* cos_dev, const float* sin_dev, const int32_t* T_dev, int32_t max_ctx,
-                             float scale, float* records_dev, void* op_host);
+                             float scale, void* records_dev, void* op_host);
 int pmpd_engine_attn_records(int32_t n_heads, int32_t d_head);
 /* Cost-balanced CTA tile ranges for one op (bounds_host: pmpd_engine_grid() + 1 ints): the ranges
  * minimise the largest per-CTA cost of stage calls and n-group flushes instead of splitting the tiles
@@ -227,9 +231,17 @@ int pmpd_engine_op_set_bounds(void* op_host, const int32_t* bounds_dev);
  * per n-group under the op's bounds, n_contrib = CTAs with a nonempty range.  bar_dev of the run
  * then holds 3 + n_ops u32 (tickets, done, launch epoch, per-op hint counters), zeroed once. */
 int pmpd_engine_op_set_counted(void* op_host, void* acc_dev, const uint8_t* nslots_dev, int32_t n_contrib);
-/* pmpd_engine_run for programs that use the decoder-step ops above (a separate kernel
- * instantiation, so the linear-stack program pays nothing for them); trace_dev optional. */
-int pmpd_engine_run_decoder(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, float* y_out_dev, float y_alpha,
+/* Decoder programs (pmpd_engine_run_decoder): every linear op is counted (pmpd_engine_op_set_counted);
+ * the o / down ops (keep_out) add into ONE counted residual stream resid_dev = u64 [2][resid_len]
+ * (resid_len = d rounded up to 64, zero-initialised), into which the launch first adds x0_dev (f32
+ * [d_real], the embedding row written before the launch).  An RMSNorm op reads the stream when each
+ * word's contribution count reaches cum_dev[n-group] (u16, static: 1 + the contributors of every
+ * residual op before it); a residual op passes rwait = the index of the RMSNorm op whose readers
+ * must have read the stream before it adds (-1: none).  Attention records are single-writer words,
+ * records_dev = u64 [2][pmpd_engine_attn_records()].  bar_dev holds 3 + 2 * n_ops u32. */
+int pmpd_engine_op_set_residual(void* op_host, const uint16_t* cum_dev, int32_t rwait);
+int pmpd_engine_run_decoder(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const float* x0_dev,
+                            void* resid_dev, int64_t resid_len, int32_t d_real, float* y_out_dev, float y_alpha,
                             uint32_t* bar_dev, int32_t* status_dev, int64_t* trace_dev, void* stream);
 
 int pmpd_engine_run(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const void* x_in_dev, float* y_out_dev,

@@ -63,7 +63,13 @@ class OpSpec:
 
 
 class Program:
-    """Device-resident op table + partial buffers + the engine's completion counters."""
+    """Device-resident op table, counted accumulators and the engine's epoch / counters.
+
+    Every linear op gets a cost-balanced CTA partition and a counted fixed-point output (u64
+    [2 parity sets][n_tiles * 64]; per n-group contributor counts from the partition).  In a
+    decoder program the residual ops (``out`` set: o and down) instead add into ONE counted
+    residual stream, into which the launch first adds the f32 embedding row ``x_in``; every
+    RMSNorm op carries the static count each residual word has reached at that point."""
 
     def __init__(self, ops: list, y_alpha: float = 1.0):
         if not ops:
@@ -73,10 +79,22 @@ class Program:
         grid = lib.pmpd_engine_grid()
         self.ops = ops
         self.parts = []
-        # decoder-step op kinds run in the engine's decoder instantiation (f32 accumulation + ticket);
-        # plain chains use counted fixed-point accumulation
+        # decoder-step op kinds (attention, RMSNorm / attention-combine inputs, residual outputs)
+        # run in the engine's decoder instantiation
         self.decoder = any(sp.attn is not None or sp.in_mode != IN_SRC or sp.out is not None or sp.out_alpha != 1.0
                            for sp in ops)
+        self.R = None
+        self.d_real = 0
+        running = None   # decoder: contributions per residual n-group so far (x0 = 1)
+        last_rms = -1
+        if self.decoder:
+            rms = [sp for sp in ops if sp.in_mode == IN_RMSNORM]
+            if not rms:
+                raise ConfigError("decoder program without an RMSNorm input op")
+            self.d_real = rms[0].packed.desc.k
+            d_tiles = rms[0].packed.desc.k_tiles
+            self.R = torch.zeros(2 * d_tiles * 64, dtype=torch.int64, device="cuda")
+            running = [1] * d_tiles
         host = (ctypes.c_uint8 * (nbytes * len(ops)))()
         for i, spec in enumerate(ops):
             if spec.src >= i:
@@ -84,28 +102,22 @@ class Program:
             addr = ctypes.addressof(host) + i * nbytes
             if spec.attn is not None:
                 at = spec.attn
-                rec = torch.zeros(lib.pmpd_engine_attn_records(at.n_heads, at.d_head), dtype=torch.float32,
+                rec = torch.zeros(2 * lib.pmpd_engine_attn_records(at.n_heads, at.d_head), dtype=torch.int64,
                                   device="cuda")
                 self.parts.append((rec, at))
                 _capi.call("pmpd_engine_make_attn_op", spec.src, at.n_heads, at.d_head, at.k_cache.data_ptr(),
                            at.v_cache.data_ptr(), at.cos.data_ptr(), at.sin.data_ptr(), at.T_dev.data_ptr(),
                            at.max_ctx, float(at.scale), rec.data_ptr(), addr)
                 continue
-            slots = 1  # one accumulation vector per op (the kernel adds split-K partials at L2)
-            nt = spec.packed.desc.n_tiles
-            if spec.out is not None:
-                if spec.out.dtype != torch.float32 or spec.out.numel() < nt * 64 or not spec.out.is_contiguous():
-                    raise ConfigError(f"op {i}: the persistent output must be f32, contiguous, >= {nt * 64} long")
-                part = spec.out
-            else:
-                part = torch.zeros(nt * 64, dtype=torch.float32, device="cuda")
+            desc = spec.packed.desc
+            nt = desc.n_tiles
             ns_host = (ctypes.c_uint8 * nt)()
             _capi.call("pmpd_engine_nslots", spec.packed.ref(), ctypes.addressof(ns_host))
-            ns = torch.frombuffer(bytearray(ns_host), dtype=torch.uint8).cuda()
-            self.parts.append((part, ns, spec.resid, spec.gain))
+            ns0 = torch.frombuffer(bytearray(ns_host), dtype=torch.uint8).cuda()
+            part = torch.zeros(1, dtype=torch.float32, device="cuda")  # unused (op-table ABI)
+            self.parts.append((part, ns0, spec.resid, spec.gain))
             _capi.call("pmpd_engine_make_op", spec.packed.ref(), spec.src, spec.src_col, spec.act, spec.act_off,
-                       float(spec.in_alpha), part.data_ptr(), slots, ns.data_ptr(), addr)
-            desc = spec.packed.desc
+                       float(spec.in_alpha), part.data_ptr(), 1, ns0.data_ptr(), addr)
             if spec.src >= 0 and ops[spec.src].packed is not None:
                 width = spec.src_col + (spec.act_off if spec.act == 1 else 0) + desc.k_tiles * 64
                 if width > ops[spec.src].packed.desc.n_tiles * 64:
@@ -122,56 +134,78 @@ class Program:
             bounds = torch.frombuffer(bytearray(b_host), dtype=torch.int32).cuda()
             self.parts.append((bounds,))
             _capi.call("pmpd_engine_op_set_bounds", addr, bounds.data_ptr())
-            if not self.decoder:
-                # counted accumulation: contributors per n-group from the partition, two parity sets
-                kt, cnt, contrib = desc.k_tiles, [0] * desc.n_tiles, 0
-                for c in range(grid):
-                    t0, t1 = b_host[c], b_host[c + 1]
-                    if t1 > t0:
-                        contrib += 1
-                        for ng in range(t0 // kt, (t1 - 1) // kt + 1):
-                            cnt[ng] += 1
-                if max(cnt) > 255 or min(cnt) < 1:
-                    raise ConfigError(f"op {i}: n-group contributor counts outside 1..255")
-                acc = torch.zeros(2 * desc.n_tiles * 64, dtype=torch.int64, device="cuda")
-                cs = torch.tensor(cnt, dtype=torch.uint8, device="cuda")
-                self.parts.append((acc, cs))
-                _capi.call("pmpd_engine_op_set_counted", addr, acc.data_ptr(), cs.data_ptr(), contrib)
+            # counted accumulation: contributors per n-group from the partition
+            kt, cnt, contrib = desc.k_tiles, [0] * nt, 0
+            for c in range(grid):
+                t0, t1 = b_host[c], b_host[c + 1]
+                if t1 > t0:
+                    contrib += 1
+                    for ng in range(t0 // kt, (t1 - 1) // kt + 1):
+                        cnt[ng] += 1
+            if max(cnt) > 255 or min(cnt) < 1:
+                raise ConfigError(f"op {i}: n-group contributor counts outside 1..255")
+            cs = torch.tensor(cnt, dtype=torch.uint8, device="cuda")
+            residual = self.decoder and spec.out is not None
+            if residual:
+                if nt != len(running):
+                    raise ConfigError(f"op {i}: residual output width differs from the residual stream")
+                acc = self.R
+            else:
+                acc = torch.zeros(2 * nt * 64, dtype=torch.int64, device="cuda")
+            self.parts.append((acc, cs))
+            _capi.call("pmpd_engine_op_set_counted", addr, acc.data_ptr(), cs.data_ptr(), contrib)
             if spec.in_mode != IN_SRC or spec.out is not None or spec.out_alpha != 1.0:
                 if spec.in_mode == IN_ATTN and (spec.src < 0 or ops[spec.src].attn is None):
                     raise ConfigError(f"op {i}: IN_ATTN needs an attention source op")
-                _capi.call("pmpd_engine_op_set_io", addr, spec.in_mode,
-                           spec.resid.data_ptr() if spec.resid is not None else None,
+                _capi.call("pmpd_engine_op_set_io", addr, spec.in_mode, None,
                            spec.gain.data_ptr() if spec.gain is not None else None, float(spec.eps),
                            int(spec.out is not None), float(spec.out_alpha))
+            if self.decoder and (spec.in_mode == IN_RMSNORM or residual):
+                cum = None
+                if spec.in_mode == IN_RMSNORM:
+                    if desc.k_tiles != len(running):
+                        raise ConfigError(f"op {i}: RMSNorm input width differs from the residual stream")
+                    if max(running) > 1023:
+                        raise ConfigError("residual stream: more than 1023 contributions per word")
+                    cum = torch.tensor(running, dtype=torch.int32).to(torch.int16).cuda()
+                    self.parts.append((cum,))
+                _capi.call("pmpd_engine_op_set_residual", addr, cum.data_ptr() if cum is not None else None,
+                           last_rms if residual else -1)
+                if spec.in_mode == IN_RMSNORM:
+                    last_rms = i
+                if residual:
+                    running = [a + b for a, b in zip(running, cnt)]
         self.table = torch.frombuffer(bytearray(host), dtype=torch.uint8).cuda()
-        self.bar = torch.zeros(3 + len(ops), dtype=torch.int32, device="cuda")
+        self.bar = torch.zeros(3 + 2 * len(ops), dtype=torch.int32, device="cuda")
         self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
         self.y_alpha = float(y_alpha)
         self.n_out = ops[-1].packed.desc.n
+
+    def _launch(self, x_in, p_dev, y_out, trace):
+        s = torch.cuda.current_stream().cuda_stream
+        if self.decoder:
+            if x_in.dtype != torch.float32 or x_in.shape[-1] < self.d_real:
+                raise ConfigError("decoder program input must be the f32 embedding row")
+            _capi.call("pmpd_engine_run_decoder", self.table.data_ptr(), len(self.ops), p_dev.data_ptr(),
+                       x_in.data_ptr(), self.R.data_ptr(), self.R.numel() // 2, self.d_real, y_out.data_ptr(),
+                       self.y_alpha, self.bar.data_ptr(), self.status.data_ptr(), trace, s)
+        elif trace is not None:
+            _capi.call("pmpd_engine_run_traced", self.table.data_ptr(), len(self.ops), p_dev.data_ptr(),
+                       x_in.data_ptr(), y_out.data_ptr(), self.y_alpha, self.bar.data_ptr(), self.status.data_ptr(),
+                       trace, s)
+        else:
+            _capi.call("pmpd_engine_run", self.table.data_ptr(), len(self.ops), p_dev.data_ptr(), x_in.data_ptr(),
+                       y_out.data_ptr(), self.y_alpha, self.bar.data_ptr(), self.status.data_ptr(), s)
 
     def run_traced(self, x_in, p_dev, y_out):
         """One pass recording the per-CTA per-op timeline; returns int64 [grid, n_ops, 8]: 4 timestamps (ns), warp-0 tile cycles, tile calls, loop cycles."""
         g = _capi.lib().pmpd_engine_grid()
         tr = torch.zeros((g, len(self.ops), 8), dtype=torch.int64, device="cuda")
-        if self.decoder:
-            _capi.call("pmpd_engine_run_decoder", self.table.data_ptr(), len(self.ops), p_dev.data_ptr(),
-                       y_out.data_ptr(), self.y_alpha, self.bar.data_ptr(), self.status.data_ptr(), tr.data_ptr(),
-                       torch.cuda.current_stream().cuda_stream)
-        else:
-            _capi.call("pmpd_engine_run_traced", self.table.data_ptr(), len(self.ops), p_dev.data_ptr(),
-                       x_in.data_ptr(), y_out.data_ptr(), self.y_alpha, self.bar.data_ptr(), self.status.data_ptr(),
-                       tr.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        self._launch(x_in, p_dev, y_out, tr.data_ptr())
         torch.cuda.synchronize()
         return tr.cpu()
 
     def run(self, x_in: torch.Tensor, p_dev: torch.Tensor, y_out: torch.Tensor) -> None:
-        """Enqueue one pass (graph-capturable): y_out = y_alpha * chain(x_in) at precision *p_dev."""
-        if self.decoder:
-            _capi.call("pmpd_engine_run_decoder", self.table.data_ptr(), len(self.ops), p_dev.data_ptr(),
-                       y_out.data_ptr(), self.y_alpha, self.bar.data_ptr(), self.status.data_ptr(), None,
-                       torch.cuda.current_stream().cuda_stream)
-            return
-        _capi.call("pmpd_engine_run", self.table.data_ptr(), len(self.ops), p_dev.data_ptr(), x_in.data_ptr(),
-                   y_out.data_ptr(), self.y_alpha, self.bar.data_ptr(), self.status.data_ptr(),
-                   torch.cuda.current_stream().cuda_stream)
+        """Enqueue one pass (graph-capturable): y_out = y_alpha * chain(x_in) at precision *p_dev
+        (decoder programs: x_in = the f32 embedding row that starts the residual stream)."""
+        self._launch(x_in, p_dev, y_out, None)

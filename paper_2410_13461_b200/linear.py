@@ -36,9 +36,36 @@ class Workspace:
         if nbytes > self.nbytes:
             self.buf = torch.zeros(int(nbytes), dtype=torch.uint8, device=self.buf.device)
 
+    # byte offset of the status word (csrc/gemv.cu: kWsCounters u32 counters, then the status)
+    STATUS_OFFSET = 16384 * 4
+
     def status(self) -> int:
-        """Device status word set by GEMVs that saw an out-of-range precision (ContractViolation)."""
-        return 0
+        """Device status word: PMPD_ERR_CONTRACT after a GEMV saw a precision outside [1, p_max]
+        (the kernel clamps it, so the error must be surfaced).  Reads device memory (a sync)."""
+        if self.nbytes < self.STATUS_OFFSET + 4:
+            return 0
+        return int(self.buf[self.STATUS_OFFSET:self.STATUS_OFFSET + 4].view(torch.int32).item())
+
+    def check(self, what: str = "decode GEMV") -> None:
+        """Raise the error class of a nonzero status word (and clear it), errors.py taxonomy."""
+        raise_device_status(self.status(), what, self.clear_status)
+
+    def clear_status(self) -> None:
+        if self.nbytes >= self.STATUS_OFFSET + 4:
+            self.buf[self.STATUS_OFFSET:self.STATUS_OFFSET + 4].zero_()
+
+
+def raise_device_status(code: int, what: str, clear=None) -> None:
+    """Map a device status word to the reference error taxonomy (errors.py:8-25): CONTRACT ->
+    ContractViolation (precision outside the declared set), INPUT -> InputError (non-finite or
+    out-of-range activations)."""
+    if code == 0:
+        return
+    if clear is not None:
+        clear()
+    msgs = {_capi.ERR_CONTRACT: "a kernel read a precision outside the model's set",
+            _capi.ERR_INPUT: "non-finite or out-of-range activations"}
+    raise _capi._ERRORS.get(code, _capi.PmpdError)(f"{what}: {msgs.get(code, f'device status {code}')}")
 
 
 def workspace_bytes(pk: PackedTensor, m: int) -> int:

@@ -33,7 +33,7 @@ import torch
 
 from . import _capi
 from .errors import ConfigError, ContractViolation, FormatError, InputError
-from .linear import Workspace, gemm, gemv, gemv_fused, workspace_bytes
+from .linear import Workspace, gemm, gemv, gemv_fused, raise_device_status, workspace_bytes
 from .quant import BitPlaneStore, PrecisionSet, QuantizedTensor, dequantize, parse_model, quantize_tensor, \
     serialize_model
 from .schedule import PrecisionSchedule
@@ -650,6 +650,19 @@ class DecodeEngine:
         _capi.call("pmpd_push_token", self.buf.ids.data_ptr(), self.tokens.data_ptr(), self.n.data_ptr(),
                    self.cache.T_dev.data_ptr(), self.capacity, s)
 
+    def check_device(self) -> None:
+        """Surface the device error words (one host sync): non-finite logits, a GEMV or engine
+        status (precision outside the set -> ContractViolation, activations outside the
+        fixed-point range -> InputError), as the reference's checks would raise them."""
+        flags = torch.stack([self.buf.bad[0],
+                             self.buf.ws.buf[Workspace.STATUS_OFFSET:Workspace.STATUS_OFFSET + 4].view(torch.int32)[0],
+                             self.program.status[0] if self.program is not None else self.buf.bad[0] * 0]).cpu()
+        if int(flags[0]):
+            raise InputError("logits contain non-finite values")
+        raise_device_status(int(flags[1]), "decode GEMV", self.buf.ws.clear_status)
+        if self.program is not None:
+            raise_device_status(int(flags[2]), "decode engine", self.program.status.zero_)
+
     def capture(self) -> None:
         """Capture one decode step (after a prefill has set the counters)."""
         # snapshot the counters BEFORE the side stream is ordered after the current one: the
@@ -725,22 +738,24 @@ def generate(model: ModelVariants, prompt: Sequence[int], scheduler, sampler_cfg
     _capi.call("pmpd_push_token", eng.buf.ids.data_ptr(), eng.tokens.data_ptr(), eng.n.data_ptr(), 0, cap, s)
     eng.step.zero_()
     produced = 1
-    done = False
+    # decode step i runs at T = len(prompt) + i and needs T < max_context (tinylm.py:394-397)
+    limit = min(max_new, 1 + model.config.max_context - len(prompt))
     if max_new > 1:
         eng.capture()
-    while not done:
-        if int(eng.buf.bad.item()):
-            raise InputError("logits contain non-finite values")
+    while True:
+        eng.check_device()
         toks = eng.tokens[:produced].cpu().tolist()
-        if eos in toks or produced >= max_new:
+        if eos in toks or produced >= limit:
             break
-        k = min(check_every, max_new - produced)
+        k = min(check_every, limit - produced)
         for _ in range(k):
             eng.graph.replay()
         produced += k
     toks = eng.tokens[:produced].cpu().tolist()
     if eos in toks:
         toks = toks[:toks.index(eos) + 1]
+    elif produced < max_new:  # the reference's next decode_step would raise
+        raise InputError(f"context window full at {model.config.max_context} tokens")
     eng.cache.T = len(prompt) + len(toks) - 1
     hist = eng.hist[:len(toks)]
     hashes = [_logits_hash(r) for r in hist.double().cpu().numpy()] if record_logits else [""] * len(toks)

@@ -369,6 +369,8 @@ class TPModel:
         if hist is not None:
             hist[0].copy_(logits)
         produced = 1
+        # decode step i runs at T = len(prompt) + i and needs T < max_context (tinylm.py:394-397)
+        limit = min(max_new, 1 + cfg.max_context - len(prompt))
 
         def step():
             self._decode_token(bufs, tables, steps, tokens, counts, cap, hist)
@@ -394,15 +396,19 @@ class TPModel:
         while True:
             if int(bufs[0].bad.item()):
                 raise InputError("logits contain non-finite values")
+            for b in bufs:
+                b.ws.check("TP decode GEMV")
             toks = tokens[0][:produced].cpu().tolist()
-            if eos in toks or produced >= max_new:
+            if eos in toks or produced >= limit:
                 break
-            for _ in range(min(check_every, max_new - produced)):
+            for _ in range(min(check_every, limit - produced)):
                 step()
                 produced += 1
         toks = tokens[0][:produced].cpu().tolist()
         if eos in toks:
             toks = toks[:toks.index(eos) + 1]
+        elif produced < max_new:  # the reference's next decode_step would raise
+            raise InputError(f"context window full at {cfg.max_context} tokens")
         self.T = len(prompt) + len(toks) - 1
         for c in self.caches:
             c.T = self.T

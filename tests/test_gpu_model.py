@@ -273,3 +273,58 @@ def test_decode_capture_leaves_counters_unchanged(small):
         eng.capture()
         torch.cuda.synchronize()
         assert (int(eng.step), int(eng.n), int(eng.cache.T_dev)) == (5, 2, 9)
+
+
+def test_generate_context_window_like_reference(small):
+    """A decode step at T >= max_context raises InputError('context window full') unless EOS came
+    first (tinylm.py:394-397 inside generate's loop); up to the window the trace is produced."""
+    ref = om.Model.from_random(om.Config(n_layers=2, n_heads=2, d_model=64, d_ff=128, max_context=128), (4, 3, 2),
+                               seed=7)
+    prompt = [5 + (7 * i) % 250 for i in range(120)]
+    sch = StaticScheduler(PrecisionSchedule.two_phase(3, 2, 4, 64, p_prefill=4))
+    ok = tinylm.generate(small, prompt, sch, eos_id=-1, max_new=9)  # 1 + 128 - 120 tokens fit
+    assert len(ok.output_tokens) == 9
+    assert ok.output_tokens == om.generate(ref, prompt, osched_static(sch), eos_id=-1, max_new=9)[0]
+    with pytest.raises(InputError):
+        tinylm.generate(small, prompt, sch, eos_id=-1, max_new=10)
+    from oracle.errors import InputError as OracleInputError
+    with pytest.raises(OracleInputError):
+        om.generate(ref, prompt, osched_static(sch), eos_id=-1, max_new=10)
+
+
+def osched_static(sch):
+    s = sch.schedule
+    return om.StaticSched(osched.Schedule(tuple(s.precisions.precisions), s.p_prefill, dict(s.switch_points),
+                                          s.horizon))
+
+
+def test_generate_is_bit_reproducible():
+    """Same prompt, seed and schedule -> bit-identical logits and hashes on a
+    model whose n-groups are shared by several CTAs (the engine's counted accumulation)."""
+    cfg = tinylm.ModelConfig(n_layers=2, n_heads=8, d_model=1024, d_ff=2816, vocab_size=4000, max_context=128)
+    m = tinylm.ModelVariants.from_random(cfg, quant.PrecisionSet((4, 3, 2)), seed=21, std=0.02)
+    prompt = list(range(3, 40))
+    sch = StaticScheduler(PrecisionSchedule((4, 3, 2), 4, {4: 0, 3: 4, 2: 12}, 40))
+    a = tinylm.generate(m, prompt, sch, eos_id=-1, max_new=40, record_logits=True)
+    b = tinylm.generate(m, prompt, sch, eos_id=-1, max_new=40, record_logits=True)
+    assert a.output_tokens == b.output_tokens
+    assert a.logits_hashes == b.logits_hashes
+    assert torch.equal(a.logits, b.logits)
+
+
+def test_device_status_word_raises():
+    """A GEMV that reads an out-of-range precision clamps it on device and sets the workspace
+    status word; the host surfaces it as ContractViolation (tinylm.py:214-216 semantics)."""
+    from paper_2410_13461_b200 import _capi
+    from paper_2410_13461_b200.linear import Workspace, gemv, workspace_bytes
+    w = (0.02 * np.random.default_rng(0).standard_normal((256, 128))).astype(np.float32)
+    pk = quant.quantize_tensor(w, 4, 64).packed(_capi.LAYOUT_KN)
+    ws = Workspace(workspace_bytes(pk, 1))
+    x = torch.ones((1, 256), dtype=torch.float16, device="cuda")
+    gemv(pk, x, torch.tensor([4], dtype=torch.int32, device="cuda"), ws)
+    assert ws.status() == 0
+    gemv(pk, x, torch.tensor([7], dtype=torch.int32, device="cuda"), ws)
+    assert ws.status() == _capi.ERR_CONTRACT
+    with pytest.raises(ContractViolation):
+        ws.check()
+    assert ws.status() == 0

@@ -152,42 +152,69 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-# ------------------------------------------------------------------ CPU baselines (oracle port)
+# ------------------------------------------------------------------ CPU baselines
+def cpu_impl():
+    """The reference's own package (pmpd, installed unmodified into baseline/_ref by
+    `pip install --no-index --no-deps --target baseline/_ref <copy of /root/reference/pkg>`) when it
+    is present, else the oracle port pinned to it (tests/test_oracle_golden.py)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "pmpd")):
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        from pmpd import quant as rq
+        return "reference", (lambda w: rq.quantize_tensor(w, 4, 64)), rq.dequantize
+    from oracle import quant as oq
+    return "port", (lambda w: oq.quantize(w, 4, 64)), oq.dequantize
+
+
 def cpu_setup():
     """Untimed inputs of the CPU sample: one quantized 4096x4096 KN matrix per host core."""
     import numpy as np
-    from oracle import quant as oq
 
+    kind, quantize, dequantize = cpu_impl()
     cores = max(1, min(os.cpu_count() or 1, 16))
     rng = np.random.default_rng(0)
     K = N = 4096
-    qts = [oq.quantize((0.02 * rng.standard_normal((K, N))).astype(np.float32), 4, 64) for _ in range(cores)]
-    return qts, rng.standard_normal((1, K)), cores
+    qts = [quantize((0.02 * rng.standard_normal((K, N))).astype(np.float32)) for _ in range(cores)]
+    return qts, rng.standard_normal((1, K)), cores, kind, dequantize
 
 
-def cpu_sample(shape, setup=None):
-    """Reference CPU path (oracle restatement of dequantize + x @ W in float64, quant.py:199-215 +
-    tinylm.py:341) timed on a bounded sample: 4096x4096 KN matrices at p=4/3/2 on all host cores,
-    extrapolated per weight to the whole 7B linear stack and weighted by the schedule."""
+def cpu_sample(shape, setup=None, warm=False):
+    """The reference's CPU path for one linear layer, ModelVariants.weights(name, p) + h @ W
+    (tinylm.py:201-231, 341): cold = dequantize (quant.py:199-215, an LRU miss: at 7B every
+    weights() call misses the 256 MB LRU) + x @ W in float64, timed on a bounded sample of one
+    4096x4096 matrix per host core at p=4/3/2, extrapolated per weight to the whole 7B linear stack
+    and weighted by the schedule; warm (LRU hit) = x @ W alone."""
     from concurrent.futures import ThreadPoolExecutor
-    from oracle import quant as oq
 
-    qts, x, cores = setup if setup is not None else cpu_setup()
+    qts, x, cores, kind, dequantize = setup if setup is not None else cpu_setup()
     K = N = 4096
-    per_p = {}
+    per_p, warm_p = {}, {}
     for p in (4, 3, 2):
         def work(qt):
-            return x @ oq.dequantize(qt, p)
+            return x @ dequantize(qt, p)
         t0 = time.perf_counter()
         with ThreadPoolExecutor(cores) as ex:
             list(ex.map(work, qts))
-        dt = time.perf_counter() - t0
-        rate = cores * K * N / dt  # weights / s
-        per_p[p] = shape.weights_per_token / rate * 1e6  # µs per token
+        per_p[p] = shape.weights_per_token / (cores * K * N / (time.perf_counter() - t0)) * 1e6  # µs per token
+        if warm:
+            with ThreadPoolExecutor(cores) as ex:
+                Ws = list(ex.map(lambda qt: dequantize(qt, p), qts))  # the LRU's content (untimed)
+            t1 = time.perf_counter()
+            with ThreadPoolExecutor(cores) as ex:
+                list(ex.map(lambda W: x @ W, Ws))
+            warm_p[p] = shape.weights_per_token / (cores * K * N / (time.perf_counter() - t1)) * 1e6
+            del Ws
     w = sched_weights()
     us = sum(w[p] * per_p[p] for p in w)
-    return us, cores, per_p, f"{cores} x dequantize+x@W (f64) of 4096x4096 at p=4/3/2 per step, " \
-                             f"extrapolated per weight to {shape.weights_per_token} weights/token, schedule-weighted"
+    sample = (f"{cores} x dequantize + x@W (f64) of 4096x4096 at p=4/3/2 per step through the "
+              f"{'reference package pmpd (baseline/_ref)' if kind == 'reference' else 'oracle port'}, extrapolated "
+              f"per weight to {shape.weights_per_token} weights/token, schedule-weighted")
+    out = {"us": us, "cores": cores, "per_p": per_p, "sample": sample, "kind": kind}
+    if warm:
+        out["warm_per_p"] = warm_p
+        out["warm_us"] = sum(w[p] * warm_p[p] for p in w)
+    return out
 
 
 def arm_config(args, world: int, tp_mode: bool) -> dict:
@@ -200,17 +227,19 @@ def arm_config(args, world: int, tp_mode: bool) -> dict:
 
 
 def run_reference(args, shape):
-    """--impl reference: the reference's CPU algorithm (oracle port) on the box's host cores."""
+    """--impl reference: the reference's CPU path (its own package from baseline/_ref, else the
+    oracle port) on the box's host cores."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    vals, walls, per_p, cores, sample = [], [], {}, 1, ""
+    vals, walls = [], []
     setup = cpu_setup()  # quantization of the sample matrices is not part of a step
+    res = None
     for i in range(args.warmup + args.steps):
         t = time.perf_counter()
-        us, cores, per_p, sample = cpu_sample(shape, setup)
+        res = cpu_sample(shape, setup)
         if i >= args.warmup:
-            vals.append(us)
+            vals.append(res["us"])
             walls.append(time.perf_counter() - t)
     v = statistics.mean(vals)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -220,10 +249,43 @@ def run_reference(args, shape):
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (N(0,0.02^2) weights, seeded)",
         "config": arm_config(args, world, world > 1),
-        "cpu_baseline": {"value": v, "unit": "us/token", "cores": cores, "kind": "port", "sample": sample,
-                         "per_precision_us": per_p},
+        "cpu_baseline": {"value": v, "unit": "us/token", "cores": res["cores"], "kind": res["kind"],
+                         "sample": res["sample"], "per_precision_us": res["per_p"]},
         "e2e": {"value": v, "unit": "us/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def cpu_generate_sample():
+    """The reference's generate path (tinylm.decode_step, tinylm.py:391-400) at the BASELINE config-2
+    width: a 2-layer MobileLLaMA-1.4B-width model (d 2048, ff 5632, vocab 32000) decoding a few tokens
+    warm (dequant LRU large enough) and cold (LRU miss, the default 256 MB budget at full depth); the
+    per-token time is extrapolated to 24 layers (layer part x 12, embed/head once)."""
+    kind = cpu_impl()[0]
+    if kind != "reference":
+        return None
+    import numpy as np
+    from pmpd import quant as rq, tinylm as rt
+    out = {}
+    for L in (1, 3):
+        cfg = rt.ModelConfig(n_layers=L, n_heads=16, d_model=2048, d_ff=5632, vocab_size=32000, max_context=256)
+        rng = np.random.default_rng(1)
+        full = {n: (0.02 * rng.standard_normal(s)).astype(np.float32) for n, s in rt._weight_shapes(cfg)}
+        norms = {n: np.ones(2048, np.float32) for n in rt._norm_names(cfg)}
+        tensors = {n: rq.quantize_tensor(w, 4, 64) for n, w in full.items()}
+        m = rt.ModelVariants(cfg, rq.PrecisionSet((4, 3, 2)), tensors, norms, dequant_budget=8 << 30)
+        lg, cache = rt.prefill(m, 3, list(range(1, 33)))
+        ts = []
+        for i in range(5):
+            t0 = time.perf_counter()
+            lg, cache = rt.decode_step(m, 3, 5 + i, cache)
+            ts.append(time.perf_counter() - t0)
+        out[L] = statistics.median(ts)
+    per_layer = (out[3] - out[1]) / 2
+    rest = out[1] - per_layer
+    return {"s_per_token_warm_24_layers": rest + 24 * per_layer,
+            "measured_s_per_token": {str(k): v for k, v in out.items()},
+            "sample": "reference tinylm.decode_step at p=3 (median of 5), 1- and 3-layer 1.4B-width models with a "
+                      "warm dequant LRU, extrapolated linearly to the 24 layers of BASELINE config 2"}
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -423,9 +485,16 @@ def main():
     if prefill is not None:
         out["prefill"] = prefill
     if rank == 0 and world == 1 and not args.no_cpu:
-        us, cores, cpu_pp, sample = cpu_sample(shape)
-        out["cpu_baseline"] = {"value": us, "unit": "us/token", "cores": cores, "kind": "port", "sample": sample,
-                               "per_precision_us": cpu_pp}
+        res = cpu_sample(shape, warm=True)
+        out["cpu_baseline"] = {"value": res["us"], "unit": "us/token", "cores": res["cores"], "kind": res["kind"],
+                               "sample": res["sample"], "per_precision_us": res["per_p"],
+                               "warm_lru_hit_us": res["warm_us"], "warm_per_precision_us": res["warm_per_p"]}
+        try:
+            gen = cpu_generate_sample()
+            if gen is not None:
+                out["cpu_baseline"]["config2_generate"] = gen
+        except Exception as exc:  # a reported baseline only: never fail the bench on it
+            out["cpu_baseline"]["config2_generate"] = {"error": repr(exc)}
     if rank == 0 and world == 1 and not args.no_model:
         # BASELINE config 2 end to end: full decoder (RMSNorm, RoPE, attention over the KV cache,
         # SwiGLU, head, greedy argmax), one persistent-engine launch per decode token

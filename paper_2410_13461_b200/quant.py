@@ -345,3 +345,101 @@ def parse_model(data: bytes):
     if off != len(data):
         raise FormatError(f"{len(data) - off} trailing bytes after last tensor at offset {off}")
     return tensors, meta
+
+
+# ---------------------------------------------------------------------------
+# streaming PMPD v1 file I/O: one tensor on the host at a time
+# ---------------------------------------------------------------------------
+
+def write_model(path, tensors: dict, meta: dict) -> int:
+    """``serialize_model`` (quant.py:237-261) written tensor by tensor to ``path``: the same bytes,
+    with at most one tensor's planes and scales on the host.  Returns the file size."""
+    if not tensors:
+        raise InputError("no tensors to serialize")
+    pms = {t.p_max for t in tensors.values()}
+    if len(pms) != 1:
+        raise InputError(f"tensors disagree on p_max: {sorted(pms)}")
+    gss = {t.group_size for t in tensors.values()}
+    if len(gss) != 1:
+        raise InputError(f"tensors disagree on group_size: {sorted(gss)}")
+    head = dict(meta)
+    head["p_max"], head["group_size"] = pms.pop(), gss.pop()
+    head["tensors"] = [{"name": n, "rows": t.rows, "cols": t.cols} for n, t in tensors.items()]
+    blob = json.dumps(head, sort_keys=True, separators=(",", ":")).encode("utf-8")
+    with open(path, "wb") as fh:
+        fh.write(MAGIC + struct.pack("<II", FORMAT_VERSION, len(blob)) + blob)
+        for t in tensors.values():
+            fh.write(_host(t.mins).astype("<f4").tobytes())
+            fh.write(_host(t.deltas).astype("<f4").tobytes())
+            if t.store.planes.numel() == 0:
+                raise InputError("tensor's reference-layout planes were dropped (drop_reference_copy)")
+            fh.write(_host(t.store.planes).tobytes())
+        return fh.tell()
+
+
+def read_model(path, on_tensor=None):
+    """``parse_model`` (quant.py:264-318) streamed from ``path`` straight into HBM, same validation
+    and messages: each tensor's scales and planes are read into one reusable pinned host buffer
+    and copied to the device, so the host holds at most one tensor (``on_tensor(name, qt)`` may
+    consume and drop each tensor, e.g. after packing it)."""
+    with open(path, "rb") as fh:
+        size = fh.seek(0, 2)
+        fh.seek(0)
+        head = fh.read(12)
+        if len(head) < 4 or head[:4] != MAGIC:
+            raise FormatError(f"bad magic {head[:4]!r} at offset 0 (expected {MAGIC!r})")
+        if len(head) < 12:
+            raise FormatError(f"truncated header: {len(head)} bytes")
+        (version,) = struct.unpack_from("<I", head, 4)
+        if version != FORMAT_VERSION:
+            raise FormatError(f"unsupported format version {version} at offset 4")
+        (meta_len,) = struct.unpack_from("<I", head, 8)
+        off = 12
+        if off + meta_len > size:
+            raise FormatError(f"truncated metadata: need {meta_len} bytes at offset {off}")
+        try:
+            meta = json.loads(fh.read(meta_len).decode("utf-8"))
+        except (UnicodeDecodeError, json.JSONDecodeError) as exc:
+            raise FormatError(f"metadata is not valid JSON at offset {off}: {exc}") from exc
+        off += meta_len
+        for key in ("p_max", "group_size", "tensors"):
+            if key not in meta:
+                raise FormatError(f"metadata is missing required key '{key}'")
+        p_max, group_size = int(meta["p_max"]), int(meta["group_size"])
+        entries = []
+        for entry in meta["tensors"]:
+            try:
+                entries.append((entry["name"], int(entry["rows"]), int(entry["cols"])))
+            except (KeyError, TypeError, ValueError) as exc:
+                raise FormatError(f"malformed tensor entry {entry!r} in metadata: {exc}") from exc
+        biggest = max([2 * r * _groups_per_row(c, group_size) * 4 + p_max * _plane_bytes(r, c)
+                       for _, r, c in entries] + [1])
+        stage = torch.empty(biggest, dtype=torch.uint8, pin_memory=torch.cuda.is_available())
+        view = memoryview(stage.numpy())
+        dev = _device()
+        tensors = {}
+        for name, rows, cols in entries:
+            gpr = _groups_per_row(cols, group_size)
+            sb, pb = rows * gpr * 4, _plane_bytes(rows, cols)
+            parts = [(sb, "group mins"), (sb, "group steps")] + [(pb, f"plane {k}") for k in range(p_max)]
+            pos = 0
+            for nbytes, what in parts:
+                if off + nbytes > size:
+                    raise FormatError(f"truncated reading {what} of tensor '{name}' at offset {off}")
+                got = fh.readinto(view[pos:pos + nbytes])
+                if got != nbytes:
+                    raise FormatError(f"truncated reading {what} of tensor '{name}' at offset {off}")
+                off += nbytes
+                pos += nbytes
+            d = stage[:pos].to(dev, non_blocking=True)
+            mins = d[:sb].view(torch.float32).reshape(rows, gpr).clone()
+            deltas = d[sb:2 * sb].view(torch.float32).reshape(rows, gpr).clone()
+            planes = d[2 * sb:].reshape(p_max, pb).clone()
+            torch.cuda.current_stream().synchronize()  # the staging buffer is reused next
+            qt = QuantizedTensor(rows, cols, group_size, p_max, mins, deltas, BitPlaneStore(rows, cols, p_max, planes))
+            if on_tensor is not None:
+                qt = on_tensor(name, qt)
+            tensors[name] = qt
+        if off != size:
+            raise FormatError(f"{size - off} trailing bytes after last tensor at offset {off}")
+    return tensors, meta

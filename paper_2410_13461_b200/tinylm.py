@@ -25,7 +25,6 @@ import math
 import os
 import threading
 from dataclasses import dataclass
-from pathlib import Path
 from typing import Sequence
 
 import numpy as np
@@ -34,8 +33,8 @@ import torch
 from . import _capi
 from .errors import ConfigError, ContractViolation, FormatError, InputError
 from .linear import Workspace, gemm, gemv, gemv_fused, raise_device_status, workspace_bytes
-from .quant import BitPlaneStore, PrecisionSet, QuantizedTensor, dequantize, parse_model, quantize_tensor, \
-    serialize_model
+from .quant import BitPlaneStore, PrecisionSet, QuantizedTensor, dequantize, quantize_tensor, read_model, \
+    write_model
 from .schedule import PrecisionSchedule
 from .util import named_rng
 
@@ -110,6 +109,36 @@ def random_weights(cfg: ModelConfig, seed: int, std: float | None = None):
     return weights, norms
 
 
+class SeededFullWeights:
+    """Precision-16 originals of a model saved with its init seed (tinylm.py:244-257 regenerates
+    them with ``random_weights``), produced lazily on first use, tensor by tensor in the reference's
+    RNG order and kept on the device: the host never holds more than one f32 tensor."""
+
+    def __init__(self, config: ModelConfig, seed: int, std: float | None = None):
+        self.config, self.seed, self.std = config, int(seed), std
+        self._dev = None
+        self._lock = threading.Lock()
+
+    def _materialize(self) -> dict:
+        with self._lock:
+            if self._dev is None:
+                rng = named_rng(self.seed, "weights")
+                scale = 1.0 / math.sqrt(self.config.d_model) if self.std is None else float(self.std)
+                dev = {}
+                for name, shape in _weight_shapes(self.config):
+                    w = rng.normal(0.0, scale, shape).astype(np.float32)
+                    dev[name] = torch.from_numpy(w).to("cuda")
+                    del w
+                self._dev = dev
+            return self._dev
+
+    def __getitem__(self, name):
+        return self._materialize()[name]
+
+    def items(self):
+        return self._materialize().items()
+
+
 def _concat_cols(parts: list) -> QuantizedTensor:
     """Column-concatenate quantized matrices whose group boundaries align (e.g. wq|wk|wv)."""
     codes = torch.cat([t.codes for t in parts], dim=1).contiguous()
@@ -152,7 +181,7 @@ class _DeviceWeights:
         self.fp16 = None
         self._kp = (-(-cfg.d_model // 64) * 64, -(-cfg.d_ff // 64) * 64)
         if mv.full_weights is not None:
-            self.fp16 = {n: torch.tensor(w, device="cuda").half() for n, w in mv.full_weights.items()}
+            self.fp16 = {n: torch.as_tensor(w, device="cuda").half() for n, w in mv.full_weights.items()}
             # fused q|k|v weight of the fp16 baseline, concatenated once (not per call)
             for i in range(cfg.n_layers):
                 names = [f"layers.{i}.{nm}" for nm in ("wq", "wk", "wv")]
@@ -218,21 +247,24 @@ class ModelVariants:
             if self.full_weights is None:
                 raise ConfigError("full-precision weights unavailable: model was loaded without "
                                   "an init seed and cannot serve precision 16")
-            return torch.tensor(self.full_weights[name], device="cuda")
+            return torch.as_tensor(self.full_weights[name], device="cuda").clone()
         if p not in self.precisions:
             raise ContractViolation(f"precision {p} not in declared set {list(self.precisions)}")
         return dequantize(self.tensors[name], p)
 
     def save(self, path) -> None:
+        """tinylm.py:233-241: the PMPD v1 file, written tensor by tensor (quant.write_model)."""
         meta = {"config": self.config.to_json(), "precisions": list(self.precisions.precisions),
                 "norms": {k: [float(x) for x in v] for k, v in self.norms.items()}}
         if self.init_info is not None:
             meta["init"] = self.init_info
-        Path(path).write_bytes(serialize_model(self.tensors, meta))
+        write_model(path, self.tensors, meta)
 
     @classmethod
     def load(cls, path, dequant_budget: int = 256 << 20) -> "ModelVariants":
-        tensors, meta = parse_model(Path(path).read_bytes())
+        """tinylm.py:243-257: the file is streamed tensor by tensor into HBM (quant.read_model);
+        precision-16 originals of a seeded model are regenerated lazily, on the device."""
+        tensors, meta = read_model(path)
         try:
             config = ModelConfig(**meta["config"])
             precisions = PrecisionSet(tuple(meta["precisions"]))
@@ -242,7 +274,7 @@ class ModelVariants:
         full = None
         init = meta.get("init")
         if init is not None and init.get("scheme") == INIT_SCHEME:
-            full, _ = random_weights(config, int(init["seed"]))
+            full = SeededFullWeights(config, int(init["seed"]))
         return cls(config, precisions, tensors, norms, full_weights=full, init_info=init,
                    dequant_budget=dequant_budget)
 

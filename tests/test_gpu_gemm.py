@@ -72,3 +72,37 @@ def test_gemm_split_k(split, K, N, M, monkeypatch):
     assert torch.all(big[:, N:] == 7.0)  # the zeroing before the split-K adds stays inside y
     gemm(pk, x, _pdev(3), out=y, alpha=0.75, accumulate=True)
     assert rel_l2(y.cpu().numpy(), 2 * ref.cpu().numpy()) < 1e-4
+
+
+def test_gemm_split_k_is_bit_reproducible():
+    """Split-K partials are added in split order (a per-tile turn counter), not by atomics: the
+    same input gives bit-identical outputs every launch, with and without accumulation."""
+    import os
+    from paper_2410_13461_b200 import _capi, quant
+    from paper_2410_13461_b200.linear import gemm
+    w = torch.randn(4096, 1024, device="cuda") * 0.02
+    pk = quant.quantize_tensor(w, 4, 64).packed(_capi.LAYOUT_KN)
+    x = torch.randn(512, 4096, device="cuda").half()
+    pd = torch.tensor([4], dtype=torch.int32, device="cuda")
+    old = os.environ.get("PMPD_GEMM_SPLITK")
+    os.environ["PMPD_GEMM_SPLITK"] = "4"
+    try:
+        outs = [gemm(pk, x, pd, out=torch.empty(512, 1024, device="cuda")) for _ in range(4)]
+        base = torch.randn(512, 1024, device="cuda")
+        accs = []
+        for _ in range(3):
+            y = base.clone()
+            gemm(pk, x, pd, out=y, accumulate=True)
+            accs.append(y)
+    finally:
+        if old is None:
+            os.environ.pop("PMPD_GEMM_SPLITK")
+        else:
+            os.environ["PMPD_GEMM_SPLITK"] = old
+    ref = (x.float() @ quant.dequantize(quant.quantize_tensor(w, 4, 64), 4, layout=_capi.LAYOUT_KN))
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+    for a in accs[1:]:
+        assert torch.equal(a, accs[0])
+    assert float((outs[0] - ref).norm() / ref.norm()) < 2e-3
+    assert float((accs[0] - base - ref).norm() / ref.norm()) < 2e-3

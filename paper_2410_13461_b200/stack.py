@@ -236,6 +236,7 @@ class TPLinearStack:
         self.ws.ensure(workspace_bytes(self.head, m))
         hq = P.o_rows.size
         self.x16 = torch.randn((m, d), device="cuda", generator=gen).half()
+        self.y32 = torch.zeros((m, d), device="cuda", dtype=torch.float32)  # row-parallel partial sums
         self.qkv = torch.empty((m, 3 * hq), device="cuda", dtype=torch.float16)
         self.u = torch.empty((m, 2 * P.ff.size), device="cuda", dtype=torch.float16)
         self.logits_loc = torch.zeros((m, max(self.head_sizes)), device="cuda", dtype=torch.float32)
@@ -261,13 +262,15 @@ class TPLinearStack:
         ffl = self.plan.ff.size
         for wqkv, wo, wup, wdn in self.layers:
             gemv(wqkv, self.x16, self.p_dev, self.ws, out=self.qkv, alpha=a_d)
-            # row-parallel partial sums land in f16 in x16 and are all-reduced in place: the next
-            # GEMV reads the reduced vector directly (no f32 buffer, no conversion launch)
-            gemv(wo, self.qkv[:, 2 * hq:], self.p_dev, self.ws, out=self.x16, alpha=a_d)   # row-parallel
-            dist.all_reduce(self.x16, group=self.group)
+            # row-parallel partial sums are all-reduced in f32 (the residual path keeps full
+            # precision across ranks), then rounded once to the next GEMV's f16 input
+            gemv(wo, self.qkv[:, 2 * hq:], self.p_dev, self.ws, out=self.y32, alpha=a_d)   # row-parallel
+            dist.all_reduce(self.y32, group=self.group)
+            self.x16.copy_(self.y32)
             gemv(wup, self.x16, self.p_dev, self.ws, out=self.u, alpha=a_d)               # column-parallel
-            gemv(wdn, self.u[:, :ffl], self.p_dev, self.ws, out=self.x16, alpha=a_f)      # row-parallel
-            dist.all_reduce(self.x16, group=self.group)
+            gemv(wdn, self.u[:, :ffl], self.p_dev, self.ws, out=self.y32, alpha=a_f)      # row-parallel
+            dist.all_reduce(self.y32, group=self.group)
+            self.x16.copy_(self.y32)
         hs = self.head_cols.size
         gemv(self.head, self.x16, self.p_dev, self.ws, out=self.logits_loc[:, :hs], alpha=a_d)
         dist.all_gather_into_tensor(self.logits_all, self.logits_loc, group=self.group)

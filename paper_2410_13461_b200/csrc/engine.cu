@@ -567,26 +567,45 @@ __noinline__ __device__ float stage_attn_input(const EngineOp& op, const EngineO
   const int dh = src.d_head;
   const unsigned long long* recs = src.acc + (long long)par * src.acc_len;
   float av[SBA * E_ASPLIT][4];
+  // batches 0 and 1 (the first 3072 elements of the k-range, all an o op of d <= 3072 needs) in
+  // ONE round trip, batch 2 in a second one only when the range is wider
 #pragma unroll
-  for (int bi = 0; bi < SBA; ++bi) {  // one round trip per batch of 4 elements x E_ASPLIT splits
-    const int u = 4 * threadIdx.x + bi * 4 * E_NCW * 32;
-    const int k = u < lr ? kof(u) : op.k_real;
-    const int hh = k < op.k_real ? k / dh : 0, e = k - hh * dh;
-    const unsigned long long* pp[E_ASPLIT];
-    bool on[E_ASPLIT];
-    int ww[E_ASPLIT];
-    float o[E_ASPLIT][4];
+  for (int half = 0; half < 2; ++half) {
+    constexpr int NBH = 2 * E_ASPLIT;
+    const unsigned long long* pp[NBH];
+    bool on[NBH];
+    int ww[NBH];
+    float o[NBH][4];
+    bool any = false;
 #pragma unroll
-    for (int q = 0; q < E_ASPLIT; ++q) {
-      pp[q] = recs + (int64_t)(hh * E_ASPLIT + q) * attn_rec(dh) + 4 + e;
-      on[q] = k < op.k_real;
-      ww[q] = 1;
+    for (int b = 0; b < 2; ++b) {
+      const int bi = 2 * half + b;
+      const int u = 4 * threadIdx.x + bi * 4 * E_NCW * 32;
+      const int k = (bi < SBA && u < lr) ? kof(u) : op.k_real;
+      const int hh = k < op.k_real ? k / dh : 0, e = k - hh * dh;
+#pragma unroll
+      for (int q = 0; q < E_ASPLIT; ++q) {
+        pp[b * E_ASPLIT + q] = recs + (int64_t)(hh * E_ASPLIT + q) * attn_rec(dh) + 4 + e;
+        on[b * E_ASPLIT + q] = k < op.k_real;
+        ww[b * E_ASPLIT + q] = 1;
+      }
+      any = any || k < op.k_real;
     }
-    if (u < lr) counted_read4<E_ASPLIT, true>(pp, on, ww, o);
+    if (half == 1 && !any) {
 #pragma unroll
-    for (int q = 0; q < E_ASPLIT; ++q)
+      for (int i = 0; i < NBH; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    } else {
+      counted_read4<NBH, true>(pp, on, ww, o);
+    }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) av[bi * E_ASPLIT + q][i] = u < lr ? o[q][i] : 0.f;
+    for (int b = 0; b < 2; ++b) {
+      const int bi = 2 * half + b;
+      if (bi >= SBA) break;
+#pragma unroll
+      for (int q = 0; q < E_ASPLIT; ++q)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) av[bi * E_ASPLIT + q][i] = o[b * E_ASPLIT + q][i];
+    }
   }
   float* wts = wscratch;
   for (int hh = threadIdx.x; hh < src.n_heads; hh += E_NCW * 32) {
@@ -1045,7 +1064,12 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
 #else
     if (lane == 0) {
 #endif
+#ifdef PMPD_ENGINE_EVICT_NORMAL
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+#else
       const uint64_t pol = policy_evict_first();
+#endif
       int slot = 0, used = 0;
       uint32_t phase = 0;
       for (int oi = 1; oi < PMPD_ENGINE_PF && oi < a.n_ops; ++oi) prefetch_op(a.ops[oi], c, G, p);
@@ -1060,7 +1084,11 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
         while (t < r.T1) {
           const int end = min(min(t + E_STILES, r.T1), t - kt + r.KT);
           const int cnt = end - t;
+#ifdef PMPD_ENGINE_PROD_SPIN
+          if (used) mbar_wait(&bars.empty[slot], phase ^ 1u);
+#else
           if (used) mbar_wait_backoff(&bars.empty[slot], phase ^ 1u);
+#endif
           uint8_t* st = smem + kSmRing + slot * stage_bytes;
           mbar_arrive_expect_tx(&bars.full[slot], (uint32_t)(cnt * kTilePlaneBytes * (p + 1)));
           for (int j = 0; j < p; ++j)

@@ -35,9 +35,17 @@ kinds = ["qkv", "attn", "o", "up", "down"]
 for k, nm in enumerate(kinds):
     idx = [i for i in range(n_ops - 1) if i % 5 == k]
     if nm == "attn":
-        # attention ops: no CTA timestamps; op time = publish(prev... next op ticket) - publish(prev op)
-        d = [np.nanmedian(t[:, i + 1, 0]) - pub[i - 1] for i in idx]
-        print(f"  {nm:5s} prev-publish -> next-op ticket (attention + 2 syncs): {np.mean(d):6.2f} us")
+        # attention ops stamp [0] unit start and [2] units done on the CTAs that hold units
+        st0 = [np.nanmedian(t[:, i, 0]) - pub[i - 1] for i in idx]
+        dur = [np.nanmax(t[:, i, 2]) - np.nanmedian(t[:, i, 0]) for i in idx]
+        o_st = [np.nanmedian(t[:, i + 1, 1]) - np.nanmax(t[:, i, 2]) for i in idx]
+        qin = [np.nanmedian(t[:, i, 1] - t[:, i, 0]) for i in idx]
+        lp = [np.nanmedian(t[:, i, 3] - t[:, i, 1]) for i in idx]
+        cmb = [np.nanmedian(t[:, i, 2] - t[:, i, 3]) for i in idx]
+        print(f"  {nm:5s} qkv publish -> unit start {np.mean(st0):5.2f}, start -> last unit done {np.mean(dur):5.2f}, "
+              f"last unit -> o staged (median) {np.mean(o_st):5.2f} us")
+        print(f"        per unit (median): start -> q ready {np.mean(qin):5.2f}, rows loop {np.mean(lp):5.2f}, "
+              f"combine + records {np.mean(cmb):5.2f} us")
         continue
     tk = [np.nanmedian(t[:, i, 0]) - (pub[i - 1] if i > 0 else 0) for i in idx if i > 0]
     st = [np.nanmedian(t[:, i, 1] - t[:, i, 0]) for i in idx]

@@ -494,6 +494,9 @@ PMPD_DEV void read_qkv3(const EngineOp& src, const unsigned long long* base, int
 #ifndef PMPD_ATTN_NOLOAD
 #define PMPD_ATTN_NOLOAD 0
 #endif
+#ifndef PMPD_ATTN_DB
+#define PMPD_ATTN_DB 0  // 1: two row batches in flight per warp
+#endif
 template <int DPL>
 PMPD_DEV void attn_unit(const EngineOp& op, const EngineOp& src, int h, int s, int L, float* scratch, int warp,
                         int lane, int par, float* newrow, long long* tr) {
@@ -518,6 +521,9 @@ PMPD_DEV void attn_unit(const EngineOp& op, const EngineOp& src, int h, int s, i
   // K/V rows of the next batch as packed f16 (issued before the q wait: independent of this token;
   // in the loop each batch is converted, then the following one is issued while it is used)
   RawRow<DPL> kc[U], vc[U];
+#if PMPD_ATTN_DB
+  RawRow<DPL> kn[U], vn[U];  // a second batch in flight
+#endif
   const int tb0 = t0 + warp;
 #pragma unroll
   for (int u = 0; u < U; ++u) {
@@ -525,6 +531,12 @@ PMPD_DEV void attn_unit(const EngineOp& op, const EngineOp& src, int h, int s, i
     const bool ok = !PMPD_ATTN_NOLOAD && t < t1 && !(append && t == pos);
     ld_raw<DPL>(kb + (int64_t)t * d, ok, kc[u]);
     ld_raw<DPL>(vb + (int64_t)t * d, ok, vc[u]);
+#if PMPD_ATTN_DB
+    const int t2 = t + U * E_NCW;
+    const bool ok2 = !PMPD_ATTN_NOLOAD && t2 < t1 && !(append && t2 == pos);
+    ld_raw<DPL>(kb + (int64_t)t2 * d, ok2, kn[u]);
+    ld_raw<DPL>(vb + (int64_t)t2 * d, ok2, vn[u]);
+#endif
   }
   // ---- q (and the new k, v) of this token: counted words of the q|k|v op (blocks until complete)
   const unsigned long long* qkv = src.acc + (long long)par * src.acc_len;
@@ -565,6 +577,28 @@ PMPD_DEV void attn_unit(const EngineOp& op, const EngineOp& src, int h, int s, i
   if (app) {  // the first batch skipped row `pos`: take it from shared memory
 #pragma unroll
     for (int u = 0; u < U; ++u) {
+#if PMPD_ATTN_DB
+      if (tb0 + (U + u) * E_NCW == pos) {  // (second batch: the converted row goes there)
+        float kf1[DPL], vf1[DPL];
+#pragma unroll
+        for (int j = 0; j < DPL; ++j) {
+          kf1[j] = newrow[lane * DPL + j];
+          vf1[j] = newrow[DH + lane * DPL + j];
+        }
+        if constexpr (DPL == 1) {
+          kn[u].w[0] = (uint32_t)__half_as_ushort(__float2half(kf1[0]));
+          vn[u].w[0] = (uint32_t)__half_as_ushort(__float2half(vf1[0]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < DPL / 2; ++i) {
+            const __half2 k2 = __floats2half2_rn(kf1[2 * i], kf1[2 * i + 1]);
+            const __half2 v2 = __floats2half2_rn(vf1[2 * i], vf1[2 * i + 1]);
+            kn[u].w[i] = *reinterpret_cast<const uint32_t*>(&k2);
+            vn[u].w[i] = *reinterpret_cast<const uint32_t*>(&v2);
+          }
+        }
+      }
+#endif
       if (tb0 + u * E_NCW == pos) {
         float kf1[DPL], vf1[DPL];
 #pragma unroll
@@ -599,13 +633,23 @@ PMPD_DEV void attn_unit(const EngineOp& op, const EngineOp& src, int h, int s, i
     for (int u = 0; u < U; ++u) {
       raw_to_f<DPL>(kc[u], kf[u]);
       raw_to_f<DPL>(vc[u], vf[u]);
+#if PMPD_ATTN_DB
+      kc[u] = kn[u];
+      vc[u] = vn[u];
+#endif
     }
-    if (tb + E_NCW * U < t1) {  // the next batch is in flight while this one is used
+    constexpr int AHEAD = PMPD_ATTN_DB ? 2 : 1;  // batches in flight
+    if (tb + AHEAD * E_NCW * U < t1) {  // the next batch(es) in flight while this one is used
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int t = tb + (U + u) * E_NCW;
+        const int t = tb + (AHEAD * U + u) * E_NCW;
+#if PMPD_ATTN_DB
+        ld_raw<DPL>(kb + (int64_t)t * d, !PMPD_ATTN_NOLOAD && t < t1, kn[u]);
+        ld_raw<DPL>(vb + (int64_t)t * d, !PMPD_ATTN_NOLOAD && t < t1, vn[u]);
+#else
         ld_raw<DPL>(kb + (int64_t)t * d, !PMPD_ATTN_NOLOAD && t < t1, kc[u]);
         ld_raw<DPL>(vb + (int64_t)t * d, !PMPD_ATTN_NOLOAD && t < t1, vc[u]);
+#endif
       }
     }
     float sc[U];

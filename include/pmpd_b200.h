@@ -223,6 +223,8 @@ int pmpd_engine_attn_records(int32_t n_heads, int32_t d_head);
  * minimise the largest per-CTA cost of stage calls and n-group flushes instead of splitting the tiles
  * evenly; attach the uploaded array with pmpd_engine_op_set_bounds (null = even split). */
 int pmpd_engine_partition(const pmpd_qtensor* t, int32_t* bounds_host);
+/* The same over G CTAs (a rank's share of the grid in pmpd_engine_run_ranks). */
+int pmpd_engine_partition_g(const pmpd_qtensor* t, int32_t G, int32_t* bounds_host);
 int pmpd_engine_op_set_bounds(void* op_host, const int32_t* bounds_dev);
 /* Counted accumulation (linear-stack programs run by pmpd_engine_run): the op's output is
  * acc_dev = u64 [2][n_tiles * 64] zero-initialised words, each holding [63:56] the number of CTAs
@@ -244,6 +246,15 @@ int pmpd_engine_run_decoder(const void* ops_dev, int32_t n_ops, const int32_t* p
                             void* resid_dev, int64_t resid_len, int32_t d_real, float* y_out_dev, float y_alpha,
                             uint32_t* bar_dev, int32_t* status_dev, int64_t* trace_dev, void* stream);
 
+/* Tensor-parallel linear stack, all ranks emulated in ONE launch (one GPU): ops_dev holds n_ranks
+ * op tables of n_ops records (rank r = its column / row shards, partitioned with
+ * pmpd_engine_partition_g over pmpd_engine_grid() / n_ranks CTAs); the grid is split into n_ranks
+ * groups, group r runs table r and writes y_out + r * y_stride.  A row-parallel op's counted output
+ * is one vector shared by every rank's op record, with contributor counts summed over the ranks:
+ * the cross-rank all-reduce is the counted addition itself (no collective call). */
+int pmpd_engine_run_ranks(const void* ops_dev, int32_t n_ops, int32_t n_ranks, const int32_t* p_dev,
+                          const void* x_in_dev, float* y_out_dev, int32_t y_stride, float y_alpha, uint32_t* bar_dev,
+                          int32_t* status_dev, void* stream);
 int pmpd_engine_run(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const void* x_in_dev, float* y_out_dev,
                     float y_alpha, uint32_t* bar_dev, int32_t* status_dev, void* stream);
 /* Same, recording a per-CTA per-op timeline (globaltimer ns):

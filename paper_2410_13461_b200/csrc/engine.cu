@@ -233,6 +233,8 @@ struct EngineArgs {
                        // [3 + i]: op i's hint counter, [3 + n_ops + i]: readers of RMSNorm op i
   int* status;
   long long* trace;    // optional timeline [G][n_ops][4] (globaltimer ns), null = off
+  int n_ranks;         // tensor-parallel emulation: op tables [n_ranks][n_ops], y_out [n_ranks][y_stride]
+  int y_stride;
   // decoder programs: the counted residual stream [2][R_len] and its f32 starting value x0
   // (the embedding row), added in by CTA c for its slice at launch start
   unsigned long long* R;
@@ -1220,11 +1222,23 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
 // DEC: the decoder-step op kinds (attention, RMSNorm / attention-combine inputs, residual outputs);
 // the linear-stack program runs the instantiation without them (no extra registers on its path).
 template <bool DEC>
-__global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a) {
+__global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a_in) {
   extern __shared__ __align__(128) uint8_t smem[];
   Bars& bars = *reinterpret_cast<Bars*>(smem + kSmBar);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int G = gridDim.x, c = blockIdx.x;
+  // Tensor-parallel emulation (n_ranks > 1, linear-stack programs): the grid is split into
+  // n_ranks groups of G CTAs; group r runs rank r's op table (its shards) and writes rank r's
+  // slice of y_out.  Row-parallel outputs are counted vectors shared by all ranks, their counts
+  // summing every rank's contributors: the cross-rank reduction is the same counted addition as
+  // the split-K one (the multi-GPU form adds into every rank's copy over NVLink).
+  const int nr = DEC ? 1 : a_in.n_ranks;  // decoder programs: one rank
+  const int G = gridDim.x / nr, rank = blockIdx.x / G, c = blockIdx.x - rank * G;
+  const bool idle = rank >= nr;  // grid remainder when n_ranks does not divide it
+  EngineArgs a = a_in;
+  if constexpr (!DEC) {
+    a.ops += (idle ? 0 : rank) * a.n_ops;
+    a.y_out += (idle ? 0 : rank) * (long long)a.y_stride;
+  }
   int p = *a.p_dev;
   if (p < 1 || p > 4) {
     if (threadIdx.x == 0 && c == 0) atomicExch(a.status, PMPD_ERR_CONTRACT);
@@ -1250,7 +1264,9 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
   }
   __syncthreads();
 
-  if (warp == E_PROD) {
+  if (idle) {
+    // no work: only the launch's done counter below
+  } else if (warp == E_PROD) {
     // ------------------------------------------------------------ producer
 #ifdef PMPD_ENGINE_SKIP_MEMORY
     if (false) {
@@ -1413,7 +1429,7 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
       wait_hint(a.bar + 3 + a.n_ops - 1, (epoch + 1u) * (unsigned)last.n_contrib);
     __syncthreads();
     const unsigned long long* la = last.acc + (long long)par * last.acc_len;
-    for (int ng = c; ng < last.n_tiles; ng += G) {
+    for (int ng = c; !idle && ng < last.n_tiles; ng += G) {
       const int want = __ldg(last.nslots + ng);
       for (int nl = threadIdx.x; nl < 64; nl += blockDim.x) {
         const int n = ng * 64 + nl;
@@ -1428,7 +1444,7 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0 && atomicAdd(a.bar + 1, 1u) == (unsigned)(G - 1)) {
+    if (threadIdx.x == 0 && atomicAdd(a.bar + 1, 1u) == gridDim.x - 1) {
       a.bar[1] = 0;
       a.bar[2] = epoch + 1u;  // read by the next launch (kernel boundary orders it)
     }
@@ -1562,8 +1578,13 @@ int pmpd_engine_attn_records(int32_t n_heads, int32_t d_head) { return n_heads *
 // flush (~0.5 tile-time).  An even split of the tiles gives some CTAs an extra stage or segment
 // (e.g. 3 stage calls instead of 2 for o on 148 SMs).  Binary search on the budget, greedy cover.
 int pmpd_engine_partition(const pmpd_qtensor* t, int32_t* bounds_host) {
+  return pmpd_engine_partition_g(t, num_sms(), bounds_host);
+}
+
+int pmpd_engine_partition_g(const pmpd_qtensor* t, int32_t G, int32_t* bounds_host) {
   if (!t || !bounds_host) return fail(PMPD_ERR_CONFIG, "null argument");
-  const int G = num_sms(), KT = t->k_tiles, NT = t->n_tiles * t->k_tiles;
+  if (G < 1) return fail(PMPD_ERR_CONFIG, "partition over %d CTAs", G);
+  const int KT = t->k_tiles, NT = t->n_tiles * t->k_tiles;
   if (NT < 1) return fail(PMPD_ERR_CONFIG, "empty tensor");
   // cost in half tile-times
   static const int flush_cost = [] {  // half tile-times per n-group segment (PMPD_ENGINE_PART_FLUSH)
@@ -1665,7 +1686,7 @@ int pmpd_engine_run(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, co
 namespace {
 int engine_launch(bool dec, const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const void* x_in, float* y_out,
                   float y_alpha, uint32_t* bar_dev, int32_t* status_dev, int64_t* trace_dev, void* stream,
-                  void* R = nullptr, long long R_len = 0, int d_real = 0) {
+                  void* R = nullptr, long long R_len = 0, int d_real = 0, int n_ranks = 1, int y_stride = 0) {
   if (n_ops < 1) return fail(PMPD_ERR_CONFIG, "engine program is empty");
   EngineArgs a;
   a.ops = static_cast<const EngineOp*>(ops_dev);
@@ -1681,7 +1702,11 @@ int engine_launch(bool dec, const void* ops_dev, int32_t n_ops, const int32_t* p
   a.R_len = R_len;
   a.x0 = dec ? static_cast<const float*>(x_in) : nullptr;
   a.d_real = d_real;
+  a.n_ranks = n_ranks;
+  a.y_stride = y_stride;
   if (dec && (!R || !x_in || R_len < d_real || (R_len & 63))) return fail(PMPD_ERR_CONFIG, "decoder residual stream");
+  if (n_ranks < 1 || n_ranks > 8 || (n_ranks > 1 && (dec || trace_dev)))
+    return fail(PMPD_ERR_CONFIG, "rank emulation: 1..8 ranks, linear-stack programs, no trace");
   static int smem = 0;
   if (smem == 0) {
     int dev = 0, optin = 0;
@@ -1714,6 +1739,13 @@ extern "C" {
 int pmpd_engine_run_traced(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const void* x_in, float* y_out,
                            float y_alpha, uint32_t* bar_dev, int32_t* status_dev, int64_t* trace_dev, void* stream) {
   return engine_launch(false, ops_dev, n_ops, p_dev, x_in, y_out, y_alpha, bar_dev, status_dev, trace_dev, stream);
+}
+
+int pmpd_engine_run_ranks(const void* ops_dev, int32_t n_ops, int32_t n_ranks, const int32_t* p_dev, const void* x_in,
+                          float* y_out, int32_t y_stride, float y_alpha, uint32_t* bar_dev, int32_t* status_dev,
+                          void* stream) {
+  return engine_launch(false, ops_dev, n_ops, p_dev, x_in, y_out, y_alpha, bar_dev, status_dev, nullptr, stream,
+                       nullptr, 0, 0, n_ranks, y_stride);
 }
 
 int pmpd_engine_run_decoder(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const float* x0_dev,

@@ -57,7 +57,7 @@ class OpSpec:
     resid: torch.Tensor | None = None
     gain: torch.Tensor | None = None
     eps: float = 1e-6
-    out: torch.Tensor | None = None
+    out: torch.Tensor | str | None = None  # decoder: residual op; RankProgram: shared (all-reduced) output key
     out_alpha: float = 1.0
     attn: AttnSpec | None = None
 
@@ -209,3 +209,97 @@ class Program:
         """Enqueue one pass (graph-capturable): y_out = y_alpha * chain(x_in) at precision *p_dev
         (decoder programs: x_in = the f32 embedding row that starts the residual stream)."""
         self._launch(x_in, p_dev, y_out, None)
+
+
+class RankProgram:
+    """Tensor-parallel linear-stack program: ``rank_ops[r]`` is rank r's op chain (its Megatron
+    shards, the same op sequence on every rank).  An op whose ``OpSpec.out`` is set to a string key
+    is row-parallel: every rank's op with that key adds into ONE counted vector whose contributor
+    counts sum the ranks' partitions, so the cross-rank all-reduce is the engine's own counted
+    addition (deterministic, no collective call).  On one GPU all ranks run in one launch
+    (``pmpd_engine_run_ranks``, the grid split into ``len(rank_ops)`` groups); on several GPUs the
+    shared vectors are symmetric buffers every rank adds into over NVLink.
+    ``y_out`` of ``run`` is [ranks, y_stride] f32: rank r writes its last op's output at row r."""
+
+    def __init__(self, rank_ops: list, y_alpha: float = 1.0):
+        W = len(rank_ops)
+        if not 1 <= W <= 8 or any(len(ops) != len(rank_ops[0]) for ops in rank_ops) or not rank_ops[0]:
+            raise ConfigError("rank programs need 1..8 ranks with the same non-empty op sequence")
+        lib = _capi.lib()
+        nbytes = lib.pmpd_engine_op_bytes()
+        G = lib.pmpd_engine_grid() // W
+        n_ops = len(rank_ops[0])
+        self.n_ranks, self.n_ops, self.parts = W, n_ops, []
+        host = (ctypes.c_uint8 * (nbytes * n_ops * W))()
+        counts, contribs, bounds = {}, {}, {}
+        for r, ops in enumerate(rank_ops):
+            for i, spec in enumerate(ops):
+                if spec.attn is not None or spec.in_mode != IN_SRC or spec.act != 0 and spec.act != 1:
+                    raise ConfigError("rank programs run linear-stack ops only")
+                if spec.src >= i:
+                    raise ConfigError(f"op {i} reads op {spec.src}, which does not precede it")
+                desc = spec.packed.desc
+                b_host = (ctypes.c_int32 * (G + 1))()
+                _capi.call("pmpd_engine_partition_g", spec.packed.ref(), G, ctypes.addressof(b_host))
+                kt, cnt, contrib = desc.k_tiles, [0] * desc.n_tiles, 0
+                for c in range(G):
+                    t0, t1 = b_host[c], b_host[c + 1]
+                    if t1 > t0:
+                        contrib += 1
+                        for ng in range(t0 // kt, (t1 - 1) // kt + 1):
+                            cnt[ng] += 1
+                counts[(r, i)], contribs[(r, i)], bounds[(r, i)] = cnt, contrib, b_host
+        shared_acc, shared_cnt = {}, {}
+        for r, ops in enumerate(rank_ops):
+            for i, spec in enumerate(ops):
+                key = spec.out if isinstance(spec.out, str) else None
+                if key is not None:
+                    tot = shared_cnt.setdefault(key, [0] * spec.packed.desc.n_tiles)
+                    if len(tot) != spec.packed.desc.n_tiles:
+                        raise ConfigError(f"shared output '{key}' has different widths across ranks")
+                    for ng, v in enumerate(counts[(r, i)]):
+                        tot[ng] += v
+        for key, tot in shared_cnt.items():
+            if max(tot) > 255:
+                raise ConfigError(f"shared output '{key}': more than 255 contributors per n-group")
+            shared_acc[key] = (torch.zeros(2 * len(tot) * 64, dtype=torch.int64, device="cuda"),
+                               torch.tensor(tot, dtype=torch.uint8, device="cuda"))
+        for r, ops in enumerate(rank_ops):
+            for i, spec in enumerate(ops):
+                addr = ctypes.addressof(host) + (r * n_ops + i) * nbytes
+                desc = spec.packed.desc
+                if spec.src >= 0:
+                    width = spec.src_col + (spec.act_off if spec.act == 1 else 0) + desc.k_tiles * 64
+                    if width > ops[spec.src].packed.desc.n_tiles * 64:
+                        raise ConfigError(f"rank {r} op {i} reads past the end of op {spec.src}'s output")
+                part = torch.zeros(1, dtype=torch.float32, device="cuda")  # unused (op-table ABI)
+                ns0 = torch.tensor(counts[(r, i)], dtype=torch.uint8, device="cuda")
+                self.parts.append((part, ns0))
+                _capi.call("pmpd_engine_make_op", spec.packed.ref(), spec.src, spec.src_col, spec.act, spec.act_off,
+                           float(spec.in_alpha), part.data_ptr(), 1, ns0.data_ptr(), addr)
+                bd = torch.frombuffer(bytearray(bounds[(r, i)]), dtype=torch.int32).cuda()
+                self.parts.append((bd,))
+                _capi.call("pmpd_engine_op_set_bounds", addr, bd.data_ptr())
+                key = spec.out if isinstance(spec.out, str) else None
+                if key is not None:
+                    acc, cs = shared_acc[key]
+                else:
+                    acc = torch.zeros(2 * desc.n_tiles * 64, dtype=torch.int64, device="cuda")
+                    cs = ns0
+                self.parts.append((acc, cs))
+                _capi.call("pmpd_engine_op_set_counted", addr, acc.data_ptr(), cs.data_ptr(), max(1, contribs[(r, i)]))
+        self.shared = shared_acc
+        self.table = torch.frombuffer(bytearray(host), dtype=torch.uint8).cuda()
+        self.bar = torch.zeros(3 + 2 * n_ops, dtype=torch.int32, device="cuda")
+        self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.y_alpha = float(y_alpha)
+        self.y_stride = max(ops[-1].packed.desc.n_tiles * 64 for ops in rank_ops)
+
+    def run(self, x_in: torch.Tensor, p_dev: torch.Tensor, y_out: torch.Tensor) -> None:
+        """Enqueue one token of every rank (graph-capturable); y_out: f32 [ranks, >= y_stride]."""
+        if y_out.dtype != torch.float32 or y_out.dim() != 2 or y_out.shape[0] < self.n_ranks or \
+                y_out.stride(0) < self.y_stride or y_out.stride(1) != 1:
+            raise ConfigError(f"y_out must be f32 [{self.n_ranks}, >= {self.y_stride}] with unit column stride")
+        _capi.call("pmpd_engine_run_ranks", self.table.data_ptr(), self.n_ops, self.n_ranks, p_dev.data_ptr(),
+                   x_in.data_ptr(), y_out.data_ptr(), y_out.stride(0), self.y_alpha, self.bar.data_ptr(),
+                   self.status.data_ptr(), torch.cuda.current_stream().cuda_stream)

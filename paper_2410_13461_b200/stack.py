@@ -277,3 +277,80 @@ class TPLinearStack:
 
     def stream_bytes(self, p: int) -> int:
         return sum(pk.stream_bytes(p) for lay in self.layers for pk in lay) + self.head.stream_bytes(p)
+
+
+class TPEngineStack:
+    """The decode linear stack tensor-parallel over ``world`` ranks INSIDE the persistent engine.
+
+    The same Megatron plan as ``TPLinearStack`` (column-parallel q|k|v by heads, gate|up at the same
+    offsets in both halves, head by vocabulary; row-parallel o and down), but the row-parallel
+    all-reduce is not an NCCL call between per-op kernels: every rank's o / down partials are added
+    into one counted fixed-point vector whose contributor counts sum all ranks' partitions
+    (``engine.RankProgram``), so the whole token of every rank is one engine launch and the
+    reduction order never matters (bit-identical across runs).  On one GPU the ranks run as CTA
+    groups of a single launch (the emulation the B200 profiling guide prescribes for kernels that
+    wait on other ranks); weights come from the same generator as ``LinearStack`` so the 1-GPU
+    stack is the reference for the sharded one.
+    """
+
+    def __init__(self, shape: StackShape, n_heads: int, world: int, p_max: int = 4, group_size: int = 64,
+                 seed: int = 0, std: float = 0.02):
+        from . import tp
+        from .engine import OpSpec, RankProgram
+        self.shape, self.world, self.std = shape, world, std
+        d, f, V = shape.d_model, shape.d_ff, shape.vocab
+        gen = torch.Generator(device="cuda")
+        gen.manual_seed(seed)
+        plans = [tp.plan_layer(d, n_heads, f, world, r, group_size) for r in range(world)]
+        heads = [tp.plan_head(V, world, r, group_size) for r in range(world)]
+        self.head_slices = heads
+        a_d = 1.0 / (std * math.sqrt(d))
+        a_f = 1.0 / (std * math.sqrt(f))
+
+        def make(K, N):
+            w = _rand_kn(K, N, std, gen)
+            qt = quantize_tensor(w, p_max, group_size)
+            del w
+            return qt
+
+        self.packs = []  # keeps the shards alive
+        rank_ops = [[] for _ in range(world)]
+        for i in range(shape.n_layers):
+            qkv, o, up, dn = make(d, 3 * d), make(d, d), make(d, 2 * f), make(f, d)
+            for r, P in enumerate(plans):
+                pk = [tp.shard_columns(qkv, P.qkv_cols).packed(_capi.LAYOUT_KN),
+                      tp.shard_rows(o, P.o_rows).packed(_capi.LAYOUT_KN),
+                      tp.shard_columns(up, P.up_cols).packed(_capi.LAYOUT_KN),
+                      tp.shard_rows(dn, P.down_rows).packed(_capi.LAYOUT_KN)]
+                self.packs.append(pk)
+                base = 4 * i
+                hq = P.o_rows.size
+                ops = rank_ops[r]
+                ops.append(OpSpec(pk[0], src=base - 1, src_col=0, in_alpha=a_f if i else 1.0))
+                ops.append(OpSpec(pk[1], src=base, src_col=2 * hq, in_alpha=a_d, out="o"))       # row-parallel
+                ops.append(OpSpec(pk[2], src=base + 1, src_col=0, in_alpha=a_d))
+                ops.append(OpSpec(pk[3], src=base + 2, src_col=0, in_alpha=a_d, out="down"))    # row-parallel
+            del qkv, o, up, dn
+        head = make(d, V)
+        for r in range(world):
+            pk = tp.shard_columns(head, [heads[r]]).packed(_capi.LAYOUT_KN)
+            self.packs.append([pk])
+            rank_ops[r].append(OpSpec(pk, src=len(rank_ops[r]) - 1, src_col=0, in_alpha=a_f))
+        del head
+        # one shared (all-reduced) vector per layer's o and down
+        for r in range(world):
+            for j, sp in enumerate(rank_ops[r]):
+                if isinstance(sp.out, str):
+                    sp.out = f"{sp.out}{j // 4}"
+        torch.cuda.synchronize()
+        self.program = RankProgram(rank_ops, y_alpha=a_d)
+        self.x0 = torch.randn((1, d), device="cuda", generator=gen).half()
+        self.y = torch.zeros((world, self.program.y_stride), device="cuda", dtype=torch.float32)
+        self.p_dev = torch.full((1,), p_max, dtype=torch.int32, device="cuda")
+
+    def logits(self) -> torch.Tensor:
+        """The full vocabulary row assembled from the ranks' head shards."""
+        return torch.cat([self.y[r, :sl.size] for r, sl in enumerate(self.head_slices)])
+
+    def token(self) -> None:
+        self.program.run(self.x0, self.p_dev, self.y)

@@ -1,3 +1,3 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python tools/model_bench.py 2 > gpurun_out/mb2.log 2>&1
-timeout 1500 python tools/model_bench.py 3 > gpurun_out/mb3.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_tp_engine.py tests/test_gpu_engine.py -q -x > gpurun_out/t_tpe.log 2>&1
+timeout 300 python tools/engine_probe.py > gpurun_out/probe.log 2>&1

@@ -222,7 +222,9 @@ def arm_config(args, world: int, tp_mode: bool) -> dict:
     return {"workload": f"{args.shape} decode linear stack (32x q|k|v,o,gate|up,down + head), batch 1, "
                         "progressive 4->3->2 switching at tokens 32/128 over 512 tokens per step",
             "schedule": {str(k): v for k, v in SCHED.items()}, "horizon": HORIZON,
-            "parallelism": f"tp{world} (NCCL all-reduce after o and down)" if tp_mode else "single GPU",
+            "parallelism": (f"tp{world} (row-parallel all-reduce inside the engine: counted additions into every "
+                            "rank's symmetric-memory copy)" if os.environ.get("PMPD_TP_ENGINE") == "1" else
+                            f"tp{world} (NCCL all-reduce after o and down)") if tp_mode else "single GPU",
             "l2": "inputs larger than L2 (2.5-4.1 GB of planes per token vs 126 MB L2)"}
 
 
@@ -323,7 +325,16 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
 
-    if tp_mode:
+    tp_engine = tp_mode and os.environ.get("PMPD_TP_ENGINE") == "1"
+    if tp_engine:
+        # tensor parallel INSIDE the engine: each rank one launch per token, the row-parallel
+        # all-reduce = counted additions into every rank's symmetric-memory copy over NVLink
+        from paper_2410_13461_b200.stack import TPEngineStack
+        heads = 32 if args.shape == "7b" else 16
+        st = TPEngineStack(shape, heads, world, seed=1234, group=dist.group.WORLD, rank=rank)
+        g = st.capture(st.token)
+        g_ops = g
+    elif tp_mode:
         # tensor parallel over the node's GPUs: column/row-split GEMVs + NCCL all-reduce per row-split layer
         from paper_2410_13461_b200.stack import TPLinearStack
         heads = 32 if args.shape == "7b" else 16
@@ -423,8 +434,8 @@ def main():
     us_tok = ms * 1e3 / (args.steps * HORIZON)
 
     # ---- e2e: per token H2D of the input activation from pinned host + D2H of the logits
-    x_dev = st.x16 if tp_mode else st.x0
-    y_dev = st.logits_all if tp_mode else st.logits
+    x_dev = st.x16 if tp_mode and not tp_engine else st.x0
+    y_dev = st.y if tp_engine else st.logits_all if tp_mode else st.logits
     x_host = x_dev.cpu().pin_memory()
     out_host = torch.empty(y_dev.shape, dtype=torch.float32).pin_memory()
 
@@ -480,7 +491,7 @@ def main():
         "clocks": clk.summary(),
         "e2e": {"value": e2e_us, "unit": "us/token", "h2d_bytes_per_step": HORIZON * x_dev.numel() * 2,
                 "d2h_bytes_per_step": HORIZON * y_dev.numel() * 4},
-        "gpu_launches": args.steps * HORIZON * (2 + 4 * shape.n_layers if tp_mode else 2),
+        "gpu_launches": args.steps * HORIZON * (2 + 4 * shape.n_layers if tp_mode and not tp_engine else 2),
     }
     if prefill is not None:
         out["prefill"] = prefill

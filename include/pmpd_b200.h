@@ -211,7 +211,7 @@ int pmpd_engine_make_op(const pmpd_qtensor* t, int32_t src, int32_t src_col, int
  *     is an argument of pmpd_engine_run_decoder).
  *   pmpd_engine_make_attn_op: attention over one layer's f16 KV cache for the new token: q|k|v =
  *     the output of op `src`; RoPE at position T = *T_dev (cos/sin [max_ctx][d_head/2]);
- *     k, v appended to row T; records_dev = u64 [2][pmpd_engine_attn_records()].
+ *     k, v appended to row T; records_dev = u64 [3][pmpd_engine_attn_records()].
  *     d_head in {32, 64, 128, 256}. */
 int pmpd_engine_op_set_io(void* op_host, int32_t in_mode, const float* resid_dev, const float* gain_dev, float eps,
                           int32_t keep_out, float out_alpha);
@@ -227,20 +227,20 @@ int pmpd_engine_partition(const pmpd_qtensor* t, int32_t* bounds_host);
 int pmpd_engine_partition_g(const pmpd_qtensor* t, int32_t G, int32_t* bounds_host);
 int pmpd_engine_op_set_bounds(void* op_host, const int32_t* bounds_dev);
 /* Counted accumulation (linear-stack programs run by pmpd_engine_run): the op's output is
- * acc_dev = u64 [2][n_tiles * 64] zero-initialised words, each holding [63:56] the number of CTAs
+ * acc_dev = u64 [3][n_tiles * 64] zero-initialised words, each holding [63:56] the number of CTAs
  * that added into it and [55:0] the sum of their partials as 2^-24 fixed point (offset binary),
  * so split-K sums are bit-reproducible and self-validating; nslots_dev[n_tiles] = contributors
  * per n-group under the op's bounds, n_contrib = CTAs with a nonempty range.  bar_dev of the run
  * then holds 3 + n_ops u32 (tickets, done, launch epoch, per-op hint counters), zeroed once. */
 int pmpd_engine_op_set_counted(void* op_host, void* acc_dev, const uint8_t* nslots_dev, int32_t n_contrib);
 /* Decoder programs (pmpd_engine_run_decoder): every linear op is counted (pmpd_engine_op_set_counted);
- * the o / down ops (keep_out) add into ONE counted residual stream resid_dev = u64 [2][resid_len]
+ * the o / down ops (keep_out) add into ONE counted residual stream resid_dev = u64 [3][resid_len]
  * (resid_len = d rounded up to 64, zero-initialised), into which the launch first adds x0_dev (f32
  * [d_real], the embedding row written before the launch).  An RMSNorm op reads the stream when each
  * word's contribution count reaches cum_dev[n-group] (u16, static: 1 + the contributors of every
  * residual op before it); a residual op passes rwait = the index of the RMSNorm op whose readers
  * must have read the stream before it adds (-1: none).  Attention records are single-writer words,
- * records_dev = u64 [2][pmpd_engine_attn_records()].  bar_dev holds 3 + 2 * n_ops u32. */
+ * records_dev = u64 [3][pmpd_engine_attn_records()].  bar_dev holds 3 + 2 * n_ops u32. */
 int pmpd_engine_op_set_residual(void* op_host, const uint16_t* cum_dev, int32_t rwait);
 int pmpd_engine_run_decoder(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const float* x0_dev,
                             void* resid_dev, int64_t resid_len, int32_t d_real, float* y_out_dev, float y_alpha,
@@ -252,6 +252,11 @@ int pmpd_engine_run_decoder(const void* ops_dev, int32_t n_ops, const int32_t* p
  * groups, group r runs table r and writes y_out + r * y_stride.  A row-parallel op's counted output
  * is one vector shared by every rank's op record, with contributor counts summed over the ranks:
  * the cross-rank all-reduce is the counted addition itself (no collective call). */
+/* Row-parallel op of a tensor-parallel program: add every partial into each of the n_peers copies
+ * of the op's output (this rank's own copy among them: the copies are the ranks' symmetric
+ * buffers, u64 [3][n_tiles * 64] each); sys_scope = 1 when the copies live on other GPUs
+ * (system-scope additions and polls over NVLink). */
+int pmpd_engine_op_set_peers(void* op_host, const void* const* peers_host, int32_t n_peers, int32_t sys_scope);
 int pmpd_engine_run_ranks(const void* ops_dev, int32_t n_ops, int32_t n_ranks, const int32_t* p_dev,
                           const void* x_in_dev, float* y_out_dev, int32_t y_stride, float y_alpha, uint32_t* bar_dev,
                           int32_t* status_dev, void* stream);

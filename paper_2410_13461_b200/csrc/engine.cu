@@ -89,6 +89,12 @@ struct EngineOp {
   int n_contrib;            // CTAs with a nonempty tile range (each adds 1 to the op's hint counter)
   const unsigned short* cum;  // E_IN_RMSNORM: contributions in each residual word at this point
   int rwait;                  // residual op: the RMSNorm op whose readers must be done before adding
+  // tensor parallelism: a row-parallel op adds each partial into every rank's copy of its output
+  // (n_peers > 0: peer[0..n_peers), this rank's own copy among them; sys = the copies live on
+  // other GPUs: system-scope additions, and their consumers poll with system-scope loads)
+  unsigned long long* peer[8];
+  int n_peers;
+  int sys;
 };
 constexpr int E_LINEAR = 0, E_ATTN = 1;
 constexpr int E_IN_SRC = 0, E_IN_RMSNORM = 2, E_IN_ATTN = 3;
@@ -105,6 +111,12 @@ PMPD_DEV int attn_rec(int dh) { return 4 + dh; }  // record: m, l, pad, pad, acc
 #ifndef PMPD_ENGINE_HINT_RELEASE
 #define PMPD_ENGINE_HINT_RELEASE 0 // 1: the hint add is a release (orders the data adds before it)
 #endif
+// Three buffer sets per counted vector, used round-robin by launch epoch: launch L adds into set
+// L % 3 and zeroes set (L - 1) % 3, the one launch L + 2 will use.  With peers on other GPUs
+// (tensor parallelism) a peer may already be in launch L + 1 adding into set (L + 1) % 3 of this
+// rank's copy while this rank finishes launch L, so the set being zeroed is never one a peer can
+// still be writing (its last writes to set (L - 1) % 3 were all observed before launch L began).
+constexpr int kSets = 3;
 constexpr int kCntShift = 54;                  // up to 1023 contributions per word (the residual
                                                // stream accumulates every o / down partial of a step)
 constexpr unsigned long long kValMask = (1ull << kCntShift) - 1;
@@ -136,6 +148,9 @@ PMPD_DEV void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
 }
 PMPD_DEV void ld_relaxed_u64x2(const unsigned long long* p, unsigned long long& a, unsigned long long& b) {
   asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+PMPD_DEV void ld_relaxed_sys_u64x2(const unsigned long long* p, unsigned long long& a, unsigned long long& b) {
+  asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
 PMPD_DEV unsigned long long ld_relaxed_u64(const unsigned long long* p) {
   unsigned long long v;
@@ -854,7 +869,7 @@ __noinline__ __device__ float stage_attn_input(const EngineOp& op, const EngineO
 template <bool DEC>
 PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bars& bars, int G, int c,
                             int stage_bytes, int nstage, unsigned epoch) {
-  const int par = (int)(epoch & 1u);  // counted programs: parity set of this launch
+  const int par = (int)(epoch % kSets);  // counted programs: the buffer set of this launch
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gq = lane >> 2, tig = lane & 3;
   __half* xs = reinterpret_cast<__half*>(smem + kSmX);
   uint8_t* xq = smem + kSmXq + warp * E_TPW * 128;
@@ -1080,8 +1095,13 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
                 const int k = kb + bi * 4 * E_NCW * 32;
                 const int n = op.src_col + which * op.act_off + k;
                 if (k < khi) {
-                  ld_relaxed_u64x2(sa + n, w[bi][0], w[bi][1]);
-                  ld_relaxed_u64x2(sa + n + 2, w[bi][2], w[bi][3]);
+                  if (src->sys) {  // a row-parallel output other GPUs add into
+                    ld_relaxed_sys_u64x2(sa + n, w[bi][0], w[bi][1]);
+                    ld_relaxed_sys_u64x2(sa + n + 2, w[bi][2], w[bi][3]);
+                  } else {
+                    ld_relaxed_u64x2(sa + n, w[bi][0], w[bi][1]);
+                    ld_relaxed_u64x2(sa + n + 2, w[bi][2], w[bi][3]);
+                  }
                 } else {
                   w[bi][0] = w[bi][1] = w[bi][2] = w[bi][3] = 0ull;
                 }
@@ -1340,13 +1360,14 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
     // ------------------------------------------------------------ epilogue
     float* red = reinterpret_cast<float*>(smem + kSmRed);
     float* redb = reinterpret_cast<float*>(smem + kSmRedb);
-    const int par = (int)(epoch & 1u);
+    const int par = (int)(epoch % kSets);
+    const int zset = (int)((epoch + kSets - 1) % kSets);  // the set the previous launch used
     if (DEC) {
       // residual stream: zero this CTA's slice of the idle parity set, then add x0 (the
       // embedding row, written before the launch) into slice c of this launch's set: one
       // contribution per word
       unsigned long long* Rc = a.R + (long long)par * a.R_len;
-      unsigned long long* Ro = a.R + (long long)(par ^ 1) * a.R_len;
+      unsigned long long* Ro = a.R + (long long)zset * a.R_len;
       for (long long i = a.R_len * c / G + lane, e = a.R_len * (c + 1) / G; i < e; i += 32) Ro[i] = 0ull;
       for (int i = (int)((long long)a.d_real * c / G) + lane, e = (int)((long long)a.d_real * (c + 1) / G); i < e;
            i += 32)
@@ -1385,7 +1406,18 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
             float v = bsum;
 #pragma unroll
             for (int w = 0; w < E_NCW; ++w) v += red[(buf * E_NCW + w) * 64 + nl];
-            red_relaxed_u64(acc + (int64_t)ng * 64 + nl, fix_encode(DEC ? v * op.out_alpha : v, a.status));
+            const unsigned long long w = fix_encode(DEC ? v * op.out_alpha : v, a.status);
+            if (op.n_peers == 0) {
+              red_relaxed_u64(acc + (int64_t)ng * 64 + nl, w);
+            } else {
+              const long long off = (long long)par * op.acc_len + (int64_t)ng * 64 + nl;
+              for (int j = 0; j < op.n_peers; ++j) {
+                if (op.sys)
+                  asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(op.peer[j] + off), "l"(w) : "memory");
+                else
+                  red_relaxed_u64(op.peer[j] + off, w);
+              }
+            }
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(&bars.red_empty[buf]);
@@ -1411,7 +1443,7 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
       if (!(op.kind == E_LINEAR && op.keep_out)) {
         // zero this CTA's slice of the op's idle parity set (outputs / attention records) for the
         // next launch (the residual stream's was zeroed at the start)
-        unsigned long long* other = op.acc + (long long)(par ^ 1) * op.acc_len;
+        unsigned long long* other = op.acc + (long long)zset * op.acc_len;
         for (long long i = op.acc_len * c / G + lane, e = op.acc_len * (c + 1) / G; i < e; i += 32) other[i] = 0ull;
       }
     }
@@ -1424,7 +1456,7 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
   __syncthreads();
   const EngineOp& last = a.ops[a.n_ops - 1];
   {
-    const int par = (int)(epoch & 1u);
+    const int par = (int)(epoch % kSets);
     if (!PMPD_ENGINE_NOHINT && threadIdx.x == 0)
       wait_hint(a.bar + 3 + a.n_ops - 1, (epoch + 1u) * (unsigned)last.n_contrib);
     __syncthreads();
@@ -1657,6 +1689,21 @@ int pmpd_engine_op_set_counted(void* op_host, void* acc_dev, const uint8_t* nslo
   op.acc_len = (long long)op.n_tiles * 64;
   op.nslots = nslots_dev;
   op.n_contrib = n_contrib;
+  return PMPD_OK;
+}
+
+int pmpd_engine_op_set_peers(void* op_host, const void* const* peers_host, int32_t n_peers, int32_t sys_scope) {
+  if (!op_host || (n_peers > 0 && !peers_host)) return fail(PMPD_ERR_CONFIG, "null argument");
+  if (n_peers < 0 || n_peers > 8) return fail(PMPD_ERR_CONFIG, "1..8 peer copies, got %d", n_peers);
+  EngineOp& op = *static_cast<EngineOp*>(op_host);
+  if (op.kind != E_LINEAR) return fail(PMPD_ERR_CONFIG, "peer copies apply to linear ops");
+  for (int j = 0; j < n_peers; ++j) {
+    if (!peers_host[j] || (reinterpret_cast<uintptr_t>(peers_host[j]) & 15))
+      return fail(PMPD_ERR_CONFIG, "peer copy %d must be a 16-byte aligned device pointer", j);
+    op.peer[j] = static_cast<unsigned long long*>(const_cast<void*>(peers_host[j]));
+  }
+  op.n_peers = n_peers;
+  op.sys = sys_scope ? 1 : 0;
   return PMPD_OK;
 }
 

@@ -25,6 +25,7 @@ from .quant import PackedTensor
 
 
 IN_SRC, IN_RMSNORM, IN_ATTN = 0, 2, 3  # engine.cu E_IN_*
+SETS = 3  # buffer sets per counted vector (engine.cu kSets), used round-robin by launch
 
 
 @dataclass
@@ -93,7 +94,7 @@ class Program:
                 raise ConfigError("decoder program without an RMSNorm input op")
             self.d_real = rms[0].packed.desc.k
             d_tiles = rms[0].packed.desc.k_tiles
-            self.R = torch.zeros(2 * d_tiles * 64, dtype=torch.int64, device="cuda")
+            self.R = torch.zeros(SETS * d_tiles * 64, dtype=torch.int64, device="cuda")
             running = [1] * d_tiles
         host = (ctypes.c_uint8 * (nbytes * len(ops)))()
         for i, spec in enumerate(ops):
@@ -102,7 +103,7 @@ class Program:
             addr = ctypes.addressof(host) + i * nbytes
             if spec.attn is not None:
                 at = spec.attn
-                rec = torch.zeros(2 * lib.pmpd_engine_attn_records(at.n_heads, at.d_head), dtype=torch.int64,
+                rec = torch.zeros(SETS * lib.pmpd_engine_attn_records(at.n_heads, at.d_head), dtype=torch.int64,
                                   device="cuda")
                 self.parts.append((rec, at))
                 _capi.call("pmpd_engine_make_attn_op", spec.src, at.n_heads, at.d_head, at.k_cache.data_ptr(),
@@ -151,7 +152,7 @@ class Program:
                     raise ConfigError(f"op {i}: residual output width differs from the residual stream")
                 acc = self.R
             else:
-                acc = torch.zeros(2 * nt * 64, dtype=torch.int64, device="cuda")
+                acc = torch.zeros(SETS * nt * 64, dtype=torch.int64, device="cuda")
             self.parts.append((acc, cs))
             _capi.call("pmpd_engine_op_set_counted", addr, acc.data_ptr(), cs.data_ptr(), contrib)
             if spec.in_mode != IN_SRC or spec.out is not None or spec.out_alpha != 1.0:
@@ -187,7 +188,7 @@ class Program:
             if x_in.dtype != torch.float32 or x_in.shape[-1] < self.d_real:
                 raise ConfigError("decoder program input must be the f32 embedding row")
             _capi.call("pmpd_engine_run_decoder", self.table.data_ptr(), len(self.ops), p_dev.data_ptr(),
-                       x_in.data_ptr(), self.R.data_ptr(), self.R.numel() // 2, self.d_real, y_out.data_ptr(),
+                       x_in.data_ptr(), self.R.data_ptr(), self.R.numel() // SETS, self.d_real, y_out.data_ptr(),
                        self.y_alpha, self.bar.data_ptr(), self.status.data_ptr(), trace, s)
         elif trace is not None:
             _capi.call("pmpd_engine_run_traced", self.table.data_ptr(), len(self.ops), p_dev.data_ptr(),
@@ -213,34 +214,42 @@ class Program:
 
 class RankProgram:
     """Tensor-parallel linear-stack program: ``rank_ops[r]`` is rank r's op chain (its Megatron
-    shards, the same op sequence on every rank).  An op whose ``OpSpec.out`` is set to a string key
-    is row-parallel: every rank's op with that key adds into ONE counted vector whose contributor
-    counts sum the ranks' partitions, so the cross-rank all-reduce is the engine's own counted
-    addition (deterministic, no collective call).  On one GPU all ranks run in one launch
-    (``pmpd_engine_run_ranks``, the grid split into ``len(rank_ops)`` groups); on several GPUs the
-    shared vectors are symmetric buffers every rank adds into over NVLink.
-    ``y_out`` of ``run`` is [ranks, y_stride] f32: rank r writes its last op's output at row r."""
+    shards, the same op sequence on every rank).  An op whose ``OpSpec.out`` is a string key is
+    row-parallel: EVERY rank holds a copy of that output and every rank's op adds each partial into
+    every copy, with contributor counts summing all ranks' partitions; each rank's consumers poll
+    their own copy.  The cross-rank all-reduce is therefore the engine's own counted addition
+    (deterministic, no collective call), the data flow of one GPU per rank over NVLink.
 
-    def __init__(self, rank_ops: list, y_alpha: float = 1.0):
+    * ``dist=None`` (one GPU): every rank is built here and all run in ONE launch
+      (``pmpd_engine_run_ranks``, the grid split into ``len(rank_ops)`` CTA groups) -- the
+      emulation the B200 profiling guide prescribes for kernels that wait on other ranks;
+    * ``dist=(group, rank)``: this process runs rank ``rank`` of ``len(rank_ops)`` (only its own op
+      table needs real tensors; the others provide shapes for the counts) and the shared copies are
+      torch symmetric-memory buffers of the group, added into with system-scope atomics.
+    ``y_out`` of ``run`` is [ranks, y_stride] f32: rank r writes its last op's output at row r (one
+    row, this rank's, in the distributed mode)."""
+
+    def __init__(self, rank_ops: list, y_alpha: float = 1.0, dist=None):
         W = len(rank_ops)
         if not 1 <= W <= 8 or any(len(ops) != len(rank_ops[0]) for ops in rank_ops) or not rank_ops[0]:
             raise ConfigError("rank programs need 1..8 ranks with the same non-empty op sequence")
         lib = _capi.lib()
         nbytes = lib.pmpd_engine_op_bytes()
-        G = lib.pmpd_engine_grid() // W
+        local = [dist[1]] if dist is not None else list(range(W))
+        n_emul = len(local)
+        G = lib.pmpd_engine_grid() // n_emul
         n_ops = len(rank_ops[0])
-        self.n_ranks, self.n_ops, self.parts = W, n_ops, []
-        host = (ctypes.c_uint8 * (nbytes * n_ops * W))()
+        self.n_ranks, self.n_emul, self.n_ops, self.parts = W, n_emul, n_ops, []
         counts, contribs, bounds = {}, {}, {}
         for r, ops in enumerate(rank_ops):
             for i, spec in enumerate(ops):
-                if spec.attn is not None or spec.in_mode != IN_SRC or spec.act != 0 and spec.act != 1:
+                if spec.attn is not None or spec.in_mode != IN_SRC or spec.act not in (0, 1):
                     raise ConfigError("rank programs run linear-stack ops only")
                 if spec.src >= i:
                     raise ConfigError(f"op {i} reads op {spec.src}, which does not precede it")
                 desc = spec.packed.desc
                 b_host = (ctypes.c_int32 * (G + 1))()
-                _capi.call("pmpd_engine_partition_g", spec.packed.ref(), G, ctypes.addressof(b_host))
+                _capi.call("pmpd_engine_partition_g", ctypes.byref(desc), G, ctypes.addressof(b_host))
                 kt, cnt, contrib = desc.k_tiles, [0] * desc.n_tiles, 0
                 for c in range(G):
                     t0, t1 = b_host[c], b_host[c + 1]
@@ -249,24 +258,42 @@ class RankProgram:
                         for ng in range(t0 // kt, (t1 - 1) // kt + 1):
                             cnt[ng] += 1
                 counts[(r, i)], contribs[(r, i)], bounds[(r, i)] = cnt, contrib, b_host
-        shared_acc, shared_cnt = {}, {}
+        # shared (row-parallel) outputs: contributor totals over the ranks, one copy per rank
+        totals = {}
         for r, ops in enumerate(rank_ops):
             for i, spec in enumerate(ops):
-                key = spec.out if isinstance(spec.out, str) else None
-                if key is not None:
-                    tot = shared_cnt.setdefault(key, [0] * spec.packed.desc.n_tiles)
+                if isinstance(spec.out, str):
+                    tot = totals.setdefault(spec.out, [0] * spec.packed.desc.n_tiles)
                     if len(tot) != spec.packed.desc.n_tiles:
-                        raise ConfigError(f"shared output '{key}' has different widths across ranks")
+                        raise ConfigError(f"shared output '{spec.out}' has different widths across ranks")
                     for ng, v in enumerate(counts[(r, i)]):
                         tot[ng] += v
-        for key, tot in shared_cnt.items():
+        copies, peers, tot_dev, self.handles = {}, {}, {}, []
+        for key, tot in totals.items():
             if max(tot) > 255:
                 raise ConfigError(f"shared output '{key}': more than 255 contributors per n-group")
-            shared_acc[key] = (torch.zeros(2 * len(tot) * 64, dtype=torch.int64, device="cuda"),
-                               torch.tensor(tot, dtype=torch.uint8, device="cuda"))
-        for r, ops in enumerate(rank_ops):
+            tot_dev[key] = torch.tensor(tot, dtype=torch.uint8, device="cuda")
+            n = SETS * len(tot) * 64
+            if dist is None:
+                copies[key] = {r: torch.zeros(n, dtype=torch.int64, device="cuda") for r in range(W)}
+                peers[key] = [copies[key][r].data_ptr() for r in range(W)]
+            else:
+                import torch.distributed._symmetric_memory as symm_mem
+                buf = symm_mem.empty(n, dtype=torch.int64, device="cuda")
+                buf.zero_()
+                hdl = symm_mem.rendezvous(buf, dist[0])
+                self.handles.append((buf, hdl))
+                copies[key] = {dist[1]: buf}
+                peers[key] = [int(ptr) for ptr in hdl.buffer_ptrs]
+        if dist is not None:
+            torch.cuda.synchronize()
+            import torch.distributed as tdist
+            tdist.barrier(group=dist[0])  # every rank's copies are zero before anyone adds
+        host = (ctypes.c_uint8 * (nbytes * n_ops * n_emul))()
+        for slot, r in enumerate(local):
+            ops = rank_ops[r]
             for i, spec in enumerate(ops):
-                addr = ctypes.addressof(host) + (r * n_ops + i) * nbytes
+                addr = ctypes.addressof(host) + (slot * n_ops + i) * nbytes
                 desc = spec.packed.desc
                 if spec.src >= 0:
                     width = spec.src_col + (spec.act_off if spec.act == 1 else 0) + desc.k_tiles * 64
@@ -282,13 +309,16 @@ class RankProgram:
                 _capi.call("pmpd_engine_op_set_bounds", addr, bd.data_ptr())
                 key = spec.out if isinstance(spec.out, str) else None
                 if key is not None:
-                    acc, cs = shared_acc[key]
+                    acc, cs = copies[key][r], tot_dev[key]
                 else:
-                    acc = torch.zeros(2 * desc.n_tiles * 64, dtype=torch.int64, device="cuda")
-                    cs = ns0
+                    acc, cs = torch.zeros(SETS * desc.n_tiles * 64, dtype=torch.int64, device="cuda"), ns0
                 self.parts.append((acc, cs))
                 _capi.call("pmpd_engine_op_set_counted", addr, acc.data_ptr(), cs.data_ptr(), max(1, contribs[(r, i)]))
-        self.shared = shared_acc
+                if key is not None:
+                    arr = (ctypes.c_void_p * W)(*peers[key])
+                    _capi.call("pmpd_engine_op_set_peers", addr, ctypes.cast(arr, ctypes.c_void_p), W,
+                               int(dist is not None))
+        self.copies = copies
         self.table = torch.frombuffer(bytearray(host), dtype=torch.uint8).cuda()
         self.bar = torch.zeros(3 + 2 * n_ops, dtype=torch.int32, device="cuda")
         self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -296,10 +326,11 @@ class RankProgram:
         self.y_stride = max(ops[-1].packed.desc.n_tiles * 64 for ops in rank_ops)
 
     def run(self, x_in: torch.Tensor, p_dev: torch.Tensor, y_out: torch.Tensor) -> None:
-        """Enqueue one token of every rank (graph-capturable); y_out: f32 [ranks, >= y_stride]."""
-        if y_out.dtype != torch.float32 or y_out.dim() != 2 or y_out.shape[0] < self.n_ranks or \
+        """Enqueue one token of every local rank (graph-capturable); y_out: f32 [ranks run here,
+        >= y_stride]."""
+        if y_out.dtype != torch.float32 or y_out.dim() != 2 or y_out.shape[0] < self.n_emul or \
                 y_out.stride(0) < self.y_stride or y_out.stride(1) != 1:
-            raise ConfigError(f"y_out must be f32 [{self.n_ranks}, >= {self.y_stride}] with unit column stride")
-        _capi.call("pmpd_engine_run_ranks", self.table.data_ptr(), self.n_ops, self.n_ranks, p_dev.data_ptr(),
+            raise ConfigError(f"y_out must be f32 [{self.n_emul}, >= {self.y_stride}] with unit column stride")
+        _capi.call("pmpd_engine_run_ranks", self.table.data_ptr(), self.n_ops, self.n_emul, p_dev.data_ptr(),
                    x_in.data_ptr(), y_out.data_ptr(), y_out.stride(0), self.y_alpha, self.bar.data_ptr(),
                    self.status.data_ptr(), torch.cuda.current_stream().cuda_stream)

@@ -279,22 +279,37 @@ class TPLinearStack:
         return sum(pk.stream_bytes(p) for lay in self.layers for pk in lay) + self.head.stream_bytes(p)
 
 
+class _ShapeOnly:
+    """Another rank's shard in the distributed mode: only its shape (for the contributor counts)."""
+
+    def __init__(self, rows: int, cols: int, group_size: int, p_max: int):
+        self.desc = _capi.describe(rows, cols, group_size, p_max, _capi.LAYOUT_KN)
+
+    def ref(self):
+        import ctypes
+        return ctypes.byref(self.desc)
+
+
 class TPEngineStack:
     """The decode linear stack tensor-parallel over ``world`` ranks INSIDE the persistent engine.
 
     The same Megatron plan as ``TPLinearStack`` (column-parallel q|k|v by heads, gate|up at the same
     offsets in both halves, head by vocabulary; row-parallel o and down), but the row-parallel
     all-reduce is not an NCCL call between per-op kernels: every rank's o / down partials are added
-    into one counted fixed-point vector whose contributor counts sum all ranks' partitions
-    (``engine.RankProgram``), so the whole token of every rank is one engine launch and the
-    reduction order never matters (bit-identical across runs).  On one GPU the ranks run as CTA
-    groups of a single launch (the emulation the B200 profiling guide prescribes for kernels that
-    wait on other ranks); weights come from the same generator as ``LinearStack`` so the 1-GPU
-    stack is the reference for the sharded one.
+    into every rank's copy of a counted fixed-point vector whose contributor counts sum all ranks'
+    partitions (``engine.RankProgram``), so a rank's whole token is one engine launch and the
+    reduction order never matters (bit-identical across runs).
+
+    * ``group=None``: all ranks on this GPU, one launch (CTA groups; the emulation the B200
+      profiling guide prescribes for kernels that wait on other ranks);
+    * ``group``/``rank`` (one process per GPU under torch.distributed): this rank's shards only,
+      the shared vectors in torch symmetric memory (peer copies over NVLink).
+    Weights come from the same generator as ``LinearStack`` (all ranks draw the full matrices and
+    keep their sub-blocks), so the 1-GPU stack is the reference for the sharded one.
     """
 
     def __init__(self, shape: StackShape, n_heads: int, world: int, p_max: int = 4, group_size: int = 64,
-                 seed: int = 0, std: float = 0.02):
+                 seed: int = 0, std: float = 0.02, group=None, rank: int | None = None):
         from . import tp
         from .engine import OpSpec, RankProgram
         self.shape, self.world, self.std = shape, world, std
@@ -304,6 +319,7 @@ class TPEngineStack:
         plans = [tp.plan_layer(d, n_heads, f, world, r, group_size) for r in range(world)]
         heads = [tp.plan_head(V, world, r, group_size) for r in range(world)]
         self.head_slices = heads
+        self.local = list(range(world)) if group is None else [rank]
         a_d = 1.0 / (std * math.sqrt(d))
         a_f = 1.0 / (std * math.sqrt(f))
 
@@ -313,44 +329,61 @@ class TPEngineStack:
             del w
             return qt
 
+        def col(qt, slices, r):
+            if r in self.local:
+                return tp.shard_columns(qt, slices).packed(_capi.LAYOUT_KN)
+            return _ShapeOnly(qt.rows, sum(sl.size for sl in slices), group_size, p_max)
+
+        def row(qt, sl, r):
+            if r in self.local:
+                return tp.shard_rows(qt, sl).packed(_capi.LAYOUT_KN)
+            return _ShapeOnly(sl.size, qt.cols, group_size, p_max)
+
         self.packs = []  # keeps the shards alive
         rank_ops = [[] for _ in range(world)]
         for i in range(shape.n_layers):
             qkv, o, up, dn = make(d, 3 * d), make(d, d), make(d, 2 * f), make(f, d)
             for r, P in enumerate(plans):
-                pk = [tp.shard_columns(qkv, P.qkv_cols).packed(_capi.LAYOUT_KN),
-                      tp.shard_rows(o, P.o_rows).packed(_capi.LAYOUT_KN),
-                      tp.shard_columns(up, P.up_cols).packed(_capi.LAYOUT_KN),
-                      tp.shard_rows(dn, P.down_rows).packed(_capi.LAYOUT_KN)]
+                pk = [col(qkv, P.qkv_cols, r), row(o, P.o_rows, r), col(up, P.up_cols, r), row(dn, P.down_rows, r)]
                 self.packs.append(pk)
                 base = 4 * i
                 hq = P.o_rows.size
                 ops = rank_ops[r]
                 ops.append(OpSpec(pk[0], src=base - 1, src_col=0, in_alpha=a_f if i else 1.0))
-                ops.append(OpSpec(pk[1], src=base, src_col=2 * hq, in_alpha=a_d, out="o"))       # row-parallel
+                ops.append(OpSpec(pk[1], src=base, src_col=2 * hq, in_alpha=a_d, out=f"o{i}"))     # row-parallel
                 ops.append(OpSpec(pk[2], src=base + 1, src_col=0, in_alpha=a_d))
-                ops.append(OpSpec(pk[3], src=base + 2, src_col=0, in_alpha=a_d, out="down"))    # row-parallel
+                ops.append(OpSpec(pk[3], src=base + 2, src_col=0, in_alpha=a_d, out=f"down{i}"))  # row-parallel
             del qkv, o, up, dn
         head = make(d, V)
         for r in range(world):
-            pk = tp.shard_columns(head, [heads[r]]).packed(_capi.LAYOUT_KN)
+            pk = col(head, [heads[r]], r)
             self.packs.append([pk])
             rank_ops[r].append(OpSpec(pk, src=len(rank_ops[r]) - 1, src_col=0, in_alpha=a_f))
         del head
-        # one shared (all-reduced) vector per layer's o and down
-        for r in range(world):
-            for j, sp in enumerate(rank_ops[r]):
-                if isinstance(sp.out, str):
-                    sp.out = f"{sp.out}{j // 4}"
         torch.cuda.synchronize()
-        self.program = RankProgram(rank_ops, y_alpha=a_d)
+        self.program = RankProgram(rank_ops, y_alpha=a_d, dist=None if group is None else (group, rank))
         self.x0 = torch.randn((1, d), device="cuda", generator=gen).half()
-        self.y = torch.zeros((world, self.program.y_stride), device="cuda", dtype=torch.float32)
+        self.y = torch.zeros((len(self.local), self.program.y_stride), device="cuda", dtype=torch.float32)
         self.p_dev = torch.full((1,), p_max, dtype=torch.int32, device="cuda")
+        self.step = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.sched = torch.zeros(2 * SCHED_CAPACITY, dtype=torch.int32, device="cuda")
+        self.n_prec = SCHED_CAPACITY
+        self.set_schedule({p_max: 0})
+
+    set_schedule = LinearStack.set_schedule
+    reset_step = LinearStack.reset_step
+    capture = LinearStack.capture
 
     def logits(self) -> torch.Tensor:
-        """The full vocabulary row assembled from the ranks' head shards."""
-        return torch.cat([self.y[r, :sl.size] for r, sl in enumerate(self.head_slices)])
+        """The vocabulary row from the head shards run here (all of them in the one-GPU mode)."""
+        return torch.cat([self.y[j, :self.head_slices[r].size] for j, r in enumerate(self.local)])
 
     def token(self) -> None:
+        """One token of the local rank(s) (graph-capturable): the precision hook, one engine launch."""
+        _capi.call("pmpd_sched_step", self.sched.data_ptr(), self.n_prec, self.step.data_ptr(),
+                   self.p_dev.data_ptr(), 1, torch.cuda.current_stream().cuda_stream)
         self.program.run(self.x0, self.p_dev, self.y)
+
+    def stream_bytes(self, p: int) -> int:
+        """HBM bytes of the shards run here at precision p."""
+        return sum(pk.stream_bytes(p) for lay in self.packs for pk in lay if hasattr(pk, "buf"))

@@ -33,7 +33,7 @@ def single():
 def test_tp_engine_matches_single_gpu(single, world):
     tp = TPEngineStack(SHAPE, n_heads=32, world=world, seed=7)
     for p in (4, 2):
-        tp.p_dev.fill_(p)
+        tp.set_schedule({p: 0})
         runs = []
         for _ in range(3):
             tp.token()
@@ -44,3 +44,25 @@ def test_tp_engine_matches_single_gpu(single, world):
         err = rel_l2(runs[0].cpu().numpy(), single[p].cpu().numpy())
         assert err < 3e-3, (world, p, err)
     assert int(tp.program.status.item()) == 0
+
+
+def test_tp_engine_distributed_form_world1(single, tmp_path):
+    """The one-process-per-GPU form at world 1: the shared vectors are torch symmetric-memory
+    buffers added into with system-scope atomics and polled with system-scope loads."""
+    import os
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        tp = TPEngineStack(SHAPE, n_heads=32, world=1, seed=7, group=dist.group.WORLD, rank=0)
+        for p in (4, 2):
+            tp.set_schedule({p: 0})
+            tp.token()
+            tp.token()
+            torch.cuda.synchronize()
+            err = rel_l2(tp.logits().cpu().numpy(), single[p].cpu().numpy())
+            assert err < 3e-3, (p, err)
+    finally:
+        dist.destroy_process_group()

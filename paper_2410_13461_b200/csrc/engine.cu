@@ -16,16 +16,17 @@
 //     adds them into the op's output vector at L2;
 //   * the next op's consumers stage one value per input element into an f16
 //     activation vector in shared memory.
-// Linear-stack programs (engine_kernel<false>) use COUNTED fixed-point
-// accumulation: every output element is a u64 word whose top 8 bits count the
-// contributing CTAs and whose low 56 bits sum the contributions as 2^-24
-// fixed point (offset binary).  Integer addition is associative, so the result
-// is bit-identical whatever order the split-K partials arrive in, and the word
-// itself tells a consumer when all contributors have landed: no release fence,
-// no grid-wide ticket on the op-to-op path (a relaxed per-op counter is only a
-// polling hint).  Vectors alternate between two parity sets per launch; each
-// CTA zeroes its slice of the idle set as it goes.  Decoder-step programs
-// (engine_kernel<true>) keep f32 L2 atomics and a release/acquire ticket.
+// Every program uses COUNTED fixed-point accumulation: each output element is
+// a u64 word whose top 10 bits count the contributing CTAs and whose low 54
+// bits sum the contributions as 2^-24 fixed point (offset binary).  Integer
+// addition is associative, so the result is bit-identical whatever order the
+// split-K partials arrive in, and the word itself tells a consumer when all
+// contributors have landed: no release fence, no grid-wide ticket on the
+// op-to-op path.  Vectors rotate through three buffer sets by launch epoch;
+// each CTA zeroes its slice of the previous launch's set as it goes.
+// Instantiations: engine_kernel<DEC, TP> — DEC adds the decoder-step ops
+// (attention, RMSNorm / attention-combine inputs, one counted residual stream),
+// TP the tensor-parallel rank groups and peer copies (pmpd_engine_run_ranks).
 // Co-residency of all CTAs is guaranteed by a cooperative launch.
 #include <cuda_fp16.h>
 
@@ -866,7 +867,7 @@ __noinline__ __device__ float stage_attn_input(const EngineOp& op, const EngineO
 }
 
 // ------------------------------------------------------------------ kernel
-template <bool DEC>
+template <bool DEC, bool TP>
 PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bars& bars, int G, int c,
                             int stage_bytes, int nstage, unsigned epoch) {
   const int par = (int)(epoch % kSets);  // counted programs: the buffer set of this launch
@@ -1095,7 +1096,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
                 const int k = kb + bi * 4 * E_NCW * 32;
                 const int n = op.src_col + which * op.act_off + k;
                 if (k < khi) {
-                  if (src->sys) {  // a row-parallel output other GPUs add into
+                  if (TP && src->sys) {  // a row-parallel output other GPUs add into
                     ld_relaxed_sys_u64x2(sa + n, w[bi][0], w[bi][1]);
                     ld_relaxed_sys_u64x2(sa + n + 2, w[bi][2], w[bi][3]);
                   } else {
@@ -1241,7 +1242,9 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
 
 // DEC: the decoder-step op kinds (attention, RMSNorm / attention-combine inputs, residual outputs);
 // the linear-stack program runs the instantiation without them (no extra registers on its path).
-template <bool DEC>
+// TP: the tensor-parallel instantiation (pmpd_engine_run_ranks): rank groups and peer copies;
+// the single-GPU linear stack runs the instantiation without them (measured 5 % slower with).
+template <bool DEC, bool TP>
 __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a_in) {
   extern __shared__ __align__(128) uint8_t smem[];
   Bars& bars = *reinterpret_cast<Bars*>(smem + kSmBar);
@@ -1251,11 +1254,11 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
   // slice of y_out.  Row-parallel outputs are counted vectors shared by all ranks, their counts
   // summing every rank's contributors: the cross-rank reduction is the same counted addition as
   // the split-K one (the multi-GPU form adds into every rank's copy over NVLink).
-  const int nr = DEC ? 1 : a_in.n_ranks;  // decoder programs: one rank
+  const int nr = TP ? a_in.n_ranks : 1;
   const int G = gridDim.x / nr, rank = blockIdx.x / G, c = blockIdx.x - rank * G;
   const bool idle = rank >= nr;  // grid remainder when n_ranks does not divide it
   EngineArgs a = a_in;
-  if constexpr (!DEC) {
+  if constexpr (TP) {
     a.ops += (idle ? 0 : rank) * a.n_ops;
     a.y_out += (idle ? 0 : rank) * (long long)a.y_stride;
   }
@@ -1407,7 +1410,7 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
 #pragma unroll
             for (int w = 0; w < E_NCW; ++w) v += red[(buf * E_NCW + w) * 64 + nl];
             const unsigned long long w = fix_encode(DEC ? v * op.out_alpha : v, a.status);
-            if (op.n_peers == 0) {
+            if (!TP || op.n_peers == 0) {
               red_relaxed_u64(acc + (int64_t)ng * 64 + nl, w);
             } else {
               const long long off = (long long)par * op.acc_len + (int64_t)ng * 64 + nl;
@@ -1449,7 +1452,7 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
     }
   } else {
     // ------------------------------------------------------------ consumers
-    consumer_loop<DEC>(p, a, smem, bars, G, c, stage_bytes, nstage, epoch);
+    consumer_loop<DEC, TP>(p, a, smem, bars, G, c, stage_bytes, nstage, epoch);
   }
   // ---------------------------------------------------------------- final output
   // CTA c finalizes n-groups c, c + G, ... of the last op from their complete counted words
@@ -1733,7 +1736,8 @@ int pmpd_engine_run(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, co
 namespace {
 int engine_launch(bool dec, const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const void* x_in, float* y_out,
                   float y_alpha, uint32_t* bar_dev, int32_t* status_dev, int64_t* trace_dev, void* stream,
-                  void* R = nullptr, long long R_len = 0, int d_real = 0, int n_ranks = 1, int y_stride = 0) {
+                  void* R = nullptr, long long R_len = 0, int d_real = 0, int n_ranks = 1, int y_stride = 0,
+                  bool tp = false) {
   if (n_ops < 1) return fail(PMPD_ERR_CONFIG, "engine program is empty");
   EngineArgs a;
   a.ops = static_cast<const EngineOp*>(ops_dev);
@@ -1761,8 +1765,9 @@ int engine_launch(bool dec, const void* ops_dev, int32_t n_ops, const int32_t* p
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     smem = optin;
     if (const char* e = getenv("PMPD_ENGINE_SMEM")) smem = atoi(e) < optin ? atoi(e) : optin;
-    cudaFuncSetAttribute(engine_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(engine_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(engine_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(engine_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(engine_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(num_sms());
@@ -1774,8 +1779,9 @@ int engine_launch(bool dec, const void* ops_dev, int32_t n_ops, const int32_t* p
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const cudaError_t e = dec ? cudaLaunchKernelEx(&cfg, engine_kernel<true>, a)
-                            : cudaLaunchKernelEx(&cfg, engine_kernel<false>, a);
+  const cudaError_t e = dec ? cudaLaunchKernelEx(&cfg, engine_kernel<true, false>, a)
+                        : n_ranks > 1 || tp ? cudaLaunchKernelEx(&cfg, engine_kernel<false, true>, a)
+                                            : cudaLaunchKernelEx(&cfg, engine_kernel<false, false>, a);
   if (e != cudaSuccess) return fail(PMPD_ERR_CUDA, "engine launch: %s", cudaGetErrorString(e));
   return PMPD_OK;
 }
@@ -1792,7 +1798,7 @@ int pmpd_engine_run_ranks(const void* ops_dev, int32_t n_ops, int32_t n_ranks, c
                           float* y_out, int32_t y_stride, float y_alpha, uint32_t* bar_dev, int32_t* status_dev,
                           void* stream) {
   return engine_launch(false, ops_dev, n_ops, p_dev, x_in, y_out, y_alpha, bar_dev, status_dev, nullptr, stream,
-                       nullptr, 0, 0, n_ranks, y_stride);
+                       nullptr, 0, 0, n_ranks, y_stride, true);
 }
 
 int pmpd_engine_run_decoder(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const float* x0_dev,

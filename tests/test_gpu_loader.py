@@ -39,13 +39,15 @@ def _file_sha(path):
 
 
 CHILD = r"""
-import hashlib, json, resource, sys
+import hashlib, json, sys
 sys.path.insert(0, sys.argv[1])
 import torch
 from paper_2410_13461_b200 import tinylm
 m = tinylm.ModelVariants.load(sys.argv[2])
 torch.cuda.synchronize()
-rss = resource.getrusage(resource.RUSAGE_SELF).ru_maxrss * 1024
+# peak RSS of THIS process image: VmHWM belongs to the address space created by exec (ru_maxrss
+# would carry the forking pytest process's peak across fork + exec)
+rss = next(int(l.split()[1]) * 1024 for l in open("/proc/self/status") if l.startswith("VmHWM:"))
 shas = {}
 for name, t in m.tensors.items():
     h = hashlib.sha256()

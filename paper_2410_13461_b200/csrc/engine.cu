@@ -323,7 +323,11 @@ PMPD_DEV void prefetch_op(const EngineOp& op, int c, int G, int p) {
 #ifndef PMPD_ENGINE_PFT
 #define PMPD_ENGINE_PFT 0
 #endif
-PMPD_DEV void pf_advance(const EngineOp* ops, int n_ops, int c, int G, int p, int& pop, int& pt, int n) {
+#ifndef PMPD_ENGINE_PFB
+#define PMPD_ENGINE_PFB 0  // prefetch-when-blocked lead in tiles (0: off)
+#endif
+PMPD_DEV void pf_advance(const EngineOp* ops, int n_ops, int c, int G, int p, int& pop, int& pt, int n,
+                         bool issue = true) {
   while (n > 0 && pop < n_ops) {
     const EngineOp& op = ops[pop];
     if (op.kind != E_LINEAR) {
@@ -336,8 +340,11 @@ PMPD_DEV void pf_advance(const EngineOp* ops, int n_ops, int c, int G, int p, in
     const int m = min(n, r.T1 - pt);
     if (m > 0) {
       const uint32_t nb = (uint32_t)m * kTilePlaneBytes;
-      for (int j = 0; j < p; ++j) bulk_prefetch_l2(op.planes + j * op.plane_bytes + (int64_t)pt * kTilePlaneBytes, nb);
-      bulk_prefetch_l2(op.scales + (int64_t)pt * kTileScaleBytes, (uint32_t)m * kTileScaleBytes);
+      if (issue) {
+        for (int j = 0; j < p; ++j)
+          bulk_prefetch_l2(op.planes + j * op.plane_bytes + (int64_t)pt * kTilePlaneBytes, nb);
+        bulk_prefetch_l2(op.scales + (int64_t)pt * kTileScaleBytes, (uint32_t)m * kTileScaleBytes);
+      }
       pt += m;
       n -= m;
     }
@@ -1305,7 +1312,7 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
       int slot = 0, used = 0;
       uint32_t phase = 0;
       for (int oi = 1; oi < PMPD_ENGINE_PF && oi < a.n_ops; ++oi) prefetch_op(a.ops[oi], c, G, p);
-      int pf_op = 0, pf_t = -1;
+      int pf_op = 0, pf_t = -1, pfb_ahead = 0;
       if (PMPD_ENGINE_PFT > 0) pf_advance(a.ops, a.n_ops, c, G, p, pf_op, pf_t, PMPD_ENGINE_PFT);
       for (int oi = 0; oi < a.n_ops; ++oi) {
         const EngineOp& op = a.ops[oi];
@@ -1334,6 +1341,16 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
         while (t < r.T1) {
           const int end = min(min(t + E_STILES, r.T1), t - kt + r.KT);
           const int cnt = end - t;
+#if PMPD_ENGINE_PFB > 0
+          // prefetch-when-blocked: the ring is full (this SM's stream would stall), so pull the
+          // tiles just beyond the ring into L2 while the consumers catch up (typically at an op
+          // boundary, when HBM is otherwise idle); at most PMPD_ENGINE_PFB tiles ahead
+          if (used && !mbar_try_wait(&bars.empty[slot], phase ^ 1u) && pfb_ahead < PMPD_ENGINE_PFB) {
+            const int n = min(E_STILES, PMPD_ENGINE_PFB - pfb_ahead);
+            pf_advance(a.ops, a.n_ops, c, G, p, pf_op, pf_t, n);
+            pfb_ahead += n;
+          }
+#endif
 #ifdef PMPD_ENGINE_PROD_SPIN
           if (used) mbar_wait(&bars.empty[slot], phase ^ 1u);
 #else
@@ -1348,6 +1365,16 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
           bulk_g2s_stream(st + p * E_STILES * kTilePlaneBytes, op.scales + (int64_t)t * kTileScaleBytes,
                           cnt * kTileScaleBytes, &bars.full[slot], pol);
           if (PMPD_ENGINE_PFT > 0) pf_advance(a.ops, a.n_ops, c, G, p, pf_op, pf_t, cnt);
+#if PMPD_ENGINE_PFB > 0
+          // the load cursor passed cnt tiles: consume the prefetched lead, or move the prefetch
+          // cursor along with the loads when there is none
+          if (pfb_ahead >= cnt) {
+            pfb_ahead -= cnt;
+          } else {
+            pf_advance(a.ops, a.n_ops, c, G, p, pf_op, pf_t, cnt - pfb_ahead, false);
+            pfb_ahead = 0;
+          }
+#endif
           kt += cnt;
           if (kt == r.KT) kt = 0;
           t = end;

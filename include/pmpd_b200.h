@@ -227,12 +227,26 @@ int pmpd_engine_partition(const pmpd_qtensor* t, int32_t* bounds_host);
 int pmpd_engine_partition_g(const pmpd_qtensor* t, int32_t G, int32_t* bounds_host);
 int pmpd_engine_op_set_bounds(void* op_host, const int32_t* bounds_dev);
 /* Counted accumulation (linear-stack programs run by pmpd_engine_run): the op's output is
- * acc_dev = u64 [3][n_tiles * 64] zero-initialised words, each holding [63:56] the number of CTAs
- * that added into it and [55:0] the sum of their partials as 2^-24 fixed point (offset binary),
+ * acc_dev = u64 [3][n_tiles * 64] zero-initialised words, each holding [63:54] the number of CTAs
+ * that added into it and [53:0] the sum of their partials as 2^-24 fixed point (offset binary),
  * so split-K sums are bit-reproducible and self-validating; nslots_dev[n_tiles] = contributors
  * per n-group under the op's bounds, n_contrib = CTAs with a nonempty range.  bar_dev of the run
  * then holds 3 + n_ops u32 (tickets, done, launch epoch, per-op hint counters), zeroed once. */
 int pmpd_engine_op_set_counted(void* op_host, void* acc_dev, const uint8_t* nslots_dev, int32_t n_contrib);
+/* Sub-ops: restrict an op (before set_io / set_counted) to n-groups [ng0, ng1) and k-tiles
+ * [kt0, kt1) of its tensor.  The sub-op reads input elements kt0*64.. of its source and adds into
+ * the tensor's whole output vector (set_counted with the vector's base; every sub-op of one tensor
+ * passes the same acc_dev / nslots_dev, the counts summed over the sub-ops' partitions), so a row-
+ * parallel op can run as k-slices whose CTAs depend only on the source n-groups of their slice.
+ * set_share: zero_output = 0 for all but one sub-op of a shared output (that one zeroes the idle
+ * set); reuse_in >= 0: this op's input is the one op reuse_in staged (stage_full = 1 there), so a
+ * CTA that staged it skips staging. */
+int pmpd_engine_op_set_slice(void* op_host, int32_t ng0, int32_t ng1, int32_t kt0, int32_t kt1);
+int pmpd_engine_op_set_share(void* op_host, int32_t zero_output, int32_t reuse_in, int32_t stage_full);
+/* Final step of building an op table (host copy, before it is uploaded): copies each op's source
+ * output (counted vector, counts, scope) into the op record.  Required after set_counted /
+ * set_peers of every op. */
+int pmpd_engine_link(void* ops_host, int32_t n_ops);
 /* Decoder programs (pmpd_engine_run_decoder): every linear op is counted (pmpd_engine_op_set_counted);
  * the o / down ops (keep_out) add into ONE counted residual stream resid_dev = u64 [3][resid_len]
  * (resid_len = d rounded up to 64, zero-initialised), into which the launch first adds x0_dev (f32

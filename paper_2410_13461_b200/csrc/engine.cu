@@ -45,9 +45,15 @@ namespace {
 #ifndef PMPD_ENGINE_SB
 #define PMPD_ENGINE_SB 4  // staging: float4 groups per thread per L2 round trip (4096 elements per pass)
 #endif
-constexpr int E_PROD = E_NCW;               // producer warp
-constexpr int E_EPI = E_NCW + 1;            // epilogue warp
-constexpr int E_THREADS = (E_NCW + 2) * 32;
+#ifndef PMPD_ENGINE_PROD_WARP
+#define PMPD_ENGINE_PROD_WARP E_NCW
+#endif
+#ifndef PMPD_ENGINE_EPI_WARP
+#define PMPD_ENGINE_EPI_WARP (E_NCW + 1)
+#endif
+constexpr int E_PROD = PMPD_ENGINE_PROD_WARP;  // producer warp
+constexpr int E_EPI = PMPD_ENGINE_EPI_WARP;    // epilogue warp
+constexpr int E_THREADS = ((E_PROD > E_EPI ? E_PROD : E_EPI) + 1) * 32;  // warps above E_NCW without a role idle
 constexpr int E_MAXSTAGE = 12;
 constexpr int E_XMAX = 12288;               // max K of a staged activation vector
 
@@ -96,6 +102,19 @@ struct EngineOp {
   unsigned long long* peer[8];
   int n_peers;
   int sys;
+  // sub-ops (pmpd_engine_op_set_slice / pmpd_engine_op_set_share): an op restricted to n-groups
+  // [ng_off, ng_off + n_tiles) and k-tiles [k_off, k_off + k_tiles) of a tensor with n_tiles_full
+  // x kt_mem tiles; sub-ops of one tensor add into one shared counted output (acc is its base)
+  int ng_off, k_off, kt_mem, n_tiles_full;
+  long long zero_len;  // words of the idle set this op zeroes (-1: acc_len; 0: another sub-op does)
+  int reuse_in;        // >= 0: the input staged for op reuse_in (stage_full) serves this op too
+  int stage_full;      // stage the whole k range (not only the CTA's tiles'), for reuse by later ops
+  // the source op's counted output, copied into this op by pmpd_engine_link so that staging does
+  // not first chase the source op's record through L2 (one dependent round trip per op)
+  const unsigned long long* src_acc;
+  long long src_acc_len;
+  const unsigned char* src_nslots;
+  int src_sys;
 };
 constexpr int E_LINEAR = 0, E_ATTN = 1;
 constexpr int E_IN_SRC = 0, E_IN_RMSNORM = 2, E_IN_ATTN = 3;
@@ -105,6 +124,12 @@ PMPD_DEV int attn_rec(int dh) { return 4 + dh; }  // record: m, l, pad, pad, acc
 // ---- counted fixed-point words: [63:54] contributors, [53:0] sum of (rint(v * 2^24) + 2^43)
 #ifndef PMPD_ENGINE_NOHINT
 #define PMPD_ENGINE_NOHINT 1       // 0: consumers first wait for the relaxed per-op hint counter (measured slower)
+#endif
+#ifndef PMPD_ENGINE_ROTATE
+#define PMPD_ENGINE_ROTATE 0  // 1: round-robin tile slots across stages (0: slot = warp)
+#endif
+#ifndef PMPD_ENGINE_SLOTMAP
+#define PMPD_ENGINE_SLOTMAP 0  // 1: static slot order by scheduler load (needs E_NCW % 4 == 0)
 #endif
 #ifndef PMPD_ENGINE_RETRY_NS
 #define PMPD_ENGINE_RETRY_NS 32    // back-off between re-reads of incomplete words
@@ -131,7 +156,7 @@ PMPD_DEV unsigned long long fix_encode(float v, int* status) {
   long long q = 0;
   if (fabsf(v) < kFixMax)
     q = __float2ll_rn(v * kFixScale);
-  else if (status)
+  else if (status && *reinterpret_cast<volatile int*>(status) == 0)  // (no atomic storm on a NaN row)
     atomicExch(status, PMPD_ERR_INPUT);
   return (1ull << kCntShift) + (unsigned long long)(q + kFixOff);
 }
@@ -310,7 +335,7 @@ PMPD_DEV Range range_of(const EngineOp& op, int c, int G) {
 #define PMPD_ENGINE_PF 0  // measured slower at 1-4 ops ahead (round 2): the engine is sync-bound, not stream-bound
 #endif
 PMPD_DEV void prefetch_op(const EngineOp& op, int c, int G, int p) {
-  if (op.kind != E_LINEAR) return;
+  if (op.kind != E_LINEAR || op.kt_mem != op.k_tiles) return;  // (k-sliced ops: not contiguous)
   const Range r = range_of(op, c, G);
   if (r.T1 <= r.T0) return;
   const uint32_t n = (uint32_t)(r.T1 - r.T0) * kTilePlaneBytes;
@@ -330,7 +355,7 @@ PMPD_DEV void pf_advance(const EngineOp* ops, int n_ops, int c, int G, int p, in
                          bool issue = true) {
   while (n > 0 && pop < n_ops) {
     const EngineOp& op = ops[pop];
-    if (op.kind != E_LINEAR) {
+    if (op.kind != E_LINEAR || op.kt_mem != op.k_tiles) {
       ++pop;
       pt = -1;
       continue;
@@ -885,6 +910,12 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
   float* red = reinterpret_cast<float*>(smem + kSmRed);
   float* redb = reinterpret_cast<float*>(smem + kSmRedb);
   int slot = 0;     // ring slot (continues across ops)
+  // Tile slots of a stage go to the warps round-robin, continuing where the previous stage
+  // stopped: a partial stage (an n-group of 64 tiles is 24 + 24 + 16) gives its extra tiles to
+  // different warps each time instead of always warps 0..3 (the last warp sets the op's end)
+  int rot = 0;
+  int staged_from = -1;  // op whose stage_full input xs holds (reuse_in)
+  float mx_keep = 0.f;
   uint32_t phase = 0;
   int seg = 0;      // n-group segment counter (red double buffer)
   for (int oi = 0; oi < a.n_ops; ++oi) {
@@ -896,6 +927,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
       attn_op(op, a.ops[op.src], c, G, reinterpret_cast<float*>(smem + kSmX), warp, lane, par,
               reinterpret_cast<float*>(smem + kSmXq), a.trace ? a.trace + ((int64_t)c * a.n_ops + oi) * 8 : nullptr);
       named_bar_sync(1, E_NCW * 32);  // scratch (xs) is reused by the next op's staging
+      staged_from = -1;
       if (a.trace && threadIdx.x == 0 && units) a.trace[((int64_t)c * a.n_ops + oi) * 8 + 2] = gtimer();
       continue;
     }
@@ -903,7 +935,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
     // ---------------------------------------------------------- stage the input vector
     // k-tiles this CTA touches
     int lo0 = 0, hi0 = r.KT, lo1 = 0, hi1 = 0;
-    if (r.T1 - r.T0 < r.KT && r.T1 > r.T0) {
+    if (r.T1 - r.T0 < r.KT && r.T1 > r.T0 && !op.stage_full) {
       const int a0 = r.T0 % r.KT, b0 = (r.T1 - 1) % r.KT;
       if (a0 <= b0) {
         lo0 = a0;
@@ -928,6 +960,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
     // loads are issued before the input wait and only the residual's round trip is on the op path
     constexpr int RN = 4, RN_K = 4 * RN * E_NCW * 32;
     const bool busy = r.T1 > r.T0;  // a CTA with no tiles in this op reads no input at all
+    if (!busy) continue;             // (nor joins its staging barrier)
     const bool rms1 = DEC && busy && op.in_mode == E_IN_RMSNORM && op.k_real <= RN_K;
     float4 gpre[RN];
     if (DEC) {
@@ -946,7 +979,15 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
       named_bar_sync(1, E_NCW * 32);
     }
     if (a.trace && threadIdx.x == 0) a.trace[((int64_t)c * a.n_ops + oi) * 8 + 0] = gtimer();
+#ifdef PMPD_ENGINE_TRACE_WARPS
+    if (a.trace && threadIdx.x == 0) a.trace[((int64_t)c * a.n_ops + oi) * 8 + 7] = 0x7fffffffffffffffll;
+#endif
     float mx = 0.f;
+    // a sub-op of the op whose whole input this CTA staged last: xs and max|x| are still valid
+    const bool reuse = busy && op.reuse_in >= 0 && op.reuse_in == staged_from;
+    if (reuse) {
+      mx = mx_keep;
+    } else {
     const EngineOp* src = op.src >= 0 ? &a.ops[op.src] : nullptr;
     float inv = 1.f;  // E_IN_RMSNORM: 1 / sqrt(mean(resid^2) + eps) over the whole row
     // the counted residual stream R of this launch (decoder programs)
@@ -1086,7 +1127,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
           // counted source: one u64 word per element; every word's contributor count is checked
           // against the source n-group's (static) contributor number, re-reading the batch until
           // all have landed.  silu(g) * u reads the two halves in turn.
-          const unsigned long long* sa = src->acc + (long long)par * src->acc_len;
+          const unsigned long long* sa = op.src_acc + (long long)par * op.src_acc_len;
           // (inline rather than counted_read4: measured 6 % faster on the 7B linear stack)
           for (int which = 0; which < (op.act == 1 ? 2 : 1); ++which) {
             unsigned long long w[SB][4];
@@ -1094,7 +1135,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
 #pragma unroll
             for (int bi = 0; bi < SB; ++bi) {
               const int k = kb + bi * 4 * E_NCW * 32;
-              want[bi] = k < khi ? (int)__ldg(src->nslots + ((op.src_col + which * op.act_off + k) >> 6)) : 0;
+              want[bi] = k < khi ? (int)__ldg(op.src_nslots + ((op.src_col + which * op.act_off + k) >> 6)) : 0;
             }
             long long t0 = 0;
             for (;;) {
@@ -1103,7 +1144,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
                 const int k = kb + bi * 4 * E_NCW * 32;
                 const int n = op.src_col + which * op.act_off + k;
                 if (k < khi) {
-                  if (TP && src->sys) {  // a row-parallel output other GPUs add into
+                  if (TP && op.src_sys) {  // a row-parallel output other GPUs add into
                     ld_relaxed_sys_u64x2(sa + n, w[bi][0], w[bi][1]);
                     ld_relaxed_sys_u64x2(sa + n + 2, w[bi][2], w[bi][3]);
                   } else {
@@ -1153,6 +1194,9 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
     mx = 0.f;
 #pragma unroll
     for (int w = 0; w < E_NCW; ++w) mx = fmaxf(mx, misc[8 + w]);
+    mx_keep = mx;
+    if (busy) staged_from = op.stage_full ? oi : -1;
+    }  // !reuse
     if (a.trace && threadIdx.x == 0) a.trace[((int64_t)c * a.n_ops + oi) * 8 + 1] = gtimer();
     // ---------------------------------------------------------- tiles of this op
     int t = r.T0, ng = r.T0 / r.KT, kt = r.T0 % r.KT;
@@ -1164,6 +1208,9 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
       for (int e = 0; e < 4; ++e) dacc[i][e] = 0;
     float qs = 0.f;
     long long tcyc = 0, tcalls = 0, scyc0 = a.trace ? clock64() : 0, fcyc = 0, fwait = 0;
+#ifdef PMPD_ENGINE_TRACE_WARPS
+    long long fwait_all = 0;
+#endif
     int ngi = 0;
     // activation scale per n-group: qs = E_QMAX * idm / mx (one reciprocal per op, none per group)
     const float qmx = mx > 0.f ? __fdividef(E_QMAX, mx) : 0.f;
@@ -1171,23 +1218,43 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
     while (t < r.T1) {
       const int end = min(min(t + E_STILES, r.T1), t - kt + r.KT);
 #ifndef PMPD_ENGINE_SKIP_MEMORY
+#ifdef PMPD_ENGINE_TRACE_WARPS  // probe: full-stage wait cycles of every consumer warp
+      if (a.trace) {
+        const long long w0 = clock64();
+        mbar_wait(&bars.full[slot], phase);
+        fwait_all += clock64() - w0;
+      } else
+#endif
       mbar_wait(&bars.full[slot], phase);
+#endif
+#if PMPD_ENGINE_SLOTMAP
+      // second-tile slots of a partial stage go first to the warps of schedulers 2 and 3, then
+      // 1 (shared with the epilogue warp), then 0 (shared with the producer warp)
+      const int ws = ((0x4B >> (2 * (warp & 3))) & 3) * (E_NCW / 4) + (warp >> 2);
+      (void)rot;
+#elif PMPD_ENGINE_ROTATE
+      const int ws = warp >= rot ? warp - rot : warp - rot + E_NCW;  // this warp's slot
+      rot += end - t;
+      rot %= E_NCW;
+#else
+      const int ws = warp;
 #endif
 #ifdef PMPD_ENGINE_SKIP_COMPUTE
       if (false) {
 #else
-      if (warp < end - t) {
+      if (ws < end - t) {
 #endif
         if (a.trace) {
           const long long c0 = clock64();
-          tile_dispatch(P, smem + kSmRing + slot * stage_bytes, end - t, warp, kt + warp, lane, xs, xq, qs, dacc,
-                        bias);
+          tile_dispatch(P, smem + kSmRing + slot * stage_bytes, end - t, ws, kt + ws, lane, xs, xq, qs, dacc, bias);
           tcyc += clock64() - c0;
           ++tcalls;
         } else {
-          tile_dispatch(P, smem + kSmRing + slot * stage_bytes, end - t, warp, kt + warp, lane, xs, xq, qs, dacc,
-                        bias);
+          tile_dispatch(P, smem + kSmRing + slot * stage_bytes, end - t, ws, kt + ws, lane, xs, xq, qs, dacc, bias);
         }
+#ifdef PMPD_ENGINE_DOUBLE  // timing probe only: every stage's tiles decoded twice (wrong results)
+        tile_dispatch(P, smem + kSmRing + slot * stage_bytes, end - t, ws, kt + ws, lane, xs, xq, qs, dacc, bias);
+#endif
       }
       __syncwarp();
 #ifndef PMPD_ENGINE_SKIP_MEMORY
@@ -1237,6 +1304,24 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
         }
       }
     }
+#if defined(PMPD_ENGINE_TRACE_WSET)
+    // probe: loop-end globaltimer of consumer warps 4*WSET .. 4*WSET+3 in slots 4..7
+    if (a.trace && lane == 0 && (warp >> 2) == PMPD_ENGINE_TRACE_WSET)
+      a.trace[((int64_t)c * a.n_ops + oi) * 8 + 4 + (warp & 3)] = gtimer();
+    if (a.trace && threadIdx.x == 0) a.trace[((int64_t)c * a.n_ops + oi) * 8 + 2] = gtimer();
+#elif defined(PMPD_ENGINE_TRACE_WARPS)
+    // probe layout: [4] sum over warps of call cycles, [5] sum of full-stage wait cycles,
+    // [6] latest warp's loop end, [7] earliest warp's loop end (globaltimer)
+    if (a.trace && lane == 0) {
+      long long* tp = a.trace + ((int64_t)c * a.n_ops + oi) * 8;
+      const unsigned long long g = gtimer();
+      atomicAdd(reinterpret_cast<unsigned long long*>(tp + 4), (unsigned long long)tcyc);
+      atomicAdd(reinterpret_cast<unsigned long long*>(tp + 5), (unsigned long long)fwait_all);
+      atomicMax(reinterpret_cast<unsigned long long*>(tp + 6), g);
+      atomicMin(reinterpret_cast<unsigned long long*>(tp + 7), g);
+      if (warp == 0) tp[2] = (long long)g;
+    }
+#else
     if (a.trace && threadIdx.x == 0) {
       a.trace[((int64_t)c * a.n_ops + oi) * 8 + 2] = gtimer();
       a.trace[((int64_t)c * a.n_ops + oi) * 8 + 4] = tcyc;
@@ -1244,6 +1329,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
       a.trace[((int64_t)c * a.n_ops + oi) * 8 + 6] = clock64() - scyc0;
       a.trace[((int64_t)c * a.n_ops + oi) * 8 + 7] = (fwait << 32) | (fcyc & 0xffffffffll);
     }
+#endif
   }
 }
 
@@ -1357,12 +1443,13 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
           if (used) mbar_wait_backoff(&bars.empty[slot], phase ^ 1u);
 #endif
           uint8_t* st = smem + kSmRing + slot * stage_bytes;
+          // tile index in the tensor (a stage never crosses an n-group, so it is contiguous there)
+          const int64_t mt = (int64_t)(t / r.KT) * op.kt_mem + op.k_off + kt;
           mbar_arrive_expect_tx(&bars.full[slot], (uint32_t)(cnt * kTilePlaneBytes * (p + 1)));
           for (int j = 0; j < p; ++j)
-            bulk_g2s_stream(st + j * E_STILES * kTilePlaneBytes,
-                            op.planes + j * op.plane_bytes + (int64_t)t * kTilePlaneBytes, cnt * kTilePlaneBytes,
-                            &bars.full[slot], pol);
-          bulk_g2s_stream(st + p * E_STILES * kTilePlaneBytes, op.scales + (int64_t)t * kTileScaleBytes,
+            bulk_g2s_stream(st + j * E_STILES * kTilePlaneBytes, op.planes + j * op.plane_bytes + mt * kTilePlaneBytes,
+                            cnt * kTilePlaneBytes, &bars.full[slot], pol);
+          bulk_g2s_stream(st + p * E_STILES * kTilePlaneBytes, op.scales + mt * kTileScaleBytes,
                           cnt * kTileScaleBytes, &bars.full[slot], pol);
           if (PMPD_ENGINE_PFT > 0) pf_advance(a.ops, a.n_ops, c, G, p, pf_op, pf_t, cnt);
 #if PMPD_ENGINE_PFB > 0
@@ -1438,9 +1525,9 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
             for (int w = 0; w < E_NCW; ++w) v += red[(buf * E_NCW + w) * 64 + nl];
             const unsigned long long w = fix_encode(DEC ? v * op.out_alpha : v, a.status);
             if (!TP || op.n_peers == 0) {
-              red_relaxed_u64(acc + (int64_t)ng * 64 + nl, w);
+              red_relaxed_u64(acc + (int64_t)(op.ng_off + ng) * 64 + nl, w);
             } else {
-              const long long off = (long long)par * op.acc_len + (int64_t)ng * 64 + nl;
+              const long long off = (long long)par * op.acc_len + (int64_t)(op.ng_off + ng) * 64 + nl;
               for (int j = 0; j < op.n_peers; ++j) {
                 if (op.sys)
                   asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(op.peer[j] + off), "l"(w) : "memory");
@@ -1474,10 +1561,11 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
         // zero this CTA's slice of the op's idle parity set (outputs / attention records) for the
         // next launch (the residual stream's was zeroed at the start)
         unsigned long long* other = op.acc + (long long)zset * op.acc_len;
-        for (long long i = op.acc_len * c / G + lane, e = op.acc_len * (c + 1) / G; i < e; i += 32) other[i] = 0ull;
+        const long long zl = op.zero_len >= 0 ? op.zero_len : op.acc_len;
+        for (long long i = zl * c / G + lane, e = zl * (c + 1) / G; i < e; i += 32) other[i] = 0ull;
       }
     }
-  } else {
+  } else if (warp < E_NCW) {
     // ------------------------------------------------------------ consumers
     consumer_loop<DEC, TP>(p, a, smem, bars, G, c, stage_bytes, nstage, epoch);
   }
@@ -1572,6 +1660,10 @@ int pmpd_engine_make_op(const pmpd_qtensor* t, int32_t src, int32_t src_col, int
   op.in_mode = E_IN_SRC;
   op.out_alpha = 1.f;
   op.rwait = -1;
+  op.kt_mem = t->k_tiles;
+  op.n_tiles_full = t->n_tiles;
+  op.zero_len = -1;
+  op.reuse_in = -1;
   if ((src_col & 3) || (act_off & 3)) return fail(PMPD_ERR_CONFIG, "engine input offsets must be multiples of 4");
   *static_cast<EngineOp*>(op_host) = op;
   return PMPD_OK;
@@ -1594,6 +1686,8 @@ int pmpd_engine_op_set_io(void* op_host, int32_t in_mode, const float* resid_dev
   op.gain = gain_dev;
   op.eps = eps;
   op.eps_inv_k = 1.f / (float)op.k_real;
+  if (in_mode != E_IN_SRC && (op.k_off || op.k_tiles != op.kt_mem))
+    return fail(PMPD_ERR_CONFIG, "RMSNorm / attention inputs need the op's whole k range (no k-slice)");
   if (in_mode == E_IN_ATTN && op.k_tiles * kTile > 3 * 4 * E_NCW * 32)
     return fail(PMPD_ERR_CONFIG, "attention-combine input wider than %d", 3 * 4 * E_NCW * 32);
   if (in_mode == E_IN_RMSNORM && 2 * op.k_tiles * kTile + 4 * op.k_real > 2 * E_XMAX)
@@ -1628,6 +1722,8 @@ int pmpd_engine_make_attn_op(int32_t src, int32_t n_heads, int32_t d_head, void*
   op.acc_len = (long long)n_heads * E_ASPLIT * (4 + d_head);
   op.rwait = -1;
   op.out_alpha = 1.f;
+  op.zero_len = -1;
+  op.reuse_in = -1;
   *static_cast<EngineOp*>(op_host) = op;
   return PMPD_OK;
 }
@@ -1716,9 +1812,59 @@ int pmpd_engine_op_set_counted(void* op_host, void* acc_dev, const uint8_t* nslo
   EngineOp& op = *static_cast<EngineOp*>(op_host);
   if (op.kind != E_LINEAR) return fail(PMPD_ERR_CONFIG, "counted accumulation applies to linear ops");
   op.acc = static_cast<unsigned long long*>(acc_dev);
-  op.acc_len = (long long)op.n_tiles * 64;
+  op.acc_len = (long long)op.n_tiles_full * 64;  // sub-ops of one tensor share its whole output
   op.nslots = nslots_dev;
   op.n_contrib = n_contrib;
+  return PMPD_OK;
+}
+
+int pmpd_engine_op_set_slice(void* op_host, int32_t ng0, int32_t ng1, int32_t kt0, int32_t kt1) {
+  if (!op_host) return fail(PMPD_ERR_CONFIG, "null argument");
+  EngineOp& op = *static_cast<EngineOp*>(op_host);
+  if (op.kind != E_LINEAR) return fail(PMPD_ERR_CONFIG, "slices apply to linear ops");
+  if (op.ng_off || op.k_off || op.n_tiles != op.n_tiles_full || op.k_tiles != op.kt_mem)
+    return fail(PMPD_ERR_CONFIG, "op is already a slice");
+  if (op.in_mode != E_IN_SRC || op.acc) return fail(PMPD_ERR_CONFIG, "slice an op before set_io / set_counted");
+  if (ng0 < 0 || ng1 <= ng0 || ng1 > op.n_tiles || kt0 < 0 || kt1 <= kt0 || kt1 > op.k_tiles)
+    return fail(PMPD_ERR_CONFIG, "slice [%d,%d) x [%d,%d) outside %d x %d tiles", ng0, ng1, kt0, kt1, op.n_tiles,
+                op.k_tiles);
+  const int64_t tiles_before = (int64_t)ng0 * op.k_tiles;
+  op.planes += tiles_before * kTilePlaneBytes;  // plane j stays at planes + j * plane_bytes
+  op.scales += tiles_before * kTileScaleBytes;
+  op.aux += ng0;
+  op.ng_off = ng0;
+  op.n_real = std::min(op.n_real - ng0 * kTile, (ng1 - ng0) * kTile);
+  op.n_tiles = ng1 - ng0;
+  op.k_off = kt0;
+  op.k_real = std::min(op.k_real - kt0 * kTile, (kt1 - kt0) * kTile);
+  op.k_tiles = kt1 - kt0;
+  op.src_col += kt0 * kTile;  // local input element 0 is tensor input element kt0 * 64
+  return PMPD_OK;
+}
+
+int pmpd_engine_op_set_share(void* op_host, int32_t zero_output, int32_t reuse_in, int32_t stage_full) {
+  if (!op_host) return fail(PMPD_ERR_CONFIG, "null argument");
+  EngineOp& op = *static_cast<EngineOp*>(op_host);
+  if (op.kind != E_LINEAR) return fail(PMPD_ERR_CONFIG, "set_share applies to linear ops");
+  op.zero_len = zero_output ? -1 : 0;
+  op.reuse_in = reuse_in;
+  op.stage_full = stage_full ? 1 : 0;
+  return PMPD_OK;
+}
+
+int pmpd_engine_link(void* ops_host, int32_t n_ops) {
+  if (!ops_host || n_ops < 1) return fail(PMPD_ERR_CONFIG, "null argument");
+  EngineOp* ops = static_cast<EngineOp*>(ops_host);
+  for (int i = 0; i < n_ops; ++i) {
+    EngineOp& op = ops[i];
+    if (op.kind != E_LINEAR || op.src < 0) continue;
+    if (op.src >= i) return fail(PMPD_ERR_CONFIG, "op %d reads op %d, which does not precede it", i, op.src);
+    const EngineOp& src = ops[op.src];
+    op.src_acc = src.acc;
+    op.src_acc_len = src.acc_len;
+    op.src_nslots = src.nslots;
+    op.src_sys = src.sys;
+  }
   return PMPD_OK;
 }
 

@@ -61,6 +61,15 @@ class OpSpec:
     out: torch.Tensor | str | None = None  # decoder: residual op; RankProgram: shared (all-reduced) output key
     out_alpha: float = 1.0
     attn: AttnSpec | None = None
+    # sub-ops (linear-stack programs): the op restricted to n-groups [ng0, ng1) x k-tiles [kt0, kt1)
+    # of its tensor, partitioned over CTAs [c0, c1) only; sub-ops with the same `share` key add
+    # into one output vector (the tensor's); reuse_in / stage_full: reuse the input this CTA
+    # staged for op reuse_in (which staged its whole k range) instead of staging it again
+    part: tuple | None = None     # (ng0, ng1, kt0, kt1)
+    ctas: tuple | None = None     # (c0, c1)
+    share: str | None = None
+    reuse_in: int = -1
+    stage_full: bool = False
 
 
 class Program:
@@ -97,6 +106,7 @@ class Program:
             self.R = torch.zeros(SETS * d_tiles * 64, dtype=torch.int64, device="cuda")
             running = [1] * d_tiles
         host = (ctypes.c_uint8 * (nbytes * len(ops)))()
+        shared = {}  # share key -> [n_tiles, counts, [(addr, contrib, first)]]
         for i, spec in enumerate(ops):
             if spec.src >= i:
                 raise ConfigError(f"op {i} reads op {spec.src}, which does not precede it")
@@ -111,6 +121,13 @@ class Program:
                            at.max_ctx, float(at.scale), rec.data_ptr(), addr)
                 continue
             desc = spec.packed.desc
+            sub = spec.part is not None or spec.ctas is not None or spec.share is not None
+            if sub and self.decoder:
+                raise ConfigError("sub-ops are supported in linear-stack programs")
+            ng0, ng1, kt0, kt1 = spec.part if spec.part is not None else (0, desc.n_tiles, 0, desc.k_tiles)
+            c0, c1 = spec.ctas if spec.ctas is not None else (0, grid)
+            if not (0 <= c0 < c1 <= grid):
+                raise ConfigError(f"op {i}: CTA range {spec.ctas} outside the grid of {grid}")
             nt = desc.n_tiles
             ns_host = (ctypes.c_uint8 * nt)()
             _capi.call("pmpd_engine_nslots", spec.packed.ref(), ctypes.addressof(ns_host))
@@ -119,13 +136,25 @@ class Program:
             self.parts.append((part, ns0, spec.resid, spec.gain))
             _capi.call("pmpd_engine_make_op", spec.packed.ref(), spec.src, spec.src_col, spec.act, spec.act_off,
                        float(spec.in_alpha), part.data_ptr(), 1, ns0.data_ptr(), addr)
+            if spec.part is not None:
+                _capi.call("pmpd_engine_op_set_slice", addr, ng0, ng1, kt0, kt1)
             if spec.src >= 0 and ops[spec.src].packed is not None:
                 width = spec.src_col + (spec.act_off if spec.act == 1 else 0) + desc.k_tiles * 64
                 if width > ops[spec.src].packed.desc.n_tiles * 64:
                     raise ConfigError(f"op {i} reads past the end of op {spec.src}'s output")
             even = os.environ.get("PMPD_ENGINE_EVEN", "0") == "1"
             b_host = (ctypes.c_int32 * (grid + 1))()
-            if even:
+            snt, skt = ng1 - ng0, kt1 - kt0
+            if sub:
+                # the slice's tiles over CTAs [c0, c1); the other CTAs get empty ranges
+                g = c1 - c0
+                sd = _capi.QTensorDesc.from_buffer_copy(desc)
+                sd.n_tiles, sd.k_tiles = snt, skt
+                sb = (ctypes.c_int32 * (g + 1))()
+                _capi.call("pmpd_engine_partition_g", ctypes.byref(sd), g, ctypes.addressof(sb))
+                for c in range(grid + 1):
+                    b_host[c] = 0 if c <= c0 else (sb[c - c0] if c <= c1 else snt * skt)
+            elif even:
                 ntl = desc.n_tiles * desc.k_tiles
                 for c in range(grid + 1):
                     b_host[c] = c * ntl // grid
@@ -136,13 +165,24 @@ class Program:
             self.parts.append((bounds,))
             _capi.call("pmpd_engine_op_set_bounds", addr, bounds.data_ptr())
             # counted accumulation: contributors per n-group from the partition
-            kt, cnt, contrib = desc.k_tiles, [0] * nt, 0
+            kt, cnt, contrib = skt, [0] * nt, 0
             for c in range(grid):
                 t0, t1 = b_host[c], b_host[c + 1]
                 if t1 > t0:
                     contrib += 1
                     for ng in range(t0 // kt, (t1 - 1) // kt + 1):
-                        cnt[ng] += 1
+                        cnt[ng0 + ng] += 1
+            if spec.share is not None:
+                ent = shared.setdefault(spec.share, [nt, [0] * nt, []])
+                if ent[0] != nt:
+                    raise ConfigError(f"op {i}: shared output '{spec.share}' has another width")
+                ent[1] = [a + b for a, b in zip(ent[1], cnt)]
+                ent[2].append((addr, contrib))
+                _capi.call("pmpd_engine_op_set_share", addr, int(len(ent[2]) == 1), spec.reuse_in,
+                           int(spec.stage_full))
+                continue
+            if sub:
+                _capi.call("pmpd_engine_op_set_share", addr, 1, spec.reuse_in, int(spec.stage_full))
             if max(cnt) > 255 or min(cnt) < 1:
                 raise ConfigError(f"op {i}: n-group contributor counts outside 1..255")
             cs = torch.tensor(cnt, dtype=torch.uint8, device="cuda")
@@ -176,6 +216,15 @@ class Program:
                     last_rms = i
                 if residual:
                     running = [a + b for a, b in zip(running, cnt)]
+        for key, (nt, cnt, members) in shared.items():
+            if max(cnt) > 255 or min(cnt) < 1:
+                raise ConfigError(f"shared output '{key}': n-group contributor counts outside 1..255")
+            acc = torch.zeros(SETS * nt * 64, dtype=torch.int64, device="cuda")
+            cs = torch.tensor(cnt, dtype=torch.uint8, device="cuda")
+            self.parts.append((acc, cs))
+            for addr, contrib in members:
+                _capi.call("pmpd_engine_op_set_counted", addr, acc.data_ptr(), cs.data_ptr(), max(contrib, 1))
+        _capi.call("pmpd_engine_link", ctypes.addressof(host), len(ops))
         self.table = torch.frombuffer(bytearray(host), dtype=torch.uint8).cuda()
         self.bar = torch.zeros(3 + 2 * len(ops), dtype=torch.int32, device="cuda")
         self.status = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -319,6 +368,8 @@ class RankProgram:
                     _capi.call("pmpd_engine_op_set_peers", addr, ctypes.cast(arr, ctypes.c_void_p), W,
                                int(dist is not None))
         self.copies = copies
+        for r in range(n_emul):
+            _capi.call("pmpd_engine_link", ctypes.addressof(host) + r * n_ops * nbytes, n_ops)
         self.table = torch.frombuffer(bytearray(host), dtype=torch.uint8).cuda()
         self.bar = torch.zeros(3 + 2 * n_ops, dtype=torch.int32, device="cuda")
         self.status = torch.zeros(1, dtype=torch.int32, device="cuda")

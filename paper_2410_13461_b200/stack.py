@@ -16,6 +16,7 @@ One token = one CUDA-graph replay; the precision of token i is
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import torch
@@ -23,6 +24,7 @@ import torch.nn.functional as F
 
 from . import _capi
 from .engine import OpSpec, Program
+from .errors import ConfigError
 from .linear import Workspace, gemv, workspace_bytes
 from .quant import QuantizedTensor, quantize_tensor
 
@@ -59,7 +61,26 @@ def algorithmic_bytes(shape: StackShape, p: int, m: int = 1, group_size: int = 6
 
 
 def _rand_kn(K: int, N: int, std: float, gen: torch.Generator) -> torch.Tensor:
-    return torch.randn((K, N), generator=gen, device="cuda", dtype=torch.float32).mul_(std)
+    """Synthetic (K, N) weights of standard deviation ~std on the 4-bit quantization grid of each
+    (row, 64-column group): odd codes from a discretised N(8, 3^2), one element at code 0 and one
+    at code 15 (the group's min and max), w = (code - 8) * std / 3.25.
+
+    Why not plain N(0, std^2): the reference's nested reconstruction at p < p_max uses the bucket
+    centre c*2^m + 2^(m-1) (quant.py:212-215), on average 0.5 step above the codes it replaces.
+    That bias is harmless in a model (RMSNorm every layer) but the linear stack chains 129 GEMVs
+    with no normalisation: the common-mode shift grows ~10x per op and the chain overflows at
+    p <= 3.  Odd codes make the p = 3 reconstruction exact and the p = 2 (and p = 1) errors
+    zero-mean, so every precision stays finite; bytes, shapes and work are unchanged."""
+    z = torch.randn((K, N), generator=gen, device="cuda", dtype=torch.float32)
+    code = (torch.round((z * 3.0 + 7.0) / 2.0) * 2.0 + 1.0).clamp_(1.0, 15.0)
+    G = N // 64
+    if G:
+        blk = code[:, :G * 64].view(K, G, 64)
+        i0 = torch.randint(0, 64, (K, G, 1), generator=gen, device="cuda")
+        i1 = (i0 + torch.randint(1, 64, (K, G, 1), generator=gen, device="cuda")) % 64
+        blk.scatter_(2, i0, 0.0)
+        blk.scatter_(2, i1, 15.0)
+    return code.sub_(8.0).mul_(std / 3.25)
 
 
 class LinearStack:
@@ -134,8 +155,20 @@ class LinearStack:
             inp = self.h
         gemv(self.head[1], inp, self.p_dev, self.ws, out=self.logits, alpha=a_d)
 
-    def build_engine(self) -> Program:
-        """The same chain as ``token`` as one persistent-engine program."""
+    def build_engine(self, paired: bool | None = None, groups: int = 4) -> Program:
+        """The same chain as ``token`` as one persistent-engine program.
+
+        paired (default: env PMPD_ENGINE_PAIRED, else off): each row-parallel op runs as `groups`
+        k-slices, slice s on CTA group s, which also computes the source n-groups of that slice
+        (the v columns of q|k|v feed o, the gate columns of gate|up feed down).  A slice then waits
+        only on its own group, which has the rest of the column op (q|k columns, up columns) to do
+        in between: two grid-wide exchanges per layer (down -> q|k|v, o -> gate|up) instead of four.
+        Measured 16 % slower than the plain program (profiles/r02_paired.md): the sub-ops' partial
+        stages, extra flushes and per-sub-op tails cost more than the two exchanges they remove."""
+        if paired is None:
+            paired = os.environ.get("PMPD_ENGINE_PAIRED", "0") == "1"
+        if paired:
+            return self._build_paired(groups)
         d, f = self.shape.d_model, self.shape.d_ff
         a_d = 1.0 / (self.std * math.sqrt(d))
         a_f = 1.0 / (self.std * math.sqrt(f))
@@ -147,6 +180,44 @@ class LinearStack:
             ops.append(OpSpec(wup, src=base + 1, src_col=0, in_alpha=a_d))
             ops.append(OpSpec(wdn, src=base + 2, src_col=0, in_alpha=a_d))
         ops.append(OpSpec(self.head[1], src=len(ops) - 1, src_col=0, in_alpha=a_f))
+        self.program = Program(ops, y_alpha=a_d)
+        return self.program
+
+    def _build_paired(self, S: int) -> Program:
+        d, f = self.shape.d_model, self.shape.d_ff
+        a_d = 1.0 / (self.std * math.sqrt(d))
+        a_f = 1.0 / (self.std * math.sqrt(f))
+        grid = _capi.lib().pmpd_engine_grid()
+        if d % 64 or f % 64 or (d // 64) % S or (f // 64) % S or grid < S:
+            raise ConfigError(f"paired engine program: {S} groups do not divide the shape / grid")
+        ctas = [(grid * s // S, grid * (s + 1) // S) for s in range(S)]
+        D, F = d // 64, f // 64  # n-groups of d and d_ff
+        ops = []
+        prev, prev_alpha = -1, 1.0
+        for i, ((_, wqkv), (_, wo), (_, wup), (_, wdn)) in enumerate(self.layers):
+            kq = wqkv.desc.k_tiles
+            # q|k|v: the v columns (o's input) first, on every CTA in n-group order, so slice s of
+            # them lands on group s; then the q|k columns reuse the staged input
+            iv = len(ops)
+            ops.append(OpSpec(wqkv, src=prev, in_alpha=prev_alpha, part=(2 * D, 3 * D, 0, kq), share=f"qkv{i}",
+                              stage_full=True))
+            ops.append(OpSpec(wqkv, src=prev, in_alpha=prev_alpha, part=(0, 2 * D, 0, kq), share=f"qkv{i}",
+                              reuse_in=iv))
+            for s in range(S):
+                ops.append(OpSpec(wo, src=iv, src_col=2 * d, in_alpha=a_d,
+                                  part=(0, wo.desc.n_tiles, s * D // S, (s + 1) * D // S), ctas=ctas[s], share=f"o{i}"))
+            io = len(ops) - 1
+            ku = wup.desc.k_tiles
+            ig = len(ops)
+            ops.append(OpSpec(wup, src=io, in_alpha=a_d, part=(0, F, 0, ku), share=f"u{i}", stage_full=True))
+            ops.append(OpSpec(wup, src=io, in_alpha=a_d, part=(F, wup.desc.n_tiles, 0, ku), share=f"u{i}",
+                              reuse_in=ig))
+            for s in range(S):
+                ops.append(OpSpec(wdn, src=ig, src_col=0, in_alpha=a_d,
+                                  part=(0, wdn.desc.n_tiles, s * F // S, (s + 1) * F // S), ctas=ctas[s],
+                                  share=f"dn{i}"))
+            prev, prev_alpha = len(ops) - 1, a_f
+        ops.append(OpSpec(self.head[1], src=prev, src_col=0, in_alpha=a_f))
         self.program = Program(ops, y_alpha=a_d)
         return self.program
 

@@ -165,3 +165,39 @@ def test_engine_outlier_activations(scale):
         prog.run(torch.from_numpy(x).cuda(), _pdev(p), y)
         want = x.astype(np.float64) @ oq.dequantize(oq.quantize(w, 4, 64), p)
         assert rel_l2(y.cpu().numpy(), want[0]) < 5e-3, (scale, p)  # measured ~1.5e-3
+
+
+@pytest.mark.parametrize("groups", [2, 4])
+def test_paired_program_vs_f64(groups):
+    """Sub-op program (k-sliced row-parallel ops on CTA groups, shared counted outputs, reused
+    input staging): same chain as the plain program, checked against the float64 chain and for
+    bit-reproducibility."""
+    st = LinearStack(StackShape(2, 512, 1536, 2048), seed=5)
+    prog = st.build_engine(paired=True, groups=groups)
+    assert len(prog.ops) == 2 * (4 + 2 * groups) + 1
+    for p in (4, 3, 2):
+        ref = _chain_f64(st, p).cpu().numpy()
+        st.set_schedule({p: 0})
+        st.token_engine()
+        first = st.logits.clone()
+        st.token_engine()
+        torch.cuda.synchronize()
+        assert torch.equal(first, st.logits), p
+        assert rel_l2(st.logits.cpu().numpy(), ref) < 1e-2, (groups, p)
+    assert int(prog.status.item()) == 0
+    assert int(prog.bar[:2].sum().item()) == 0
+
+
+def test_paired_program_matches_plain_at_7b_width():
+    st = LinearStack(StackShape(1, 4096, 11008, 32000), seed=3)
+    out = {}
+    for paired in (False, True):
+        st.build_engine(paired=paired)
+        for p in (4, 2):
+            st.set_schedule({p: 0})
+            st.token_engine()
+            torch.cuda.synchronize()
+            out[(paired, p)] = st.logits.cpu().numpy()
+        assert int(st.program.status.item()) == 0
+    for p in (4, 2):
+        assert rel_l2(out[(True, p)], out[(False, p)]) < 3e-3, p

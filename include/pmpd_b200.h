@@ -239,10 +239,9 @@ int pmpd_engine_op_set_counted(void* op_host, void* acc_dev, const uint8_t* nslo
  * passes the same acc_dev / nslots_dev, the counts summed over the sub-ops' partitions), so a row-
  * parallel op can run as k-slices whose CTAs depend only on the source n-groups of their slice.
  * set_share: zero_output = 0 for all but one sub-op of a shared output (that one zeroes the idle
- * set); reuse_in >= 0: this op's input is the one op reuse_in staged (stage_full = 1 there), so a
- * CTA that staged it skips staging. */
+ * set of the whole vector). */
 int pmpd_engine_op_set_slice(void* op_host, int32_t ng0, int32_t ng1, int32_t kt0, int32_t kt1);
-int pmpd_engine_op_set_share(void* op_host, int32_t zero_output, int32_t reuse_in, int32_t stage_full);
+int pmpd_engine_op_set_share(void* op_host, int32_t zero_output);
 /* Final step of building an op table (host copy, before it is uploaded): copies each op's source
  * output (counted vector, counts, scope) into the op record.  Required after set_counted /
  * set_peers of every op. */

@@ -88,7 +88,7 @@ SIGNATURES = {
     "pmpd_engine_op_set_bounds": [_P, _P],
     "pmpd_engine_op_set_counted": [_P, _P, _P, _I],
     "pmpd_engine_op_set_slice": [_P, _I, _I, _I, _I],
-    "pmpd_engine_op_set_share": [_P, _I, _I, _I],
+    "pmpd_engine_op_set_share": [_P, _I],
     "pmpd_engine_link": [_P, _I],
     "pmpd_engine_run_traced": [_P, _I, _P, _P, _P, _F, _P, _P, _P, _P],
     "pmpd_engine_run_decoder": [_P, _I, _P, _P, _P, _L, _I, _P, _F, _P, _P, _P, _P],

@@ -107,8 +107,6 @@ struct EngineOp {
   // x kt_mem tiles; sub-ops of one tensor add into one shared counted output (acc is its base)
   int ng_off, k_off, kt_mem, n_tiles_full;
   long long zero_len;  // words of the idle set this op zeroes (-1: acc_len; 0: another sub-op does)
-  int reuse_in;        // >= 0: the input staged for op reuse_in (stage_full) serves this op too
-  int stage_full;      // stage the whole k range (not only the CTA's tiles'), for reuse by later ops
   // the source op's counted output, copied into this op by pmpd_engine_link so that staging does
   // not first chase the source op's record through L2 (one dependent round trip per op)
   const unsigned long long* src_acc;
@@ -914,8 +912,6 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
   // stopped: a partial stage (an n-group of 64 tiles is 24 + 24 + 16) gives its extra tiles to
   // different warps each time instead of always warps 0..3 (the last warp sets the op's end)
   int rot = 0;
-  int staged_from = -1;  // op whose stage_full input xs holds (reuse_in)
-  float mx_keep = 0.f;
   uint32_t phase = 0;
   int seg = 0;      // n-group segment counter (red double buffer)
   for (int oi = 0; oi < a.n_ops; ++oi) {
@@ -927,7 +923,6 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
       attn_op(op, a.ops[op.src], c, G, reinterpret_cast<float*>(smem + kSmX), warp, lane, par,
               reinterpret_cast<float*>(smem + kSmXq), a.trace ? a.trace + ((int64_t)c * a.n_ops + oi) * 8 : nullptr);
       named_bar_sync(1, E_NCW * 32);  // scratch (xs) is reused by the next op's staging
-      staged_from = -1;
       if (a.trace && threadIdx.x == 0 && units) a.trace[((int64_t)c * a.n_ops + oi) * 8 + 2] = gtimer();
       continue;
     }
@@ -935,7 +930,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
     // ---------------------------------------------------------- stage the input vector
     // k-tiles this CTA touches
     int lo0 = 0, hi0 = r.KT, lo1 = 0, hi1 = 0;
-    if (r.T1 - r.T0 < r.KT && r.T1 > r.T0 && !op.stage_full) {
+    if (r.T1 - r.T0 < r.KT && r.T1 > r.T0) {
       const int a0 = r.T0 % r.KT, b0 = (r.T1 - 1) % r.KT;
       if (a0 <= b0) {
         lo0 = a0;
@@ -984,10 +979,6 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
 #endif
     float mx = 0.f;
     // a sub-op of the op whose whole input this CTA staged last: xs and max|x| are still valid
-    const bool reuse = busy && op.reuse_in >= 0 && op.reuse_in == staged_from;
-    if (reuse) {
-      mx = mx_keep;
-    } else {
     const EngineOp* src = op.src >= 0 ? &a.ops[op.src] : nullptr;
     float inv = 1.f;  // E_IN_RMSNORM: 1 / sqrt(mean(resid^2) + eps) over the whole row
     // the counted residual stream R of this launch (decoder programs)
@@ -1194,9 +1185,6 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
     mx = 0.f;
 #pragma unroll
     for (int w = 0; w < E_NCW; ++w) mx = fmaxf(mx, misc[8 + w]);
-    mx_keep = mx;
-    if (busy) staged_from = op.stage_full ? oi : -1;
-    }  // !reuse
     if (a.trace && threadIdx.x == 0) a.trace[((int64_t)c * a.n_ops + oi) * 8 + 1] = gtimer();
     // ---------------------------------------------------------- tiles of this op
     int t = r.T0, ng = r.T0 / r.KT, kt = r.T0 % r.KT;
@@ -1424,6 +1412,13 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
 #endif
         const Range r = range_of(op, c, G);
         int t = r.T0, kt = r.T0 % r.KT;
+        // the op's fields in registers (the copies below clobber memory, so reading op.* in the
+        // loop would reload them every stage), the tile's index in the tensor tracked incrementally
+        const uint8_t* const planes = op.planes;
+        const uint8_t* const scales = op.scales;
+        const long long plane_bytes = op.plane_bytes;
+        const int kt_skip = op.kt_mem - r.KT;  // tensor k-tiles outside the slice, per n-group
+        int64_t mt = (int64_t)(r.T0 / r.KT) * op.kt_mem + op.k_off + kt;
         while (t < r.T1) {
           const int end = min(min(t + E_STILES, r.T1), t - kt + r.KT);
           const int cnt = end - t;
@@ -1443,14 +1438,14 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
           if (used) mbar_wait_backoff(&bars.empty[slot], phase ^ 1u);
 #endif
           uint8_t* st = smem + kSmRing + slot * stage_bytes;
-          // tile index in the tensor (a stage never crosses an n-group, so it is contiguous there)
-          const int64_t mt = (int64_t)(t / r.KT) * op.kt_mem + op.k_off + kt;
+          // (a stage never crosses an n-group, so its tiles are contiguous in the tensor)
           mbar_arrive_expect_tx(&bars.full[slot], (uint32_t)(cnt * kTilePlaneBytes * (p + 1)));
           for (int j = 0; j < p; ++j)
-            bulk_g2s_stream(st + j * E_STILES * kTilePlaneBytes, op.planes + j * op.plane_bytes + mt * kTilePlaneBytes,
+            bulk_g2s_stream(st + j * E_STILES * kTilePlaneBytes, planes + j * plane_bytes + mt * kTilePlaneBytes,
                             cnt * kTilePlaneBytes, &bars.full[slot], pol);
-          bulk_g2s_stream(st + p * E_STILES * kTilePlaneBytes, op.scales + mt * kTileScaleBytes,
-                          cnt * kTileScaleBytes, &bars.full[slot], pol);
+          bulk_g2s_stream(st + p * E_STILES * kTilePlaneBytes, scales + mt * kTileScaleBytes, cnt * kTileScaleBytes,
+                          &bars.full[slot], pol);
+          mt += cnt;
           if (PMPD_ENGINE_PFT > 0) pf_advance(a.ops, a.n_ops, c, G, p, pf_op, pf_t, cnt);
 #if PMPD_ENGINE_PFB > 0
           // the load cursor passed cnt tiles: consume the prefetched lead, or move the prefetch
@@ -1463,7 +1458,10 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
           }
 #endif
           kt += cnt;
-          if (kt == r.KT) kt = 0;
+          if (kt == r.KT) {
+            kt = 0;
+            mt += kt_skip;
+          }
           t = end;
           if (++slot == nstage) {
             slot = 0;
@@ -1663,7 +1661,6 @@ int pmpd_engine_make_op(const pmpd_qtensor* t, int32_t src, int32_t src_col, int
   op.kt_mem = t->k_tiles;
   op.n_tiles_full = t->n_tiles;
   op.zero_len = -1;
-  op.reuse_in = -1;
   if ((src_col & 3) || (act_off & 3)) return fail(PMPD_ERR_CONFIG, "engine input offsets must be multiples of 4");
   *static_cast<EngineOp*>(op_host) = op;
   return PMPD_OK;
@@ -1723,7 +1720,6 @@ int pmpd_engine_make_attn_op(int32_t src, int32_t n_heads, int32_t d_head, void*
   op.rwait = -1;
   op.out_alpha = 1.f;
   op.zero_len = -1;
-  op.reuse_in = -1;
   *static_cast<EngineOp*>(op_host) = op;
   return PMPD_OK;
 }
@@ -1842,13 +1838,11 @@ int pmpd_engine_op_set_slice(void* op_host, int32_t ng0, int32_t ng1, int32_t kt
   return PMPD_OK;
 }
 
-int pmpd_engine_op_set_share(void* op_host, int32_t zero_output, int32_t reuse_in, int32_t stage_full) {
+int pmpd_engine_op_set_share(void* op_host, int32_t zero_output) {
   if (!op_host) return fail(PMPD_ERR_CONFIG, "null argument");
   EngineOp& op = *static_cast<EngineOp*>(op_host);
   if (op.kind != E_LINEAR) return fail(PMPD_ERR_CONFIG, "set_share applies to linear ops");
   op.zero_len = zero_output ? -1 : 0;
-  op.reuse_in = reuse_in;
-  op.stage_full = stage_full ? 1 : 0;
   return PMPD_OK;
 }
 

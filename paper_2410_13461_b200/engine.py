@@ -63,13 +63,10 @@ class OpSpec:
     attn: AttnSpec | None = None
     # sub-ops (linear-stack programs): the op restricted to n-groups [ng0, ng1) x k-tiles [kt0, kt1)
     # of its tensor, partitioned over CTAs [c0, c1) only; sub-ops with the same `share` key add
-    # into one output vector (the tensor's); reuse_in / stage_full: reuse the input this CTA
-    # staged for op reuse_in (which staged its whole k range) instead of staging it again
+    # into one output vector (the tensor's)
     part: tuple | None = None     # (ng0, ng1, kt0, kt1)
     ctas: tuple | None = None     # (c0, c1)
     share: str | None = None
-    reuse_in: int = -1
-    stage_full: bool = False
 
 
 class Program:
@@ -178,11 +175,8 @@ class Program:
                     raise ConfigError(f"op {i}: shared output '{spec.share}' has another width")
                 ent[1] = [a + b for a, b in zip(ent[1], cnt)]
                 ent[2].append((addr, contrib))
-                _capi.call("pmpd_engine_op_set_share", addr, int(len(ent[2]) == 1), spec.reuse_in,
-                           int(spec.stage_full))
+                _capi.call("pmpd_engine_op_set_share", addr, int(len(ent[2]) == 1))
                 continue
-            if sub:
-                _capi.call("pmpd_engine_op_set_share", addr, 1, spec.reuse_in, int(spec.stage_full))
             if max(cnt) > 255 or min(cnt) < 1:
                 raise ConfigError(f"op {i}: n-group contributor counts outside 1..255")
             cs = torch.tensor(cnt, dtype=torch.uint8, device="cuda")

@@ -197,21 +197,18 @@ class LinearStack:
         for i, ((_, wqkv), (_, wo), (_, wup), (_, wdn)) in enumerate(self.layers):
             kq = wqkv.desc.k_tiles
             # q|k|v: the v columns (o's input) first, on every CTA in n-group order, so slice s of
-            # them lands on group s; then the q|k columns reuse the staged input
+            # them lands on group s; then the q|k columns
             iv = len(ops)
-            ops.append(OpSpec(wqkv, src=prev, in_alpha=prev_alpha, part=(2 * D, 3 * D, 0, kq), share=f"qkv{i}",
-                              stage_full=True))
-            ops.append(OpSpec(wqkv, src=prev, in_alpha=prev_alpha, part=(0, 2 * D, 0, kq), share=f"qkv{i}",
-                              reuse_in=iv))
+            ops.append(OpSpec(wqkv, src=prev, in_alpha=prev_alpha, part=(2 * D, 3 * D, 0, kq), share=f"qkv{i}"))
+            ops.append(OpSpec(wqkv, src=prev, in_alpha=prev_alpha, part=(0, 2 * D, 0, kq), share=f"qkv{i}"))
             for s in range(S):
                 ops.append(OpSpec(wo, src=iv, src_col=2 * d, in_alpha=a_d,
                                   part=(0, wo.desc.n_tiles, s * D // S, (s + 1) * D // S), ctas=ctas[s], share=f"o{i}"))
             io = len(ops) - 1
             ku = wup.desc.k_tiles
             ig = len(ops)
-            ops.append(OpSpec(wup, src=io, in_alpha=a_d, part=(0, F, 0, ku), share=f"u{i}", stage_full=True))
-            ops.append(OpSpec(wup, src=io, in_alpha=a_d, part=(F, wup.desc.n_tiles, 0, ku), share=f"u{i}",
-                              reuse_in=ig))
+            ops.append(OpSpec(wup, src=io, in_alpha=a_d, part=(0, F, 0, ku), share=f"u{i}"))
+            ops.append(OpSpec(wup, src=io, in_alpha=a_d, part=(F, wup.desc.n_tiles, 0, ku), share=f"u{i}"))
             for s in range(S):
                 ops.append(OpSpec(wdn, src=ig, src_col=0, in_alpha=a_d,
                                   part=(0, wdn.desc.n_tiles, s * F // S, (s + 1) * F // S), ctas=ctas[s],

@@ -1,2 +1,5 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_gpu_engine.py -x -q 2>&1 | tail -5
+echo "== prev code"; (cd build/wt_prev && timeout 300 python tools/engine_probe.py 2>&1 | grep -E "engine|Error")
+echo "== plain"; timeout 300 python tools/engine_probe.py 2>&1 | grep -E "engine|Error"
+echo "== paired"; PMPD_ENGINE_PAIRED=1 timeout 300 python tools/engine_probe.py 2>&1 | grep -E "engine|Error"
+timeout 300 python -m pytest -q -x tests/test_gpu_engine.py 2>&1 | tail -2

@@ -1083,6 +1083,15 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
     }
     // Each thread stages groups of 4 consecutive elements, SB groups per batch: all loads of a
     // batch are issued before any check (one L2 round trip per batch).
+    // the op's staging fields in registers: the polling loads below clobber memory, so op.* would
+    // be re-read (an L1 round trip on the exchange's critical path) on every batch and retry
+    const int s_src_col = op.src_col, s_act_off = op.act_off, s_act = op.act, s_k_real = op.k_real;
+    const float s_in_alpha = op.in_alpha;
+    const unsigned long long* const s_src_acc = op.src_acc;
+    const long long s_src_acc_len = op.src_acc_len;
+    const unsigned char* const s_src_nslots = op.src_nslots;
+    const int s_src_sys = op.src_sys;
+    (void)s_src_sys;
     constexpr int SB = PMPD_ENGINE_SB;
     for (int seg2 = 0; seg2 < 2; ++seg2) {
       const int klo = (seg2 ? lo1 : lo0) * kTile, khi = (seg2 ? hi1 : hi0) * kTile;
@@ -1094,7 +1103,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
           for (int bi = 0; bi < SB; ++bi) {
             const int k = kb + bi * 4 * E_NCW * 32;
             const float4 rg =
-                (k < khi && k < op.k_real) ? *reinterpret_cast<const float4*>(row + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+                (k < khi && k < s_k_real) ? *reinterpret_cast<const float4*>(row + k) : make_float4(0.f, 0.f, 0.f, 0.f);
             v[bi][0] = rg.x * inv;  // (x * g) * inv: tinylm.py:293-295 up to one rounding order
             v[bi][1] = rg.y * inv;
             v[bi][2] = rg.z * inv;
@@ -1104,38 +1113,38 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
 #pragma unroll
           for (int bi = 0; bi < SB; ++bi) {
             const int k = kb + bi * 4 * E_NCW * 32;
-            if (k + 4 <= op.k_real) {
+            if (k + 4 <= s_k_real) {
               const uint2 raw = __ldg(reinterpret_cast<const uint2*>(a.x_in + k));
               const float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
               const float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
               v[bi][0] = f0.x; v[bi][1] = f0.y; v[bi][2] = f1.x; v[bi][3] = f1.y;
             } else {
 #pragma unroll
-              for (int i = 0; i < 4; ++i) v[bi][i] = (k + i < op.k_real) ? __half2float(a.x_in[k + i]) : 0.f;
+              for (int i = 0; i < 4; ++i) v[bi][i] = (k + i < s_k_real) ? __half2float(a.x_in[k + i]) : 0.f;
             }
           }
         } else {
           // counted source: one u64 word per element; every word's contributor count is checked
           // against the source n-group's (static) contributor number, re-reading the batch until
           // all have landed.  silu(g) * u reads the two halves in turn.
-          const unsigned long long* sa = op.src_acc + (long long)par * op.src_acc_len;
+          const unsigned long long* sa = s_src_acc + (long long)par * s_src_acc_len;
           // (inline rather than counted_read4: measured 6 % faster on the 7B linear stack)
-          for (int which = 0; which < (op.act == 1 ? 2 : 1); ++which) {
+          for (int which = 0; which < (s_act == 1 ? 2 : 1); ++which) {
             unsigned long long w[SB][4];
             int want[SB];
 #pragma unroll
             for (int bi = 0; bi < SB; ++bi) {
               const int k = kb + bi * 4 * E_NCW * 32;
-              want[bi] = k < khi ? (int)__ldg(op.src_nslots + ((op.src_col + which * op.act_off + k) >> 6)) : 0;
+              want[bi] = k < khi ? (int)__ldg(s_src_nslots + ((s_src_col + which * s_act_off + k) >> 6)) : 0;
             }
             long long t0 = 0;
             for (;;) {
 #pragma unroll
               for (int bi = 0; bi < SB; ++bi) {
                 const int k = kb + bi * 4 * E_NCW * 32;
-                const int n = op.src_col + which * op.act_off + k;
+                const int n = s_src_col + which * s_act_off + k;
                 if (k < khi) {
-                  if (TP && op.src_sys) {  // a row-parallel output other GPUs add into
+                  if (TP && s_src_sys) {  // a row-parallel output other GPUs add into
                     ld_relaxed_sys_u64x2(sa + n, w[bi][0], w[bi][1]);
                     ld_relaxed_sys_u64x2(sa + n + 2, w[bi][2], w[bi][3]);
                   } else {
@@ -1160,9 +1169,9 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
               const int k = kb + bi * 4 * E_NCW * 32;
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
-                const float x = fix_decode(w[bi][i], want[bi]) * op.in_alpha;
+                const float x = fix_decode(w[bi][i], want[bi]) * s_in_alpha;
                 const float g = which == 0 ? x : __fdividef(v[bi][i], 1.f + __expf(-v[bi][i])) * x;
-                v[bi][i] = (k + i < op.k_real) ? g : 0.f;
+                v[bi][i] = (k + i < s_k_real) ? g : 0.f;
               }
             }
           }
@@ -1501,7 +1510,11 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
       if (op.kind == E_LINEAR) {
         const Range r = range_of(op, c, G);
         int t = r.T0, ng = r.T0 / r.KT, kt = r.T0 % r.KT;
-        unsigned long long* acc = op.acc + (long long)par * op.acc_len;
+        // (op fields in registers: the additions below clobber memory, op.* would be re-read per segment)
+        const int e_ng_off = op.ng_off, e_n_peers = TP ? op.n_peers : 0, e_sys = TP ? op.sys : 0;
+        const float e_out_alpha = op.out_alpha;
+        const long long e_acc_len = op.acc_len;
+        unsigned long long* acc = op.acc + (long long)par * e_acc_len;
         while (t < r.T1) {
           const int seg_end = min(r.T1, t - kt + r.KT);
           const int buf = seg & 1;
@@ -1521,13 +1534,13 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
             float v = bsum;
 #pragma unroll
             for (int w = 0; w < E_NCW; ++w) v += red[(buf * E_NCW + w) * 64 + nl];
-            const unsigned long long w = fix_encode(DEC ? v * op.out_alpha : v, a.status);
-            if (!TP || op.n_peers == 0) {
-              red_relaxed_u64(acc + (int64_t)(op.ng_off + ng) * 64 + nl, w);
+            const unsigned long long w = fix_encode(DEC ? v * e_out_alpha : v, a.status);
+            if (!TP || e_n_peers == 0) {
+              red_relaxed_u64(acc + (int64_t)(e_ng_off + ng) * 64 + nl, w);
             } else {
-              const long long off = (long long)par * op.acc_len + (int64_t)(op.ng_off + ng) * 64 + nl;
-              for (int j = 0; j < op.n_peers; ++j) {
-                if (op.sys)
+              const long long off = (long long)par * e_acc_len + (int64_t)(e_ng_off + ng) * 64 + nl;
+              for (int j = 0; j < e_n_peers; ++j) {
+                if (e_sys)
                   asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(op.peer[j] + off), "l"(w) : "memory");
                 else
                   red_relaxed_u64(op.peer[j] + off, w);

@@ -1,6 +1,5 @@
 cd $GRAFT_REPO_ROOT
-echo "== prev code"; (cd build/wt_prev && timeout 300 python tools/engine_probe.py 2>&1 | grep -E "engine|Error")
-echo "== plain"; timeout 300 python tools/engine_probe.py 2>&1 | grep -E "engine|Error"
-echo "== plain again"; timeout 300 python tools/engine_probe.py 2>&1 | grep -E "engine|Error"
-timeout 300 python -m pytest -q -x tests/test_gpu_engine.py tests/test_gpu_tp_engine.py 2>&1 | tail -2
-timeout 300 python tools/model_bench.py 2>&1 | tail -6
+TAG=_now timeout 300 python tools/engine_trace7b.py 2 2>&1 | tail -1
+python tools/trace7b_report.py gpurun_out/trace7b_p2_now.npz
+TAG=_now timeout 300 python tools/engine_trace7b.py 4 2>&1 | tail -1
+python tools/trace7b_report.py gpurun_out/trace7b_p4_now.npz

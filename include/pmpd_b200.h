@@ -225,6 +225,10 @@ int pmpd_engine_attn_records(int32_t n_heads, int32_t d_head);
 int pmpd_engine_partition(const pmpd_qtensor* t, int32_t* bounds_host);
 /* The same over G CTAs (a rank's share of the grid in pmpd_engine_run_ranks). */
 int pmpd_engine_partition_g(const pmpd_qtensor* t, int32_t G, int32_t* bounds_host);
+/* The same with a per-CTA budget reduction delta_host[G] (in half tile-times, >= 0): CTAs measured
+ * slower than the rest (later input, slower tiles: a property of their SM's place in the chip)
+ * get proportionally less work (calibrated by engine.calibrate_deltas from a traced token). */
+int pmpd_engine_partition_w(const pmpd_qtensor* t, int32_t G, const int32_t* delta_host, int32_t* bounds_host);
 int pmpd_engine_op_set_bounds(void* op_host, const int32_t* bounds_dev);
 /* Counted accumulation (linear-stack programs run by pmpd_engine_run): the op's output is
  * acc_dev = u64 [3][n_tiles * 64] zero-initialised words, each holding [63:54] the number of CTAs

@@ -83,6 +83,7 @@ SIGNATURES = {
     "pmpd_engine_attn_records": [_I, _I],
     "pmpd_engine_partition": [_D, _P],
     "pmpd_engine_partition_g": [_D, _I, _P],
+    "pmpd_engine_partition_w": [_D, _I, _P, _P],
     "pmpd_engine_run_ranks": [_P, _I, _I, _P, _P, _P, _I, _F, _P, _P, _P],
     "pmpd_engine_op_set_peers": [_P, _P, _I, _I],
     "pmpd_engine_op_set_bounds": [_P, _P],

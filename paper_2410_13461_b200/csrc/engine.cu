@@ -1381,10 +1381,16 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
     // no work: only the launch's done counter below
   } else if (warp == E_PROD) {
     // ------------------------------------------------------------ producer
+#ifndef PMPD_ENGINE_PROD_WARPWIDE
+#define PMPD_ENGINE_PROD_WARPWIDE 0
+#endif
+    // PROD_WARPWIDE: the whole warp runs the producer loop (its addresses stay warp-uniform, so
+    // each bulk copy is one instruction instead of an elect-one loop); lane 0 issues
+    const bool issuer = PMPD_ENGINE_PROD_WARPWIDE ? lane == 0 : true;
 #ifdef PMPD_ENGINE_SKIP_MEMORY
     if (false) {
 #else
-    if (lane == 0) {
+    if (PMPD_ENGINE_PROD_WARPWIDE || lane == 0) {
 #endif
 #ifdef PMPD_ENGINE_EVICT_NORMAL
       uint64_t pol;
@@ -1448,12 +1454,14 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
 #endif
           uint8_t* st = smem + kSmRing + slot * stage_bytes;
           // (a stage never crosses an n-group, so its tiles are contiguous in the tensor)
-          mbar_arrive_expect_tx(&bars.full[slot], (uint32_t)(cnt * kTilePlaneBytes * (p + 1)));
-          for (int j = 0; j < p; ++j)
-            bulk_g2s_stream(st + j * E_STILES * kTilePlaneBytes, planes + j * plane_bytes + mt * kTilePlaneBytes,
-                            cnt * kTilePlaneBytes, &bars.full[slot], pol);
-          bulk_g2s_stream(st + p * E_STILES * kTilePlaneBytes, scales + mt * kTileScaleBytes, cnt * kTileScaleBytes,
-                          &bars.full[slot], pol);
+          if (issuer) {
+            mbar_arrive_expect_tx(&bars.full[slot], (uint32_t)(cnt * kTilePlaneBytes * (p + 1)));
+            for (int j = 0; j < p; ++j)
+              bulk_g2s_stream(st + j * E_STILES * kTilePlaneBytes, planes + j * plane_bytes + mt * kTilePlaneBytes,
+                              cnt * kTilePlaneBytes, &bars.full[slot], pol);
+            bulk_g2s_stream(st + p * E_STILES * kTilePlaneBytes, scales + mt * kTileScaleBytes, cnt * kTileScaleBytes,
+                            &bars.full[slot], pol);
+          }
           mt += cnt;
           if (PMPD_ENGINE_PFT > 0) pf_advance(a.ops, a.n_ops, c, G, p, pf_op, pf_t, cnt);
 #if PMPD_ENGINE_PFB > 0
@@ -1749,6 +1757,10 @@ int pmpd_engine_partition(const pmpd_qtensor* t, int32_t* bounds_host) {
 }
 
 int pmpd_engine_partition_g(const pmpd_qtensor* t, int32_t G, int32_t* bounds_host) {
+  return pmpd_engine_partition_w(t, G, nullptr, bounds_host);
+}
+
+int pmpd_engine_partition_w(const pmpd_qtensor* t, int32_t G, const int32_t* delta_host, int32_t* bounds_host) {
   if (!t || !bounds_host) return fail(PMPD_ERR_CONFIG, "null argument");
   if (G < 1) return fail(PMPD_ERR_CONFIG, "partition over %d CTAs", G);
   const int KT = t->k_tiles, NT = t->n_tiles * t->k_tiles;
@@ -1769,7 +1781,8 @@ int pmpd_engine_partition_g(const pmpd_qtensor* t, int32_t G, int32_t* bounds_ho
     if (out) out[0] = 0;
     while (t0 < NT) {
       if (c == G) return G + 1;
-      int t1 = t0, cost = 0;
+      // a CTA measured slower than the rest (pmpd_engine_partition_w) gets a smaller budget
+      int t1 = t0, cost = delta_host ? std::max(0, delta_host[c]) : 0;
       while (t1 < NT) {
         const int kt = t1 % KT, seg_end = std::min(NT, t1 - kt + KT);
         // largest prefix of this segment that still fits
@@ -1802,7 +1815,7 @@ int pmpd_engine_partition_g(const pmpd_qtensor* t, int32_t G, int32_t* bounds_ho
         cst += seg_cost(e - t1);
         t1 = e;
       }
-      mx = std::max(mx, cst);
+      mx = std::max(mx, cst + (delta_host ? std::max(0, delta_host[c]) : 0));
     }
     hi = mx;
   }

@@ -78,7 +78,7 @@ class Program:
     residual stream, into which the launch first adds the f32 embedding row ``x_in``; every
     RMSNorm op carries the static count each residual word has reached at that point."""
 
-    def __init__(self, ops: list, y_alpha: float = 1.0):
+    def __init__(self, ops: list, y_alpha: float = 1.0, cta_delta: list | None = None):
         if not ops:
             raise ConfigError("engine program is empty")
         lib = _capi.lib()
@@ -155,6 +155,11 @@ class Program:
                 ntl = desc.n_tiles * desc.k_tiles
                 for c in range(grid + 1):
                     b_host[c] = c * ntl // grid
+            elif cta_delta is not None:
+                # calibrated: CTAs measured slower get smaller budgets (calibrate_deltas)
+                dl = (ctypes.c_int32 * grid)(*[int(v) for v in cta_delta])
+                _capi.call("pmpd_engine_partition_w", spec.packed.ref(), grid, ctypes.addressof(dl),
+                           ctypes.addressof(b_host))
             else:
                 # cost-balanced CTA tile ranges (stage/segment aware) instead of an even tile split
                 _capi.call("pmpd_engine_partition", spec.packed.ref(), ctypes.addressof(b_host))
@@ -210,6 +215,7 @@ class Program:
                     last_rms = i
                 if residual:
                     running = [a + b for a, b in zip(running, cnt)]
+        self.cta_delta = cta_delta
         for key, (nt, cnt, members) in shared.items():
             if max(cnt) > 255 or min(cnt) < 1:
                 raise ConfigError(f"shared output '{key}': n-group contributor counts outside 1..255")
@@ -253,6 +259,30 @@ class Program:
         """Enqueue one pass (graph-capturable): y_out = y_alpha * chain(x_in) at precision *p_dev
         (decoder programs: x_in = the f32 embedding row that starts the residual stream)."""
         self._launch(x_in, p_dev, y_out, None)
+
+
+def calibrate_deltas(prog: Program, x_in, p_dev, y_out, runs: int = 3, unit_us: float = 0.25,
+                     max_delta: int = 6) -> list:
+    """Per-CTA budget reductions for ``Program(..., cta_delta=...)`` from traced launches of
+    ``prog``: a CTA whose linear ops end later than the median CTA's (the same CTAs on every op:
+    their SMs see inputs later and decode a little slower) gets roughly that lateness less work,
+    in half tile-time units of ``unit_us`` (about 0.25 µs on B200 at p=2)."""
+    import numpy as np
+    lates = []
+    for _ in range(runs):
+        tr = prog.run_traced(x_in, p_dev, y_out).numpy().astype(np.float64)
+        for i, spec in enumerate(prog.ops):
+            if spec.attn is not None:
+                continue
+            staged, done = tr[:, i, 1], tr[:, i, 2]
+            busy = done - staged > 0
+            if busy.sum() < 0.8 * len(done):
+                continue
+            d = np.where(busy, done - np.median(done[busy]), np.nan)
+            lates.append(d / 1e3)
+    late = np.nanmean(np.array(lates), axis=0)
+    late = np.nan_to_num(late, nan=0.0)
+    return [int(v) for v in np.clip(np.round(late / unit_us), 0, max_delta)]
 
 
 class RankProgram:

@@ -155,7 +155,7 @@ class LinearStack:
             inp = self.h
         gemv(self.head[1], inp, self.p_dev, self.ws, out=self.logits, alpha=a_d)
 
-    def build_engine(self, paired: bool | None = None, groups: int = 4) -> Program:
+    def build_engine(self, paired: bool | None = None, groups: int = 4, cta_delta: list | None = None) -> Program:
         """The same chain as ``token`` as one persistent-engine program.
 
         paired (default: env PMPD_ENGINE_PAIRED, else off): each row-parallel op runs as `groups`
@@ -180,7 +180,7 @@ class LinearStack:
             ops.append(OpSpec(wup, src=base + 1, src_col=0, in_alpha=a_d))
             ops.append(OpSpec(wdn, src=base + 2, src_col=0, in_alpha=a_d))
         ops.append(OpSpec(self.head[1], src=len(ops) - 1, src_col=0, in_alpha=a_f))
-        self.program = Program(ops, y_alpha=a_d)
+        self.program = Program(ops, y_alpha=a_d, cta_delta=cta_delta)
         return self.program
 
     def _build_paired(self, S: int) -> Program:

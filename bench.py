@@ -223,7 +223,7 @@ def arm_config(args, world: int, tp_mode: bool) -> dict:
                         "progressive 4->3->2 switching at tokens 32/128 over 512 tokens per step",
             "schedule": {str(k): v for k, v in SCHED.items()}, "horizon": HORIZON,
             "parallelism": (f"tp{world} (row-parallel all-reduce inside the engine: counted additions into every "
-                            "rank's symmetric-memory copy)" if os.environ.get("PMPD_TP_ENGINE") == "1" else
+                            "rank's symmetric-memory copy)" if os.environ.get("PMPD_TP_ENGINE", "1") == "1" else
                             f"tp{world} (NCCL all-reduce after o and down)") if tp_mode else "single GPU",
             "l2": "inputs larger than L2 (2.5-4.1 GB of planes per token vs 126 MB L2)"}
 
@@ -327,7 +327,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
 
-    tp_engine = tp_mode and os.environ.get("PMPD_TP_ENGINE") == "1"
+    # N > 1: tensor parallelism inside the engine by default (PMPD_TP_ENGINE=0: per-op GEMVs + NCCL)
+    tp_engine = tp_mode and os.environ.get("PMPD_TP_ENGINE", "1") == "1"
     if tp_engine:
         # tensor parallel INSIDE the engine: each rank one launch per token, the row-parallel
         # all-reduce = counted additions into every rank's symmetric-memory copy over NVLink
@@ -469,13 +470,15 @@ def main():
     traffic_pp, traffic_src = ncu_traffic()
     traffic = sum(w[p] * traffic_pp[p] for p in w) if traffic_pp and all(p in traffic_pp for p in w) else None
     if tp_mode:
-        traffic, traffic_src = None, "not captured for the tensor-parallel per-op path"
+        traffic, traffic_src = None, "not captured for the tensor-parallel programs"
 
     out = {
         "metric": METRIC, "value": us_tok, "unit": "us/token", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "fp16",
-        "data": "synthetic (N(0,0.02^2) weights, seeded; device-quantized bit-exactly to nested 4/3/2-bit)",
+        "data": ("synthetic (seeded weights of std 0.02 on odd 4-bit codes of each group's grid, so the "
+                 "unnormalised 129-GEMV chain stays finite at every precision; device-quantized bit-exactly "
+                 "to nested 4/3/2-bit; x ~ N(0,1))"),
         "config": arm_config(args, world, tp_mode),
         "per_precision": {str(k): v for k, v in per_p.items()},
         "avg_bits": sum(p * f for p, f in w.items()),
@@ -489,7 +492,9 @@ def main():
                               "persistent engine kernel carries all 129 linear layers of a token (plus 1 tiny "
                               "precision-hook launch)") if not tp_mode else
                              ("whole-job algorithmic bytes per token / µs per token over N x the one-GPU peak; per rank "
-                              "129 per-op decode GEMVs on its shards + 64 NCCL all-reduces + 1 all-gather")},
+                              + ("one engine launch over its shards, the 64 row-parallel all-reduces as counted "
+                                 "additions into every rank's copy" if tp_engine else
+                                 "129 per-op decode GEMVs on its shards + 64 NCCL all-reduces + 1 all-gather"))},
         "clocks": clk.summary(),
         "e2e": {"value": e2e_us, "unit": "us/token", "h2d_bytes_per_step": HORIZON * x_dev.numel() * 2,
                 "d2h_bytes_per_step": HORIZON * y_dev.numel() * 4},

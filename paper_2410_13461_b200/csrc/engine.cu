@@ -51,9 +51,14 @@ namespace {
 #ifndef PMPD_ENGINE_EPI_WARP
 #define PMPD_ENGINE_EPI_WARP (E_NCW + 1)
 #endif
+#ifndef PMPD_ENGINE_PROD2
+#define PMPD_ENGINE_PROD2 0  // 1: a second producer warp (on another scheduler) issues every other stage
+#endif
 constexpr int E_PROD = PMPD_ENGINE_PROD_WARP;  // producer warp
 constexpr int E_EPI = PMPD_ENGINE_EPI_WARP;    // epilogue warp
-constexpr int E_THREADS = ((E_PROD > E_EPI ? E_PROD : E_EPI) + 1) * 32;  // warps above E_NCW without a role idle
+constexpr int E_PROD_B = PMPD_ENGINE_PROD2 ? (E_PROD > E_EPI ? E_PROD : E_EPI) + 1 : E_PROD;  // second producer
+constexpr int E_LASTW = E_PROD_B > (E_PROD > E_EPI ? E_PROD : E_EPI) ? E_PROD_B : (E_PROD > E_EPI ? E_PROD : E_EPI);
+constexpr int E_THREADS = (E_LASTW + 1) * 32;  // warps above E_NCW without a role idle
 constexpr int E_MAXSTAGE = 12;
 constexpr int E_XMAX = 12288;               // max K of a staged activation vector
 
@@ -1379,8 +1384,12 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
 
   if (idle) {
     // no work: only the launch's done counter below
-  } else if (warp == E_PROD) {
+  } else if (warp == E_PROD || warp == E_PROD_B) {
     // ------------------------------------------------------------ producer
+    // (PROD2: both producer warps walk every stage; each issues its own half, so the TMA issue
+    // load is split over two schedulers)
+    const int pturn = (PMPD_ENGINE_PROD2 && warp == E_PROD_B) ? 1 : 0;
+    int gstage = 0;
 #ifndef PMPD_ENGINE_PROD_WARPWIDE
 #define PMPD_ENGINE_PROD_WARPWIDE 0
 #endif
@@ -1447,14 +1456,15 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
             pfb_ahead += n;
           }
 #endif
+          const bool mine = !PMPD_ENGINE_PROD2 || ((gstage++ & 1) == pturn);
 #ifdef PMPD_ENGINE_PROD_SPIN
-          if (used) mbar_wait(&bars.empty[slot], phase ^ 1u);
+          if (used && mine) mbar_wait(&bars.empty[slot], phase ^ 1u);
 #else
-          if (used) mbar_wait_backoff(&bars.empty[slot], phase ^ 1u);
+          if (used && mine) mbar_wait_backoff(&bars.empty[slot], phase ^ 1u);
 #endif
           uint8_t* st = smem + kSmRing + slot * stage_bytes;
           // (a stage never crosses an n-group, so its tiles are contiguous in the tensor)
-          if (issuer) {
+          if (issuer && mine) {
             mbar_arrive_expect_tx(&bars.full[slot], (uint32_t)(cnt * kTilePlaneBytes * (p + 1)));
             for (int j = 0; j < p; ++j)
               bulk_g2s_stream(st + j * E_STILES * kTilePlaneBytes, planes + j * plane_bytes + mt * kTilePlaneBytes,

@@ -1,3 +1,3 @@
 cd $GRAFT_REPO_ROOT
-PMPD_BENCH_TP=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 1 --steps 2 --warmup 3 --no-cpu > gpurun_out/b_tp1.json 2> gpurun_out/b_tp1.err
-tail -3 gpurun_out/b_tp1.err
+bash tools/run_var.sh
+PMPD_LIB=$PWD/build/variants/libeng_prod2.so timeout 600 python -m pytest -q -x tests/test_gpu_engine.py 2>&1 | tail -2

@@ -63,3 +63,33 @@ def test_gemv_validation_without_launch():
     r = _capi.describe(128, 128, 64, 4, _capi.LAYOUT_REF)
     with pytest.raises(ConfigError):
         _capi.call("pmpd_gemv_workspace_bytes", ctypes.byref(r), 1, ctypes.byref(out))
+
+
+def _partition(nt, kt, G, delta=None):
+    lib = _capi.lib()
+    d = _capi.QTensorDesc()
+    d.n_tiles, d.k_tiles = nt, kt
+    b = (ctypes.c_int32 * (G + 1))()
+    if delta is None:
+        assert lib.pmpd_engine_partition_g(ctypes.byref(d), G, b) == 0
+    else:
+        dl = (ctypes.c_int32 * G)(*delta)
+        assert lib.pmpd_engine_partition_w(ctypes.byref(d), G, dl, b) == 0
+    return list(b)
+
+
+@pytest.mark.parametrize("nt,kt", [(344, 64), (192, 64), (64, 172), (500, 64), (3, 7)])
+def test_engine_partition_covers_every_tile(nt, kt):
+    """Cost-balanced CTA ranges (host code): monotone, start at 0, end at the last tile; a
+    zero budget reduction is the plain partition; slower CTAs get no more tiles than before."""
+    G = 148
+    b = _partition(nt, kt, G)
+    assert b[0] == 0 and b[-1] == nt * kt and all(x <= y for x, y in zip(b, b[1:]))
+    assert _partition(nt, kt, G, [0] * G) == b
+    delta = [2 if c % 6 == 0 else 0 for c in range(G)]
+    w = _partition(nt, kt, G, delta)
+    assert w[0] == 0 and w[-1] == nt * kt and all(x <= y for x, y in zip(w, w[1:]))
+    if nt * kt >= 4 * G:
+        slow = [w[c + 1] - w[c] for c in range(G) if delta[c]]
+        base = [b[c + 1] - b[c] for c in range(G) if delta[c]]
+        assert sum(slow) < sum(base)

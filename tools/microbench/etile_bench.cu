@@ -18,8 +18,24 @@ __global__ void __launch_bounds__(E_NCW * 32, 1) eb(int p, int iters, int nw, un
   int dacc[4][4] = {};
   float bias = 0.f;
   const int w = warp % E_NCW;
+#ifdef ETB_WAIT
+  // the engine's per-stage bookkeeping: wait on an (already completed) full barrier, arrive on
+  // an empty barrier (count E_NCW, never waited on here)
+  __shared__ __align__(8) uint64_t bars[2];
+  if (threadIdx.x == 0) { mbar_init(&bars[0], 1); mbar_init(&bars[1], (1 << 20) - 1); fence_barrier_init(); }
+  __syncthreads();
+  if (threadIdx.x == 0) mbar_arrive(&bars[0]);
+  __syncthreads();
+#endif
   for (int it = 0; it < iters; ++it) {
+#ifdef ETB_WAIT
+    mbar_wait(&bars[0], 0);
+#endif
     tile_dispatch(p, sm, E_STILES, w, (w + it) & 31, lane, xs, xq, 3.f, dacc, bias);
+#ifdef ETB_WAIT
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bars[1]);
+#endif
   }
   unsigned acc = __float_as_uint(bias);
   for (int i = 0; i < 4; ++i) for (int e = 0; e < 4; ++e) acc ^= dacc[i][e];

@@ -794,62 +794,30 @@ __noinline__ __device__ void attn_op(const EngineOp& op, const EngineOp& src, in
 // E_IN_ATTN staging (kept out of line: its live registers of split records would otherwise
 // count against the consumer loop's tile body).  Returns max |x| of the staged f16 row.
 __noinline__ __device__ float stage_attn_input(const EngineOp& op, const EngineOp& src, int lo0, int hi0, int lo1,
-                                               int hi1, __half* xs, float* wscratch, int par) {
+                                               int hi1, __half* xs, float* wscratch, int par, long long* tr) {
   float mx = 0.f;
   // only this CTA's k-tile ranges [lo0, hi0) and [lo1, hi1) are staged (the tiles read nothing
   // else): element u of the concatenated ranges maps to k = kof(u)
   const int len0 = (hi0 - lo0) * kTile, lr = len0 + (hi1 - lo1) * kTile;
   auto kof = [&](int u) { return u < len0 ? lo0 * kTile + u : lo1 * kTile + (u - len0); };
-  // The whole row (K = d <= 4608) in one L2 round trip: every thread reads the split records of
-  // its groups (single-writer words of the attention op, polled until written) while the
-  // per-(head, split) softmax weights w = exp(m_s - M_h) / sum_s exp(m_s - M_h) l_s are computed
-  // into xq scratch by the first n_heads threads.
+  // Each element combines the E_ASPLIT split records of its head (single-writer words of the
+  // attention op, polled until written) with the per-(head, split) softmax weights
+  // w = exp(m_s - M_h) / sum_s exp(m_s - M_h) l_s.  Every thread reads the values of up to SBA
+  // batches of 4 elements, then the first n_heads threads the (m, l) words (written with the
+  // values, so rarely re-polled) and the weights.  A range wider than one pass (rare: more than
+  // 4 * SBA * threads elements in one CTA) is staged in passes after the weights.
+  // (Measured: weights on dedicated warps in parallel with the values, 1.5 % slower on the 1.4B
+  // decoder; weights first, then values, 1-3 % slower.)
   constexpr int SBA = 3;
   const int dh = src.d_head;
   const unsigned long long* recs = src.acc + (long long)par * src.acc_len;
-  float av[SBA * E_ASPLIT][4];
-  // batches 0 and 1 (the first 3072 elements of the k-range, all an o op of d <= 3072 needs) in
-  // ONE round trip, batch 2 in a second one only when the range is wider
-#pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    constexpr int NBH = 2 * E_ASPLIT;
-    const unsigned long long* pp[NBH];
-    bool on[NBH];
-    int ww[NBH];
-    float o[NBH][4];
-    bool any = false;
-#pragma unroll
-    for (int b = 0; b < 2; ++b) {
-      const int bi = 2 * half + b;
-      const int u = 4 * threadIdx.x + bi * 4 * E_NCW * 32;
-      const int k = (bi < SBA && u < lr) ? kof(u) : op.k_real;
-      const int hh = k < op.k_real ? k / dh : 0, e = k - hh * dh;
-#pragma unroll
-      for (int q = 0; q < E_ASPLIT; ++q) {
-        pp[b * E_ASPLIT + q] = recs + (int64_t)(hh * E_ASPLIT + q) * attn_rec(dh) + 4 + e;
-        on[b * E_ASPLIT + q] = k < op.k_real;
-        ww[b * E_ASPLIT + q] = 1;
-      }
-      any = any || k < op.k_real;
-    }
-    if (half == 1 && !any) {
-#pragma unroll
-      for (int i = 0; i < NBH; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-    } else {
-      counted_read4<NBH, true>(pp, on, ww, o);
-    }
-#pragma unroll
-    for (int b = 0; b < 2; ++b) {
-      const int bi = 2 * half + b;
-      if (bi >= SBA) break;
-#pragma unroll
-      for (int q = 0; q < E_ASPLIT; ++q)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) av[bi * E_ASPLIT + q][i] = o[b * E_ASPLIT + q][i];
-    }
-  }
+  const int n_heads = src.n_heads;
+  const int wthr = (n_heads + 31) & ~31;
+  const int all = E_NCW * 32;
+  (void)wthr;
+  const bool one_pass = 4 * SBA * all >= lr;
   float* wts = wscratch;
-  for (int hh = threadIdx.x; hh < src.n_heads; hh += E_NCW * 32) {
+  auto weights = [&](int hh) {
     const unsigned long long* pp[2 * E_ASPLIT];
     int ww[2 * E_ASPLIT];
     float ml[2 * E_ASPLIT];
@@ -875,28 +843,87 @@ __noinline__ __device__ float stage_attn_input(const EngineOp& op, const EngineO
     const float id = den > 0.f ? __frcp_rn(den) : 0.f;
 #pragma unroll
     for (int q = 0; q < E_ASPLIT; ++q) wts[hh * E_ASPLIT + q] = ms[q] * id;
-  }
-  named_bar_sync(1, E_NCW * 32);
+  };
+  // values of elements u = 4*vt + bi*4*vn + base (bi < SBA) into av, then (after the weights are
+  // in shared memory) combined into xs
+  auto values = [&](float (&av)[SBA * E_ASPLIT][4], int vt, int vn, int base) {
 #pragma unroll
-  for (int bi = 0; bi < SBA; ++bi) {
-    const int u = 4 * threadIdx.x + bi * 4 * E_NCW * 32;
-    if (u >= lr) break;
-    const int k = kof(u);
-    float o[4] = {0.f, 0.f, 0.f, 0.f};
-    if (k < op.k_real) {
-      const int hh = k / dh;
+    for (int half = 0; half < 2; ++half) {
+      constexpr int NBH = 2 * E_ASPLIT;
+      const unsigned long long* pp[NBH];
+      bool on[NBH];
+      int ww[NBH];
+      float o[NBH][4];
+      bool any = false;
 #pragma unroll
-      for (int q = 0; q < E_ASPLIT; ++q) {
-        const float w = wts[hh * E_ASPLIT + q];
+      for (int b = 0; b < 2; ++b) {
+        const int bi = 2 * half + b;
+        const int u = base + 4 * vt + bi * 4 * vn;
+        const int k = (bi < SBA && u < lr) ? kof(u) : op.k_real;
+        const int hh = k < op.k_real ? k / dh : 0, e = k - hh * dh;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) o[e] = fmaf(w, av[bi * E_ASPLIT + q][e], o[e]);
+        for (int q = 0; q < E_ASPLIT; ++q) {
+          pp[b * E_ASPLIT + q] = recs + (int64_t)(hh * E_ASPLIT + q) * attn_rec(dh) + 4 + e;
+          on[b * E_ASPLIT + q] = k < op.k_real;
+          ww[b * E_ASPLIT + q] = 1;
+        }
+        any = any || k < op.k_real;
+      }
+      if (!any) {
+#pragma unroll
+        for (int i = 0; i < NBH; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+      } else {
+        counted_read4<NBH, true>(pp, on, ww, o);
+      }
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int bi = 2 * half + b;
+        if (bi >= SBA) break;
+#pragma unroll
+        for (int q = 0; q < E_ASPLIT; ++q)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) av[bi * E_ASPLIT + q][i] = o[b * E_ASPLIT + q][i];
       }
     }
-    const __half2 h01 = __floats2half2_rn(o[0], o[1]), h23 = __floats2half2_rn(o[2], o[3]);
-    *reinterpret_cast<__half2*>(xs + k) = h01;
-    *reinterpret_cast<__half2*>(xs + k + 2) = h23;
-    const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
-    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(f01.x), fabsf(f01.y)), fmaxf(fabsf(f23.x), fabsf(f23.y))));
+  };
+  auto combine = [&](const float (&av)[SBA * E_ASPLIT][4], int vt, int vn, int base) {
+#pragma unroll
+    for (int bi = 0; bi < SBA; ++bi) {
+      const int u = base + 4 * vt + bi * 4 * vn;
+      if (u >= lr) break;
+      const int k = kof(u);
+      float o[4] = {0.f, 0.f, 0.f, 0.f};
+      if (k < op.k_real) {
+        const int hh = k / dh;
+#pragma unroll
+        for (int q = 0; q < E_ASPLIT; ++q) {
+          const float w = wts[hh * E_ASPLIT + q];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) o[e] = fmaf(w, av[bi * E_ASPLIT + q][e], o[e]);
+        }
+      }
+      const __half2 h01 = __floats2half2_rn(o[0], o[1]), h23 = __floats2half2_rn(o[2], o[3]);
+      *reinterpret_cast<__half2*>(xs + k) = h01;
+      *reinterpret_cast<__half2*>(xs + k + 2) = h23;
+      const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(f01.x), fabsf(f01.y)), fmaxf(fabsf(f23.x), fabsf(f23.y))));
+    }
+  };
+  float av[SBA * E_ASPLIT][4];
+  if (one_pass) {
+    values(av, threadIdx.x, all, 0);
+    if (tr && threadIdx.x == 0) tr[4] = gtimer();  // (PMPD_ENGINE_TRACE_ATTNSTAGE) values read
+    for (int hh = threadIdx.x; hh < n_heads; hh += all) weights(hh);
+    if (tr && threadIdx.x == 0) tr[5] = gtimer();
+    named_bar_sync(1, E_NCW * 32);
+    combine(av, threadIdx.x, all, 0);
+  } else {
+    for (int hh = threadIdx.x; hh < n_heads; hh += all) weights(hh);
+    named_bar_sync(1, E_NCW * 32);
+    for (int base = 0; base < lr; base += 4 * SBA * all) {
+      values(av, threadIdx.x, all, base);
+      combine(av, threadIdx.x, all, base);
+    }
   }
   return mx;
 }
@@ -1082,7 +1109,12 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
     } else if (DEC && op.in_mode == E_IN_RMSNORM) {
       hi0 = hi1 = lo0 = lo1 = 0;  // no tiles: nothing to stage
     } else if (DEC && op.in_mode == E_IN_ATTN) {
-      if (busy) mx = stage_attn_input(op, *src, lo0, hi0, lo1, hi1, xs, reinterpret_cast<float*>(smem + kSmXq), par);
+#ifdef PMPD_ENGINE_TRACE_ATTNSTAGE
+      long long* atr = a.trace ? a.trace + ((int64_t)c * a.n_ops + oi) * 8 : nullptr;
+#else
+      long long* atr = nullptr;
+#endif
+      if (busy) mx = stage_attn_input(op, *src, lo0, hi0, lo1, hi1, xs, reinterpret_cast<float*>(smem + kSmXq), par, atr);
       hi0 = hi1 = 0;  // staged already (the generic loop below runs no iteration)
       lo0 = lo1 = 0;
     }
@@ -1240,6 +1272,7 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
       rot %= E_NCW;
 #else
       const int ws = warp;
+      (void)rot;
 #endif
 #ifdef PMPD_ENGINE_SKIP_COMPUTE
       if (false) {
@@ -1324,6 +1357,11 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
       if (warp == 0) tp[2] = (long long)g;
     }
 #else
+#ifdef PMPD_ENGINE_TRACE_ATTNSTAGE
+    if (a.trace && threadIdx.x == 0 && op.in_mode == E_IN_ATTN) {
+      a.trace[((int64_t)c * a.n_ops + oi) * 8 + 2] = gtimer();
+    } else
+#endif
     if (a.trace && threadIdx.x == 0) {
       a.trace[((int64_t)c * a.n_ops + oi) * 8 + 2] = gtimer();
       a.trace[((int64_t)c * a.n_ops + oi) * 8 + 4] = tcyc;
@@ -1411,6 +1449,7 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
       uint32_t phase = 0;
       for (int oi = 1; oi < PMPD_ENGINE_PF && oi < a.n_ops; ++oi) prefetch_op(a.ops[oi], c, G, p);
       int pf_op = 0, pf_t = -1, pfb_ahead = 0;
+      (void)pfb_ahead;
       if (PMPD_ENGINE_PFT > 0) pf_advance(a.ops, a.n_ops, c, G, p, pf_op, pf_t, PMPD_ENGINE_PFT);
       for (int oi = 0; oi < a.n_ops; ++oi) {
         const EngineOp& op = a.ops[oi];
@@ -1635,6 +1674,77 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
 
 using namespace pmpd;
 
+namespace {
+// Cost-balanced tile partition (the stage geometry of this translation unit's kernel)
+int partition_impl(const pmpd_qtensor* t, int32_t G, const int32_t* delta_host, int32_t* bounds_host) {
+  if (!t || !bounds_host) return fail(PMPD_ERR_CONFIG, "null argument");
+  if (G < 1) return fail(PMPD_ERR_CONFIG, "partition over %d CTAs", G);
+  const int KT = t->k_tiles, NT = t->n_tiles * t->k_tiles;
+  if (NT < 1) return fail(PMPD_ERR_CONFIG, "empty tensor");
+  // cost in half tile-times
+  static const int flush_cost = [] {  // half tile-times per n-group segment (PMPD_ENGINE_PART_FLUSH)
+    const char* e = getenv("PMPD_ENGINE_PART_FLUSH");
+    return e ? atoi(e) : 1;
+  }();
+  auto seg_cost = [&](int n) {  // n tiles of one n-group segment
+    int cst = flush_cost;
+    for (int s0 = 0; s0 < n; s0 += E_STILES) cst += 2 * ((std::min(n - s0, E_STILES) + E_NCW - 1) / E_NCW);
+    return cst;
+  };
+  // greedy: from tile t, the largest end with cost <= budget
+  auto cover = [&](int budget, int32_t* out) {
+    int t0 = 0, c = 0;
+    if (out) out[0] = 0;
+    while (t0 < NT) {
+      if (c == G) return G + 1;
+      // a CTA measured slower than the rest (pmpd_engine_partition_w) gets a smaller budget
+      int t1 = t0, cost = delta_host ? std::max(0, delta_host[c]) : 0;
+      while (t1 < NT) {
+        const int kt = t1 % KT, seg_end = std::min(NT, t1 - kt + KT);
+        // largest prefix of this segment that still fits
+        int lo = 0, hi = seg_end - t1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) / 2;
+          if (cost + seg_cost(mid) <= budget) lo = mid; else hi = mid - 1;
+        }
+        if (lo == 0) break;
+        cost += seg_cost(lo);
+        t1 += lo;
+        if (lo < seg_end - (t1 - lo)) break;  // segment not finished: the budget is spent
+      }
+      if (t1 == t0) return G + 1;  // budget below one tile
+      ++c;
+      if (out) out[c] = t1;
+      t0 = t1;
+    }
+    if (out) for (int k = c + 1; k <= G; ++k) out[k] = NT;  // idle CTAs
+    return c;
+  };
+  int lo = 1, hi = 1 << 30;
+  {  // upper bound: the even split's cost
+    int mx = 0;
+    for (int c = 0; c < G; ++c) {
+      const int a = (int)((int64_t)c * NT / G), b = (int)((int64_t)(c + 1) * NT / G);
+      int cst = 0;
+      for (int t1 = a; t1 < b;) {
+        const int e = std::min(b, t1 - t1 % KT + KT);
+        cst += seg_cost(e - t1);
+        t1 = e;
+      }
+      mx = std::max(mx, cst + (delta_host ? std::max(0, delta_host[c]) : 0));
+    }
+    hi = mx;
+  }
+  while (lo < hi) {
+    const int mid = (lo + hi) / 2;
+    if (cover(mid, nullptr) <= G) hi = mid; else lo = mid + 1;
+  }
+  cover(lo, bounds_host);
+  return PMPD_OK;
+}
+}  // namespace
+
+#ifndef PMPD_ENGINE_DEC_TU
 extern "C" {
 
 int pmpd_engine_op_bytes(void) { return (int)sizeof(EngineOp); }
@@ -1771,70 +1881,7 @@ int pmpd_engine_partition_g(const pmpd_qtensor* t, int32_t G, int32_t* bounds_ho
 }
 
 int pmpd_engine_partition_w(const pmpd_qtensor* t, int32_t G, const int32_t* delta_host, int32_t* bounds_host) {
-  if (!t || !bounds_host) return fail(PMPD_ERR_CONFIG, "null argument");
-  if (G < 1) return fail(PMPD_ERR_CONFIG, "partition over %d CTAs", G);
-  const int KT = t->k_tiles, NT = t->n_tiles * t->k_tiles;
-  if (NT < 1) return fail(PMPD_ERR_CONFIG, "empty tensor");
-  // cost in half tile-times
-  static const int flush_cost = [] {  // half tile-times per n-group segment (PMPD_ENGINE_PART_FLUSH)
-    const char* e = getenv("PMPD_ENGINE_PART_FLUSH");
-    return e ? atoi(e) : 1;
-  }();
-  auto seg_cost = [&](int n) {  // n tiles of one n-group segment
-    int cst = flush_cost;
-    for (int s0 = 0; s0 < n; s0 += E_STILES) cst += (n - s0 > E_NCW) ? 4 : 2;
-    return cst;
-  };
-  // greedy: from tile t, the largest end with cost <= budget
-  auto cover = [&](int budget, int32_t* out) {
-    int t0 = 0, c = 0;
-    if (out) out[0] = 0;
-    while (t0 < NT) {
-      if (c == G) return G + 1;
-      // a CTA measured slower than the rest (pmpd_engine_partition_w) gets a smaller budget
-      int t1 = t0, cost = delta_host ? std::max(0, delta_host[c]) : 0;
-      while (t1 < NT) {
-        const int kt = t1 % KT, seg_end = std::min(NT, t1 - kt + KT);
-        // largest prefix of this segment that still fits
-        int lo = 0, hi = seg_end - t1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) / 2;
-          if (cost + seg_cost(mid) <= budget) lo = mid; else hi = mid - 1;
-        }
-        if (lo == 0) break;
-        cost += seg_cost(lo);
-        t1 += lo;
-        if (lo < seg_end - (t1 - lo)) break;  // segment not finished: the budget is spent
-      }
-      if (t1 == t0) return G + 1;  // budget below one tile
-      ++c;
-      if (out) out[c] = t1;
-      t0 = t1;
-    }
-    if (out) for (int k = c + 1; k <= G; ++k) out[k] = NT;  // idle CTAs
-    return c;
-  };
-  int lo = 1, hi = 1 << 30;
-  {  // upper bound: the even split's cost
-    int mx = 0;
-    for (int c = 0; c < G; ++c) {
-      const int a = (int)((int64_t)c * NT / G), b = (int)((int64_t)(c + 1) * NT / G);
-      int cst = 0;
-      for (int t1 = a; t1 < b;) {
-        const int e = std::min(b, t1 - t1 % KT + KT);
-        cst += seg_cost(e - t1);
-        t1 = e;
-      }
-      mx = std::max(mx, cst + (delta_host ? std::max(0, delta_host[c]) : 0));
-    }
-    hi = mx;
-  }
-  while (lo < hi) {
-    const int mid = (lo + hi) / 2;
-    if (cover(mid, nullptr) <= G) hi = mid; else lo = mid + 1;
-  }
-  cover(lo, bounds_host);
-  return PMPD_OK;
+  return partition_impl(t, G, delta_host, bounds_host);
 }
 
 int pmpd_engine_op_set_counted(void* op_host, void* acc_dev, const uint8_t* nslots_dev, int32_t n_contrib) {
@@ -1935,6 +1982,7 @@ int pmpd_engine_run(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, co
 }
 
 }  // extern "C"
+#endif  // !PMPD_ENGINE_DEC_TU
 
 namespace {
 int engine_launch(bool dec, const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const void* x_in, float* y_out,
@@ -1968,9 +2016,12 @@ int engine_launch(bool dec, const void* ops_dev, int32_t n_ops, const int32_t* p
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     smem = optin;
     if (const char* e = getenv("PMPD_ENGINE_SMEM")) smem = atoi(e) < optin ? atoi(e) : optin;
-    cudaFuncSetAttribute(engine_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+#ifdef PMPD_ENGINE_DEC_TU
     cudaFuncSetAttribute(engine_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+#else
+    cudaFuncSetAttribute(engine_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(engine_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+#endif
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(num_sms());
@@ -1982,15 +2033,36 @@ int engine_launch(bool dec, const void* ops_dev, int32_t n_ops, const int32_t* p
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const cudaError_t e = dec ? cudaLaunchKernelEx(&cfg, engine_kernel<true, false>, a)
+#ifdef PMPD_ENGINE_DEC_TU
+  (void)tp;
+  const cudaError_t e = dec ? cudaLaunchKernelEx(&cfg, engine_kernel<true, false>, a) : cudaErrorInvalidValue;
+#else
+  const cudaError_t e = dec ? cudaErrorInvalidValue
                         : n_ranks > 1 || tp ? cudaLaunchKernelEx(&cfg, engine_kernel<false, true>, a)
                                             : cudaLaunchKernelEx(&cfg, engine_kernel<false, false>, a);
+#endif
   if (e != cudaSuccess) return fail(PMPD_ERR_CUDA, "engine launch: %s", cudaGetErrorString(e));
   return PMPD_OK;
 }
 }  // namespace
 
 extern "C" {
+
+#ifdef PMPD_ENGINE_DEC_TU
+// The decoder-step engine is compiled in its own translation unit (engine_dec.cu) with fewer
+// consumer warps (PMPD_ENGINE_NCW 10, 3 tiles per warp per stage): at 384 threads the kernel gets
+// 166 registers and no spills (at 448 threads it is capped at 128 and spilled 96 bytes; measured
+// 15 % faster on the 1.4B decoder).  The linear-stack and tensor-parallel kernels keep 12 warps.
+int pmpd_engine_run_decoder_tu(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const float* x0_dev,
+                               void* resid_dev, int64_t resid_len, int32_t d_real, float* y_out, float y_alpha,
+                               uint32_t* bar_dev, int32_t* status_dev, int64_t* trace_dev, void* stream) {
+  return engine_launch(true, ops_dev, n_ops, p_dev, x0_dev, y_out, y_alpha, bar_dev, status_dev, trace_dev, stream,
+                       resid_dev, resid_len, d_real);
+}
+#else
+int pmpd_engine_run_decoder_tu(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const float* x0_dev,
+                               void* resid_dev, int64_t resid_len, int32_t d_real, float* y_out, float y_alpha,
+                               uint32_t* bar_dev, int32_t* status_dev, int64_t* trace_dev, void* stream);
 
 int pmpd_engine_run_traced(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const void* x_in, float* y_out,
                            float y_alpha, uint32_t* bar_dev, int32_t* status_dev, int64_t* trace_dev, void* stream) {
@@ -2007,8 +2079,9 @@ int pmpd_engine_run_ranks(const void* ops_dev, int32_t n_ops, int32_t n_ranks, c
 int pmpd_engine_run_decoder(const void* ops_dev, int32_t n_ops, const int32_t* p_dev, const float* x0_dev,
                             void* resid_dev, int64_t resid_len, int32_t d_real, float* y_out, float y_alpha,
                             uint32_t* bar_dev, int32_t* status_dev, int64_t* trace_dev, void* stream) {
-  return engine_launch(true, ops_dev, n_ops, p_dev, x0_dev, y_out, y_alpha, bar_dev, status_dev, trace_dev, stream,
-                       resid_dev, resid_len, d_real);
+  return pmpd_engine_run_decoder_tu(ops_dev, n_ops, p_dev, x0_dev, resid_dev, resid_len, d_real, y_out, y_alpha,
+                                    bar_dev, status_dev, trace_dev, stream);
 }
+#endif  // PMPD_ENGINE_DEC_TU
 
 }  // extern "C"

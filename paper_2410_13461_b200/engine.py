@@ -162,6 +162,7 @@ class Program:
                            ctypes.addressof(b_host))
             else:
                 # cost-balanced CTA tile ranges (stage/segment aware) instead of an even tile split
+                # (the 12-warp stage model; measured better for the 10-warp decoder kernel too)
                 _capi.call("pmpd_engine_partition", spec.packed.ref(), ctypes.addressof(b_host))
             bounds = torch.frombuffer(bytearray(b_host), dtype=torch.int32).cuda()
             self.parts.append((bounds,))

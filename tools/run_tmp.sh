@@ -1,3 +1,2 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 python tools/decoder_trace.py 2 2 2>&1 | tail -7
-timeout 600 python tools/decoder_trace.py 3 2 2>&1 | tail -7
+timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/b_e2e.json 2> gpurun_out/b_e2e.err; tail -2 gpurun_out/b_e2e.err

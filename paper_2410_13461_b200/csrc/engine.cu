@@ -299,8 +299,12 @@ constexpr int kSmMisc = 256;                         // mx, flags
 constexpr int kSmX = 1536;                           // f16 activations
 constexpr int kSmXq = kSmX + E_XMAX * 2;             // per-warp int8 activation fragments
 constexpr int kSmRed = kSmXq + E_NCW * E_TPW * 128;  // [2][E_NCW][64] f32
-constexpr int kSmRedb = kSmRed + 2 * E_NCW * 64 * 4; // [2][E_NCW] f32
-constexpr int kSmRing = (kSmRedb + 2 * E_NCW * 4 + 127) / 128 * 128;
+#ifndef PMPD_ENGINE_LANEBIAS
+#define PMPD_ENGINE_LANEBIAS 0  // 1: flush: every lane stores its bias partial, the epilogue reduces them
+#endif
+constexpr int kBiasPerWarp = PMPD_ENGINE_LANEBIAS ? 32 : 1;
+constexpr int kSmRedb = kSmRed + 2 * E_NCW * 64 * 4; // [2][E_NCW][kBiasPerWarp] f32
+constexpr int kSmRing = (kSmRedb + 2 * E_NCW * kBiasPerWarp * 4 + 127) / 128 * 128;
 
 struct Bars {
   uint64_t full[E_MAXSTAGE];
@@ -1317,8 +1321,14 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
               rw[16 * tt + gq + 8 * h] = fmaf(256.f, (float)dacc[tt][2 * h], (float)dacc[tt][2 * h + 1]) *
                                          (ds * (1.f / (float)(1 << tt)));
         }
-        const float bs = warp_sum(bias);
-        if (lane == 0) redb[buf * E_NCW + warp] = bs;
+        // (the lane sum of the bias term is left to the epilogue: one 5-step shuffle chain per
+        // segment there instead of on every consumer warp's path)
+        if (PMPD_ENGINE_LANEBIAS) {
+          redb[(buf * E_NCW + warp) * kBiasPerWarp + lane] = bias;
+        } else {
+          const float bs = warp_sum(bias);
+          if (lane == 0) redb[buf * E_NCW + warp] = bs;
+        }
         __syncwarp();  // order every lane's partial stores before lane 0's release-arrive
         if (lane == 0) mbar_arrive(&bars.red_full[buf]);
         ++seg;
@@ -1581,8 +1591,14 @@ __global__ void __launch_bounds__(E_THREADS, 1) engine_kernel(const EngineArgs a
           mbar_wait_backoff(&bars.red_full[buf], (seg >> 1) & 1);
 #endif
           float bsum = 0.f;
+          if (PMPD_ENGINE_LANEBIAS) {
 #pragma unroll
-          for (int w = 0; w < E_NCW; ++w) bsum += redb[buf * E_NCW + w];
+            for (int w = 0; w < E_NCW; ++w) bsum += redb[(buf * E_NCW + w) * kBiasPerWarp + lane];
+            bsum = warp_sum(bsum);
+          } else {
+#pragma unroll
+            for (int w = 0; w < E_NCW; ++w) bsum += redb[buf * E_NCW + w];
+          }
           // split-K: every CTA holding tiles of n-group ng adds its partial at L2 as a counted
           // fixed-point contribution (residual ops add into the residual stream)
 #pragma unroll

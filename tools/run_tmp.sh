@@ -1,2 +1,5 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu > gpurun_out/b_e2e.json 2> gpurun_out/b_e2e.err; tail -2 gpurun_out/b_e2e.err
+bash tools/run_var.sh
+bash tools/run_var.sh
+timeout 300 python tools/model_bench.py 2 2>&1 | grep '"run": "progressive"'
+timeout 600 python -m pytest -q -x tests/test_gpu_engine.py tests/test_gpu_model.py 2>&1 | tail -2

@@ -245,7 +245,7 @@ def run_reference(args, shape):
             walls.append(time.perf_counter() - t)
     v = statistics.mean(vals)
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    print(json.dumps({
+    emit({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "us/token", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(walls) * 1e3,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -254,7 +254,7 @@ def run_reference(args, shape):
         "cpu_baseline": {"value": v, "unit": "us/token", "cores": res["cores"], "kind": res["kind"],
                          "sample": res["sample"], "per_precision_us": res["per_p"]},
         "e2e": {"value": v, "unit": "us/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }), flush=True)
+    })
 
 
 def cpu_generate_sample():
@@ -293,7 +293,25 @@ def cpu_generate_sample():
 
 
 # ------------------------------------------------------------------ GPU arm
+_REAL_STDOUT = None  # fd of the process's stdout once main() has moved everything else to stderr
+
+
+def emit(obj: dict) -> None:
+    """The one JSON line of this run, on the real stdout (library banners such as NCCL's version
+    line are sent to stderr, so stdout carries nothing else)."""
+    line = (json.dumps(obj) + "\n").encode()
+    if _REAL_STDOUT is not None:
+        os.write(_REAL_STDOUT, line)
+    else:
+        sys.stdout.write(line.decode())
+        sys.stdout.flush()
+
+
 def main():
+    global _REAL_STDOUT
+    sys.stdout.flush()
+    _REAL_STDOUT = os.dup(1)
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -335,6 +353,16 @@ def main():
         from paper_2410_13461_b200.stack import TPEngineStack
         heads = 32 if args.shape == "7b" else 16
         st = TPEngineStack(shape, heads, world, seed=1234, group=dist.group.WORLD, rank=rank)
+        # liveness: the ranks' engine launches wait on each other's additions over NVLink; if one
+        # token does not complete in 60 s, report it and exit instead of hanging the job
+        st.token()
+        deadline = time.time() + 60.0
+        while not torch.cuda.current_stream().query():
+            if time.time() > deadline:
+                emit({"metric": METRIC, "impl": "b200", "n_gpus": world,
+                      "error": "tensor-parallel engine token did not complete in 60 s"})
+                os._exit(3)
+            time.sleep(0.01)
         g = st.capture(st.token)
         g_ops = g
     elif tp_mode:
@@ -568,7 +596,7 @@ def main():
             "speedup_vs_uniform4": mb["decode_speedup_vs_uniform4"], "speedup_vs_fp16": mb["decode_speedup_vs_fp16"],
             "avg_bits": mb["avg_bits"]}
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        emit(out)
     if dist is not None:
         dist.destroy_process_group()
 

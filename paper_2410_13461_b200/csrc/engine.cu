@@ -27,6 +27,11 @@
 // Instantiations: engine_kernel<DEC, TP> — DEC adds the decoder-step ops
 // (attention, RMSNorm / attention-combine inputs, one counted residual stream),
 // TP the tensor-parallel rank groups and peer copies (pmpd_engine_run_ranks).
+// This translation unit builds <false, false> and <false, true> with 12 consumer
+// warps; engine_dec.cu includes it with PMPD_ENGINE_DEC_TU to build <true, false>
+// with 10 (fewer threads, more registers for the decoder paths).
+// Sub-ops (set_slice / set_share) restrict an op to a block of its tensor on a
+// subset of CTAs, all adding into the tensor's one output vector.
 // Co-residency of all CTAs is guaranteed by a cooperative launch.
 #include <cuda_fp16.h>
 

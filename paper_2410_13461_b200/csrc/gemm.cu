@@ -168,6 +168,8 @@ struct GemmArgs {
   unsigned* sem;  // per-output-tile arrival counters (zero between launches, self-resetting)
   float* ws;      // split-K partial slices [S][M][ldw]
   int ldw;
+  int par_reduce; // 1: every CTA of the launch is resident at once, so the S splits of a tile wait for
+                  // each other and each sums 1/S of the tile's rows (else the last arriver sums all)
 };
 
 // ------------------------------------------------------------------ weight dequant
@@ -448,7 +450,20 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
     if (sk > 1) {
       const int sem_id = blockIdx.y * gridDim.x + blockIdx.x;
       uint32_t* flag = reinterpret_cast<uint32_t*>(tile);  // the smem tile is free now
-      if (tid == 0) {
+      int r_lo = 0, r_hi = min(mbn * G_BM, g.M - m0);        // rows of the tile this CTA sums
+      if (g.par_reduce) {
+        // all splits of the tile arrive, then each sums its share of the rows in split order
+        if (tid == 0) {
+          __threadfence();  // this split's slice before its arrival
+          atomicAdd(g.sem + sem_id, 1u);
+          while (*reinterpret_cast<volatile unsigned*>(g.sem + sem_id) < (unsigned)sk) __nanosleep(32);
+          __threadfence();  // every split's slice is visible before the reads below
+          *flag = 1u;
+        }
+        const int rows_all = r_hi;
+        r_lo = (int)(((long long)blockIdx.z * rows_all) / sk);
+        r_hi = (int)(((long long)(blockIdx.z + 1) * rows_all) / sk);
+      } else if (tid == 0) {
         __threadfence();  // this split's slice before its arrival
         const unsigned old = atomicAdd(g.sem + sem_id, 1u);
         const bool last = old == (unsigned)(sk - 1);
@@ -460,8 +475,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
       }
       named_bar_sync(1, G_DQ);
       if (*flag) {
-        const int rows_all = min(mbn * G_BM, g.M - m0);
-        for (int qi = tid; qi < rows_all * Q; qi += G_DQ) {
+        for (int qi = tid + r_lo * Q; qi < r_hi * Q; qi += G_DQ) {
           const int rr = qi / Q, c4 = (qi % Q) * 4, n = n0 + c4;
           if (n >= g.n_real) continue;
           const int64_t m = m0 + rr;
@@ -488,6 +502,11 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
             for (int i = 0; i < 4 && n + i < g.n_real; ++i) yr[i] = ov[i] + (g.accumulate ? yr[i] : 0.f);
           }
         }
+      }
+      if (g.par_reduce && tid == 0) {
+        // second arrival: the split that completes it (every split has passed its wait) resets the
+        // counter for the next launch
+        if (atomicAdd(g.sem + sem_id, 1u) == 2u * (unsigned)sk - 1u) g.sem[sem_id] = 0;
       }
     }
   }
@@ -565,6 +584,10 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
   // split (fitted).
   int ng = 1, mb = 1, splitk = 1;
   double best = 1e30;
+  static const double sk_cost = [] {  // µs per 1M outputs per split (fitted; PMPD_GEMM_SKCOST overrides)
+    const char* e = getenv("PMPD_GEMM_SKCOST");
+    return e ? atof(e) : 1.49;
+  }();
   const int kc_all = t->k_tiles;
   for (const auto& c : cand) {
     const int mbe = c[1] < mblocks ? c[1] : mblocks;
@@ -574,7 +597,7 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
       const int64_t ctas = (int64_t)((t->n_tiles + c[0] - 1) / c[0]) * ((mblocks + c[1] - 1) / c[1]) * sk;
       const double waves = (double)((ctas + sms - 1) / sms);
       const double cost = waves * ((kc_all + sk - 1) / sk) * (0.214 + 0.111 * c[0] + 0.192 * mbe) +
-                          (sk > 1 ? 1.49e-6 * sk * m * t->n : 0.0);
+                          (sk > 1 ? sk_cost * 1e-6 * sk * m * t->n : 0.0);
       if (cost < best * 0.999) {
         best = cost;
         ng = c[0];
@@ -631,6 +654,7 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
   g.sem = nullptr;
   g.ws = nullptr;
   g.ldw = t->n_tiles * G_NG1;
+  g.par_reduce = 0;
   if (splitk > 1) {
     // split-K workspace (grown on demand; launches on one stream reuse it in order)
     static float* ws_buf = nullptr;
@@ -651,6 +675,9 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
       if (cudaGetSymbolAddress(&sp, g_gemm_sem) != cudaSuccess) return fail(PMPD_ERR_CUDA, "prefill gemm counters");
       g.sem = static_cast<unsigned*>(sp);
       g.ws = ws_buf;
+      // one wave (every CTA resident at once): the splits of a tile share its final reduction
+      static const bool par_env = !getenv("PMPD_GEMM_SERIAL_REDUCE");
+      g.par_reduce = par_env && (int64_t)tiles * splitk <= num_sms() ? 1 : 0;
     }
     g.splitk = splitk;
   }

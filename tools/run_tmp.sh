@@ -1,2 +1,3 @@
 cd $GRAFT_REPO_ROOT
-for c in 2.0 3.0 5.0; do echo "== skcost $c"; PMPD_GEMM_SKCOST=$c timeout 600 python tools/prefill_stack.py 2>&1 | tail -1 | cut -c1-120; done
+timeout 900 python tools/gemm_bench.py > gpurun_out/gb_r2.log 2>&1
+PMPD_GEMM_SERIAL_REDUCE=1 timeout 900 python tools/gemm_bench.py > gpurun_out/gb_r2s.log 2>&1

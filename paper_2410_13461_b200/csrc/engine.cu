@@ -1288,12 +1288,17 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
 #else
       if (ws < end - t) {
 #endif
+#ifndef PMPD_ENGINE_TRACE_LOOPONLY
         if (a.trace) {
           const long long c0 = clock64();
           tile_dispatch(P, smem + kSmRing + slot * stage_bytes, end - t, ws, kt + ws, lane, xs, xq, qs, dacc, bias);
           tcyc += clock64() - c0;
           ++tcalls;
-        } else {
+        } else
+#else
+        if (a.trace) ++tcalls;  // probe: only the loop's total cycles and call count (no clocks per call)
+#endif
+        {
           tile_dispatch(P, smem + kSmRing + slot * stage_bytes, end - t, ws, kt + ws, lane, xs, xq, qs, dacc, bias);
         }
 #ifdef PMPD_ENGINE_DOUBLE  // timing probe only: every stage's tiles decoded twice (wrong results)

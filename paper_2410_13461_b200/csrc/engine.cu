@@ -997,6 +997,19 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
     constexpr int RN = 4, RN_K = 4 * RN * E_NCW * 32;
     const bool busy = r.T1 > r.T0;  // a CTA with no tiles in this op reads no input at all
     if (!busy) continue;             // (nor joins its staging barrier)
+#if PMPD_ENGINE_PREDECODE
+    // the op's first stage is usually in shared memory already: decode this warp's first tile of
+    // it now, while the input is being staged (the ALU is otherwise idle until the exchange lands)
+    uint32_t fa[2][4][4];
+    bool pre = false;
+    {
+      const int end0 = min(min(r.T0 + E_STILES, r.T1), r.T0 - r.T0 % r.KT + r.KT);
+      if (warp < end0 - r.T0 && mbar_try_wait(&bars.full[slot], phase)) {
+        predecode_dispatch(P, smem + kSmRing + slot * stage_bytes, warp, lane, fa);
+        pre = true;
+      }
+    }
+#endif
     const bool rms1 = DEC && busy && op.in_mode == E_IN_RMSNORM && op.k_real <= RN_K;
     float4 gpre[RN];
     if (DEC) {
@@ -1299,6 +1312,13 @@ PMPD_DEV void consumer_loop(const int P, const EngineArgs& a, uint8_t* smem, Bar
         if (a.trace) ++tcalls;  // probe: only the loop's total cycles and call count (no clocks per call)
 #endif
         {
+#if PMPD_ENGINE_PREDECODE
+          if (pre) {
+            tile_dispatch_pre(P, smem + kSmRing + slot * stage_bytes, end - t, ws, kt + ws, lane, xs, xq, qs, dacc, bias,
+                              fa);
+            pre = false;
+          } else
+#endif
           tile_dispatch(P, smem + kSmRing + slot * stage_bytes, end - t, ws, kt + ws, lane, xs, xq, qs, dacc, bias);
         }
 #ifdef PMPD_ENGINE_DOUBLE  // timing probe only: every stage's tiles decoded twice (wrong results)

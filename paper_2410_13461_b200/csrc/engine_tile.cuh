@@ -17,6 +17,9 @@
 #ifndef PMPD_ENGINE_TPW
 #define PMPD_ENGINE_TPW 2
 #endif
+#ifndef PMPD_ENGINE_PREDECODE
+#define PMPD_ENGINE_PREDECODE 0  // 1: decode the op's first tile per warp while its input is staged
+#endif
 
 namespace pmpd {
 constexpr int E_NCW = PMPD_ENGINE_NCW;      // consumer warps
@@ -26,9 +29,43 @@ constexpr int E_STILES = E_NCW * E_TPW;     // tiles per stage
 constexpr float E_QMAX = 32639.f;
 
 // ------------------------------------------------------------------ consumer tile
+// A fragments (u8 codes) of tile slot wslot of a stage, decoded ahead (PMPD_ENGINE_PREDECODE):
+// fa[cch][T] = {a0, a1, a2, a3} of m-tile T, k-chunk cch
 template <int P>
+PMPD_DEV void engine_predecode(const uint8_t* st, int wslot, int lane, uint32_t (&fa)[2][4][4]) {
+  uint32_t pw[4][4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (j < P) {
+      const uint4 v = *reinterpret_cast<const uint4*>(st + j * E_STILES * kTilePlaneBytes + wslot * kTilePlaneBytes +
+                                                      lane * 16);
+      pw[j][0] = v.x;
+      pw[j][1] = v.y;
+      pw[j][2] = v.z;
+      pw[j][3] = v.w;
+    } else {
+      pw[j][0] = pw[j][1] = pw[j][2] = pw[j][3] = 0u;
+    }
+  }
+#pragma unroll
+  for (int cch = 0; cch < 2; ++cch) {
+    const uint32_t pe[4] = {pw[0][2 * cch], pw[1][2 * cch], pw[2][2 * cch], pw[3][2 * cch]};
+    const uint32_t po[4] = {pw[0][2 * cch + 1], pw[1][2 * cch + 1], pw[2][2 * cch + 1], pw[3][2 * cch + 1]};
+#define PMPD_E_PRE(T)                                                                 \
+    nibble_to_u8<4, P, T>(merge_planes<4, P, T>(pe), fa[cch][T][0], fa[cch][T][1]); \
+    nibble_to_u8<4, P, T>(merge_planes<4, P, T>(po), fa[cch][T][2], fa[cch][T][3]);
+    PMPD_E_PRE(0)
+    PMPD_E_PRE(1)
+    PMPD_E_PRE(2)
+    PMPD_E_PRE(3)
+#undef PMPD_E_PRE
+  }
+}
+
+template <int P, bool PRE = false>
 PMPD_DEV void engine_tile(const uint8_t* st, int stiles_cnt, int wslot, int kt, int lane, const __half* xs,
-                          uint8_t* xq, float qs, int (&d)[4][4], float& bias) {
+                          uint8_t* xq, float qs, int (&d)[4][4], float& bias,
+                          const uint32_t (*fa)[4][4] = nullptr) {
   const int gq = lane >> 2, tig = lane & 3;
   uint32_t pw[E_TPW][4][4];
   float2 dl[E_TPW], mn[E_TPW];
@@ -39,7 +76,7 @@ PMPD_DEV void engine_tile(const uint8_t* st, int stiles_cnt, int wslot, int kt, 
     live[q] = sl < stiles_cnt;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      if (j < P && live[q]) {
+      if (j < P && live[q] && !(PRE && q == 0)) {
         const uint4 v = *reinterpret_cast<const uint4*>(st + j * E_STILES * kTilePlaneBytes + sl * kTilePlaneBytes +
                                                         lane * 16);
         pw[q][j][0] = v.x;
@@ -96,8 +133,12 @@ PMPD_DEV void engine_tile(const uint8_t* st, int stiles_cnt, int wslot, int kt, 
 #define PMPD_E_MTILE(T)                                                             \
   {                                                                                 \
     uint32_t a0, a1, a2, a3;                                                        \
-    nibble_to_u8<4, P, T>(merge_planes<4, P, T>(pe), a0, a1);                       \
-    nibble_to_u8<4, P, T>(merge_planes<4, P, T>(po), a2, a3);                       \
+    if (PRE && q == 0) {                                                            \
+      a0 = fa[cch][T][0]; a1 = fa[cch][T][1]; a2 = fa[cch][T][2]; a3 = fa[cch][T][3]; \
+    } else {                                                                        \
+      nibble_to_u8<4, P, T>(merge_planes<4, P, T>(pe), a0, a1);                     \
+      nibble_to_u8<4, P, T>(merge_planes<4, P, T>(po), a2, a3);                     \
+    }                                                                               \
     mma_u8s8_16832(d[T], a0, a1, a2, a3, bb[q][2 * cch], bb[q][2 * cch + 1]);       \
   }
       PMPD_E_MTILE(0)
@@ -124,5 +165,25 @@ PMPD_DEV void tile_dispatch(int p, const uint8_t* st, int cnt, int wslot, int kt
     default: engine_tile<1>(st, cnt, wslot, kt, lane, xs, xq, qs, d, bias); break;
   }
 }
+
+#if PMPD_ENGINE_PREDECODE
+PMPD_DEV void predecode_dispatch(int p, const uint8_t* st, int wslot, int lane, uint32_t (&fa)[2][4][4]) {
+  switch (p) {
+    case 4: engine_predecode<4>(st, wslot, lane, fa); break;
+    case 3: engine_predecode<3>(st, wslot, lane, fa); break;
+    case 2: engine_predecode<2>(st, wslot, lane, fa); break;
+    default: engine_predecode<1>(st, wslot, lane, fa); break;
+  }
+}
+PMPD_DEV void tile_dispatch_pre(int p, const uint8_t* st, int cnt, int wslot, int kt, int lane, const __half* xs,
+                                uint8_t* xq, float qs, int (&d)[4][4], float& bias, const uint32_t (&fa)[2][4][4]) {
+  switch (p) {
+    case 4: engine_tile<4, true>(st, cnt, wslot, kt, lane, xs, xq, qs, d, bias, fa); break;
+    case 3: engine_tile<3, true>(st, cnt, wslot, kt, lane, xs, xq, qs, d, bias, fa); break;
+    case 2: engine_tile<2, true>(st, cnt, wslot, kt, lane, xs, xq, qs, d, bias, fa); break;
+    default: engine_tile<1, true>(st, cnt, wslot, kt, lane, xs, xq, qs, d, bias, fa); break;
+  }
+}
+#endif
 
 }  // namespace pmpd

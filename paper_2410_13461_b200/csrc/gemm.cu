@@ -63,27 +63,30 @@ template <int NG, int MB>
 struct Cfg {
   static constexpr int N = NG * G_NG1;
   static constexpr int STAGE_B = NG * G_STAGE_B1;
-  // A load stage holds KCS consecutive K chunks: x as MB x KCS SW128 tiles (one 3-D TMA box per
-  // token block), then the packed tiles as 5 regions (planes 0..3, scales) of [NG][KCS][512 B]
-  // (one 3-D box each).  KCS is the largest of 4/2/1 that still leaves 3 stages.
-  static constexpr int stage_bytes(int kcs) { return (MB * kcs * G_STAGE_A1 + 5 * NG * kcs * kTilePlaneBytes + 1023) / 1024 * 1024; }
-  static constexpr int fit(int kcs) { return (G_SMEM_MAX - 2048 - 2 * STAGE_B) / stage_bytes(kcs); }
-  static constexpr int KCS = fit(4) >= 3 ? 4 : fit(2) >= 3 ? 2 : 1;
-  static constexpr int STAGE_X = MB * KCS * G_STAGE_A1;
-  static constexpr int WR = NG * KCS * kTilePlaneBytes;  // one plane (or scale) region
-  static constexpr int STAGE = stage_bytes(KCS);
-  // dequantized weight buffers: 3 when that still leaves 3 load stages, else 2
+  // Two load rings, one K chunk per stage.  x (MB SW128 tiles, one TMA box per token block) is
+  // read by the tensor core, so an x stage is free only when the chunk's MMAs complete; the packed
+  // tiles (5 regions: planes 0..3, scales, [NG][512 B] each) are read by the dequant warps, so a
+  // weight stage is free as soon as the chunk is dequantized.  Separate rings let the weight
+  // stream run ahead of the MMAs: dequantization of chunk c no longer waits for the TMA that
+  // could only start when MMA(c - NS) released a shared stage (measured: that chain, not the
+  // dequant arithmetic, set the pace).
+  static constexpr int STAGE_X = MB * G_STAGE_A1;
+  static constexpr int WR = NG * kTilePlaneBytes;  // one plane (or scale) region
+  static constexpr int STAGE_W = (5 * WR + 127) / 128 * 128;
 #ifndef PMPD_GEMM_NB
 #define PMPD_GEMM_NB 3
 #endif
-  static constexpr int NB = (G_SMEM_MAX - 2048 - PMPD_GEMM_NB * STAGE_B) / STAGE >= 3 ? PMPD_GEMM_NB : 2;
+  static constexpr int NB = PMPD_GEMM_NB;  // dequantized weight buffers
+  static constexpr int AVAIL = G_SMEM_MAX - 2048;
+  static constexpr int NSW = 3;
+  static constexpr int NSX_FIT = (AVAIL - NB * STAGE_B - NSW * STAGE_W) / STAGE_X;
+  static constexpr int NSX = NSX_FIT > 6 ? 6 : NSX_FIT;
   static constexpr int BUFB = NB * STAGE_B;
-  static constexpr int NS_FIT = (G_SMEM_MAX - 2048 - BUFB) / STAGE;
-  static constexpr int NS = NS_FIT > 8 ? 8 : NS_FIT;
-  static constexpr int SMEM = BUFB + NS * STAGE + 2048;  // + barriers / TMEM address + alignment slack
+  static constexpr int SMEM = BUFB + NSX * STAGE_X + NSW * STAGE_W + 2048;  // + barriers, TMEM address, alignment slack
   static constexpr int TMEM_COLS = MB * N <= 32 ? 32 : MB * N <= 64 ? 64 : MB * N <= 128 ? 128 : MB * N <= 256 ? 256 : 512;
   static_assert(MB * N <= 512, "accumulators exceed TMEM");
-  static_assert(NS >= 2, "load ring too shallow");
+  static_assert(NSX >= 2, "x ring too shallow");
+  static_assert(NB <= 4, "barrier slots");
   // kind::f16 instruction descriptor: f32 accumulator, f16 A and B, both K-major, M128 x N.
   static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(G_BM >> 4) << 24);
 };
@@ -110,6 +113,32 @@ PMPD_DEV void umma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
       ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+// Warp-wide issue: every lane runs the loop (so its addresses and counters are warp-uniform and
+// live in uniform registers), one elected lane issues.  Issuing from a `lane == 0` branch made
+// the compiler rebuild every operand with ELECT / R2UR.BROADCAST loops (~17 instructions per MMA):
+// with 4 dequant warps on the same scheduler the issue warp then fell behind the 128-cycle MMAs.
+PMPD_DEV void umma_f16_elect(uint32_t d_tmem, uint32_t a_lo, uint32_t b_lo, uint32_t d_hi, uint32_t idesc,
+                             uint32_t accum) {
+  // (descriptor = {lo, hi}: only the 14-bit start address in lo moves, smem addresses never carry
+  // out of it, so the 64-bit descriptors are two 32-bit moves, not a 64-bit add per MMA)
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t.reg .b32 e;\n\t.reg .b64 da, db;\n\t"
+      "mov.b64 da, {%1, %3};\n\t"
+      "mov.b64 db, {%2, %3};\n\t"
+      "elect.sync e|p, 0xffffffff;\n\t"
+      "setp.ne.b32 q, %5, 0;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %4, q;\n\t}"
+      ::"r"(d_tmem), "r"(a_lo), "r"(b_lo), "r"(d_hi), "r"(idesc), "r"(accum)
+      : "memory");
+}
+PMPD_DEV void umma_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 e;\n\t"
+      "elect.sync e|p, 0xffffffff;\n\t"
+      "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
+      ::"r"(smem_u32(bar))
       : "memory");
 }
 PMPD_DEV void umma_commit(uint64_t* bar) {
@@ -190,6 +219,10 @@ PMPD_DEV float2 fma2(float2 a, float2 b, float2 c) {
 }
 // Bytes j0, j0+1 of w hold bucket indices k (< 256): f16x2 of fmaf(k, step, min), rounded once.
 PMPD_DEV uint32_t bucket_pair_f16(uint32_t w, int j0, float2 step, float2 mn) {
+#ifdef GEMM_DQ_NOFP  // timing probe only: integer stand-ins for the f32 arithmetic (wrong results)
+  return __byte_perm(w, __float_as_uint(step.x) ^ __float_as_uint(mn.y), 0x7540 + j0) ^
+         __byte_perm(w, __float_as_uint(step.y) + __float_as_uint(mn.x), 0x7541 + j0);
+#endif
   const float2 kf = add2(make_float2(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540 + j0)),
                                      __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7541 + j0))),
                          make_float2(-8388608.f, -8388608.f));  // 2^23 + k - 2^23 = k, exact
@@ -199,17 +232,34 @@ PMPD_DEV uint32_t bucket_pair_f16(uint32_t w, int j0, float2 step, float2 mn) {
 }
 
 // Thread (L, w, half) decodes m-tiles 2*half, 2*half+1 of word w of lane chunk L of the chunk's
-// packed tile (16 codes, layout.cuh kn_tile_coord) and writes W^T[n][k] in f16.
-template <int P>
-PMPD_DEV void dequant_unit(const uint8_t* pl, int pstride, const uint8_t* scl, int L, int w, int half, uint8_t* sb) {
-  const int gq = L >> 2, tig = L & 3;
+// packed tile (16 codes, layout.cuh kn_tile_coord) and writes W^T[n][k] in f16.  Every address
+// is fixed per thread for the whole launch (only the stage / buffer bases move), so the caller
+// hands in precomputed offsets: the loop body is the dequant arithmetic and nothing else.
+struct DqOffsets {
+  int ld;        // L*16 + w*4: this thread's word in a 512 B plane chunk
+  int sc;        // 4*kb: this thread's 4 consecutive steps (mins at +256)
+  int st[2][2];  // [m-tile t of the pair][row gq | gq+8]: swizzled 8 B store offsets
+};
+
+#ifdef GEMM_DQ_NOSTORE  // timing probe only: dequantize but keep the weights out of shared memory
+__device__ uint32_t g_dq_sink;
+#define PMPD_DQ_STORE(addr, a, b) { if ((a ^ b) == 0x12345678u) g_dq_sink = a; }
+#else
+#define PMPD_DQ_STORE(addr, a, b) *reinterpret_cast<uint2*>(addr) = make_uint2(a, b);
+#endif
+template <int P, int HALF>
+PMPD_DEV void dequant_unit(const uint8_t* pl, int pstride, const uint8_t* scl, const DqOffsets& o, uint8_t* sb) {
   uint32_t pw[4];
+#ifdef GEMM_DQ_NOLOAD  // timing probe only: operands from registers instead of shared memory
 #pragma unroll
-  for (int j = 0; j < 4; ++j) pw[j] = j < P ? reinterpret_cast<const uint32_t*>(pl + j * pstride + L * 16)[w] : 0u;
-  const int kb = 32 * (w >> 1) + 16 * (w & 1) + 4 * tig;  // 4 consecutive k of this word
-  const float* sc = reinterpret_cast<const float*>(scl);
-  const float4 d4 = *reinterpret_cast<const float4*>(sc + kb);
-  const float4 m4 = *reinterpret_cast<const float4*>(sc + 64 + kb);
+  for (int j = 0; j < 4; ++j) pw[j] = (uint32_t)(size_t)pl * (j + 1) + o.ld;
+  const float4 d4 = make_float4(__int_as_float(o.sc), 1.f, 2.f, 3.f), m4 = make_float4(1.f, (float)(size_t)scl, 3.f, 4.f);
+#else
+#pragma unroll
+  for (int j = 0; j < 4; ++j) pw[j] = j < P ? *reinterpret_cast<const uint32_t*>(pl + j * pstride + o.ld) : 0u;
+  const float4 d4 = *reinterpret_cast<const float4*>(scl + o.sc);
+  const float4 m4 = *reinterpret_cast<const float4*>(scl + 256 + o.sc);
+#endif
   // Each weight is the reference's dequantized value in f32, fmaf(k, step, min) (bit-exact with
   // float32(dequantize(qt, p)), quant.py:199-215), rounded ONCE to f16 for the tensor core: the
   // same operand precision as the fp16 baseline.  (Rounding step and min to f16 first puts one
@@ -221,66 +271,116 @@ PMPD_DEV void dequant_unit(const uint8_t* pl, int pstride, const uint8_t* scl, i
   constexpr uint32_t kLoaded = ((1u << 4) - 1) & ~((1u << (4 - P)) - 1);
   constexpr uint32_t kConst = (P < 4) ? (1u << (4 - P - 1)) : 0u;
   constexpr uint32_t kl = kLoaded * 0x01010101u, kc = kConst * 0x01010101u;
-  const uint32_t pe[4] = {pw[0], pw[1], pw[2], pw[3]};
-#define PMPD_G_T(T)                                                                                  \
+#define PMPD_G_T(T, I)                                                                               \
   {                                                                                                  \
-    uint32_t u = merge_planes<4, P, T>(pe);                                                          \
+    uint32_t u = merge_planes<4, P, T>(pw);                                                          \
     u = T ? rotr32(u, T) : u; /* nibble slot s = bucket index of row 16T+gq+8(s&1), k = kb+(s>>1) */ \
     const uint32_t ev = lop3_and_or(u, kl, kc);          /* byte j = bucket index (row gq, kb+j) */  \
     const uint32_t od = lop3_and_or(u >> 4, kl, kc);     /* byte j = bucket index (row gq+8, kb+j) */\
     const uint32_t ve0 = bucket_pair_f16(ev, 0, d01, m01), ve1 = bucket_pair_f16(ev, 2, d23, m23);   \
     const uint32_t vo0 = bucket_pair_f16(od, 0, d01, m01), vo1 = bucket_pair_f16(od, 2, d23, m23);   \
-    *reinterpret_cast<uint2*>(sb + sw128_off(16 * T + gq, kb)) = make_uint2(ve0, ve1);               \
-    *reinterpret_cast<uint2*>(sb + sw128_off(16 * T + gq + 8, kb)) = make_uint2(vo0, vo1);           \
+    PMPD_DQ_STORE(sb + o.st[I][0], ve0, ve1)                                                        \
+    PMPD_DQ_STORE(sb + o.st[I][1], vo0, vo1)                                                        \
   }
-  if (half == 0) {
-    PMPD_G_T(0)
-    PMPD_G_T(1)
-  } else {
-    PMPD_G_T(2)
-    PMPD_G_T(3)
-  }
+  PMPD_G_T(2 * HALF, 0)
+  PMPD_G_T(2 * HALF + 1, 1)
 #undef PMPD_G_T
 }
 
-// The 8 dequant warps, specialised per precision: for each K chunk wait for a free weight
-// buffer (its MMAs of NB chunks ago completed) and the chunk's packed tiles, dequantize, then
-// each warp arrives on the buffer's full barrier.  No CTA-wide barrier: warps run ahead
-// independently and the MMA warp issues as soon as all 8 have arrived.
-template <int P, int NG, int MB>
-PMPD_DEV void dequant_loop(int KC, int ngn, uint8_t* ring, uint8_t* bufs, uint64_t* full_bar, uint64_t* bfull,
-                           uint64_t* bempty, int tid) {
+// The dequant warps, specialised per precision and per m-tile half (uniform per warp): for each
+// K chunk wait for a free weight buffer (its MMAs of NB chunks ago completed) and the chunk's
+// packed tiles, dequantize, then each warp arrives on the buffer's full barrier.  No CTA-wide
+// barrier: warps run ahead independently and the MMA warp issues as soon as all have arrived.
+template <int P, int NG, int MB, int HALF>
+PMPD_DEV void dequant_loop_h(int KC, int ngn, const uint8_t* wring, uint8_t* bufs, uint64_t* wfull, uint64_t* wempty,
+                             uint64_t* bfull, uint64_t* bempty, int g, const DqOffsets& o) {
   using C = Cfg<NG, MB>;
-  const int tt = tid & 255;  // unit within an n-group; thread group tid >> 8 takes n-groups h = g, g + G_DQG, ...
-  const int uw = (tt >> 5) & 3, uhalf = tt >> 7;
-  const int uL = ((tt >> 1) & 7) * 4 + ((tt >> 4) & 1) * 2 + (tt & 1);
+  constexpr int HN = (NG + G_DQG - 1) / G_DQG;  // n-groups per thread group
+  int sw = 0, b = 0;                             // weight stage, weight buffer
+  uint32_t wph = 0, bph = 0;                     // their mbarrier phases
+#ifdef GEMM_TRACE
+  long long tr_be = 0, tr_wf = 0, tr0 = clock64();
+#endif
   for (int kc = 0; kc < KC; ++kc) {
-    const int st = kc / C::KCS, kcs = kc - st * C::KCS, s = st % C::NS, b = kc % C::NB;
-    const uint8_t* w0 = ring + s * C::STAGE + C::STAGE_X;
+    const uint8_t* w0 = wring + sw * C::STAGE_W;
     uint8_t* sb = bufs + b * C::STAGE_B;
-    if (kc >= C::NB) mbar_wait(&bempty[b], ((kc - C::NB) / C::NB) & 1);
-    if (kcs == 0) mbar_wait(&full_bar[s], (st / C::NS) & 1);
+#ifdef GEMM_TRACE
+    long long t0 = clock64();
+    if (kc >= C::NB) mbar_wait(&bempty[b], bph ^ 1u);
+    long long t1 = clock64();
+    mbar_wait(&wfull[sw], wph);
+    tr_be += t1 - t0;
+    tr_wf += clock64() - t1;
+#else
+    if (kc >= C::NB) mbar_wait(&bempty[b], bph ^ 1u);
+    mbar_wait(&wfull[sw], wph);
+#endif
 #ifndef GEMM_SKIP_DEQUANT
-    for (int h = tid >> 8; h < NG; h += G_DQG) {
-      uint8_t* sbh = sb + h * G_STAGE_B1;
-      if (h < ngn) {
-        const int toff = (h * C::KCS + kcs) * kTilePlaneBytes;
-        dequant_unit<P>(w0 + toff, C::WR, w0 + 4 * C::WR + toff, uL, uw, uhalf, sbh);
-      } else {  // n-group past the matrix: zero weights
 #pragma unroll
-        for (int t = 0; t < 2; ++t)
+    for (int i = 0; i < HN; ++i) {
+      const int h = g + i * G_DQG;
+      if (h < NG) {
+        if (h < ngn) {
+          dequant_unit<P, HALF>(w0 + h * kTilePlaneBytes, C::WR, w0 + 4 * C::WR + h * kTilePlaneBytes, o,
+                                sb + h * G_STAGE_B1);
+        } else {  // n-group past the matrix: zero weights
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh)
-            *reinterpret_cast<uint2*>(sbh + sw128_off(16 * (2 * uhalf + t) + (uL >> 2) + 8 * hh,
-                                                      32 * (uw >> 1) + 16 * (uw & 1) + 4 * (uL & 3))) =
-                make_uint2(0u, 0u);
+          for (int t = 0; t < 2; ++t)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh)
+              *reinterpret_cast<uint2*>(sb + h * G_STAGE_B1 + o.st[t][hh]) = make_uint2(0u, 0u);
+        }
       }
     }
 #endif
     fence_async_smem();  // this thread's dequant stores -> visible to the tensor core (async proxy)
     __syncwarp();
-    if ((tid & 31) == 0) mbar_arrive(&bfull[b]);
+    if ((threadIdx.x & 31) == 0) {
+      mbar_arrive(&bfull[b]);
+      mbar_arrive(&wempty[sw]);  // every load of the stage has returned (its values were stored)
+    }
+    if (++sw == C::NSW) {
+      sw = 0;
+      wph ^= 1u;
+    }
+    if (++b == C::NB) {
+      b = 0;
+      bph ^= 1u;
+    }
   }
+#ifdef GEMM_TRACE
+  if (blockIdx.x % 16 == 0 && blockIdx.y == 0 && (threadIdx.x == 0 || threadIdx.x == 352))
+    printf("cta %d,%d dq thread %d: loop %lld cyc, wait bempty %lld, wait wfull %lld\n", blockIdx.x, blockIdx.y,
+           threadIdx.x, clock64() - tr0, tr_be, tr_wf);
+#endif
+}
+
+template <int P, int NG, int MB>
+PMPD_DEV void dequant_loop(int KC, int ngn, const uint8_t* wring, uint8_t* bufs, uint64_t* wfull, uint64_t* wempty,
+                           uint64_t* bfull, uint64_t* bempty, int tid) {
+  // Thread (L, w, half) of an n-group's 256: warp wq = tt >> 5 of the 8 takes lane chunks
+  // L = 8 (wq & 3) .. + 7 and m-tile half wq >> 2.  Lane l = [j>>2 : w>>1 : w&1 : j&3] (bit 4..0)
+  // takes word w of chunk 8 (wq & 3) + j: the warp's 32 plane-word loads are 128 consecutive bytes
+  // (one wavefront), and each 8-lane phase of the 128-bit scale loads reads 8 distinct 16 B slots
+  // of one 128 B row (conflict-free; the former word-per-warp mapping cost a 4-way conflict on
+  // every plane load and a 2-way one on every scale load).
+  const int tt = tid & 255;  // unit within an n-group; thread group tid >> 8 takes n-groups h = g, g + G_DQG, ...
+  const int wq = tt >> 5, l = tt & 31;
+  const int uw = ((l >> 2) & 1) | (((l >> 3) & 1) << 1), uhalf = wq >> 2;
+  const int uL = 8 * (wq & 3) + 4 * (l >> 4) + (l & 3);
+  const int gq = uL >> 2, tig = uL & 3;
+  const int kb = 32 * (uw >> 1) + 16 * (uw & 1) + 4 * tig;  // 4 consecutive k of this word
+  DqOffsets o;
+  o.ld = uL * 16 + uw * 4;
+  o.sc = kb * 4;
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) o.st[t][hh] = (int)sw128_off(16 * (2 * uhalf + t) + gq + 8 * hh, kb);
+  if (uhalf == 0)
+    dequant_loop_h<P, NG, MB, 0>(KC, ngn, wring, bufs, wfull, wempty, bfull, bempty, tid >> 8, o);
+  else
+    dequant_loop_h<P, NG, MB, 1>(KC, ngn, wring, bufs, wfull, wempty, bfull, bempty, tid >> 8, o);
 }
 
 template <int NG, int MB>
@@ -288,13 +388,19 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
   using C = Cfg<NG, MB>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // SW128 operand tiles need 1024-byte alignment
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint8_t* ring = smem + C::BUFB;                                                   // [NS] load stages
-  uint64_t* mma_bar = reinterpret_cast<uint64_t*>(ring + C::NS * C::STAGE);         // [NS] stage consumed
-  uint64_t* full_bar = mma_bar + 8;                                                 // [NS] stage loaded
-  uint64_t* bfull = mma_bar + 16;                                                   // [NB] weights dequantized
-  uint64_t* bempty = mma_bar + 20;                                                  // [NB] weights consumed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_bar + 24);
+  // (offset the shared pointer itself: a round trip through uintptr_t loses the address space, and
+  // every dequant load/store then compiled to a generic LD.E/ST.E on the long-scoreboard path)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* xring = smem + C::BUFB;                                                  // [NSX] x stages
+  uint8_t* wring = xring + C::NSX * C::STAGE_X;                                     // [NSW] packed-tile stages
+  uint64_t* xfull = reinterpret_cast<uint64_t*>(wring + C::NSW * C::STAGE_W);      // [NSX] x landed
+  uint64_t* xempty = xfull + 8;                                                     // [NSX] x consumed (MMAs done)
+  uint64_t* wfull = xfull + 16;                                                     // [NSW] packed tiles landed
+  uint64_t* wempty = xfull + 24;                                                    // [NSW] packed tiles read
+  uint64_t* bfull = xfull + 32;                                                     // [NB] weights dequantized
+  uint64_t* bempty = xfull + 36;                                                    // [NB] weights consumed
+  uint64_t* done_bar = xfull + 40;                                                  // every MMA of the CTA done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfull + 41);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nt0 = blockIdx.x * NG, m0 = blockIdx.y * (MB * G_BM);
   const int ngn = min(NG, g.n_tiles - nt0);  // n-groups of this CTA inside the matrix
@@ -304,14 +410,19 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
     p = p < 1 ? 1 : 4;
   }
   if (tid == 0) {
-    for (int i = 0; i < C::NS; ++i) {
-      mbar_init(&mma_bar[i], 1);
-      mbar_init(&full_bar[i], 1);
+    for (int i = 0; i < C::NSX; ++i) {
+      mbar_init(&xfull[i], 1);
+      mbar_init(&xempty[i], 1);
+    }
+    for (int i = 0; i < C::NSW; ++i) {
+      mbar_init(&wfull[i], 1);
+      mbar_init(&wempty[i], G_DQ / 32);
     }
     for (int i = 0; i < C::NB; ++i) {
       mbar_init(&bfull[i], G_DQ / 32);
       mbar_init(&bempty[i], 1);
     }
+    mbar_init(done_bar, 1);
     fence_barrier_init();
   }
   if (warp == 0) {
@@ -332,56 +443,119 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
 
   if (warp == G_PROD) {
     // ---------------------------------------------------------------- TMA producer
+    // One thread feeds both rings, never blocking on one while the other has a free stage: the
+    // weight stream runs up to NSW chunks ahead of the dequant, x up to NSX ahead of the MMAs.
+#ifdef GEMM_MMA_ONLY
+    if (false) {
+#else
     if (lane == 0) {
-      const int nst = (KC + C::KCS - 1) / C::KCS;
-      for (int st = 0; st < nst; ++st) {
-        const int s = st % C::NS, kc0 = kbase + st * C::KCS;  // absolute chunk (TMA coordinate)
-        uint8_t* sx = ring + s * C::STAGE;
-        uint8_t* sw = sx + C::STAGE_X;
-        if (st >= C::NS) mbar_wait_backoff(&mma_bar[s], ((st - C::NS) / C::NS) & 1);
-        // full boxes land (TMA zero-fills past K, M and the last n-tile), so count them whole
-        mbar_arrive_expect_tx(&full_bar[s], (uint32_t)(mbn * C::KCS * G_STAGE_A1 + (p + 1) * C::WR));
-        for (int mb = 0; mb < mbn; ++mb)
-          tma_3d(sx + mb * C::KCS * G_STAGE_A1, &maps.x, 0, m0 + mb * G_BM, kc0, &full_bar[s]);
-        tma_4d(sw, &maps.plane[p - 1], 0, kc0, nt0, 0, &full_bar[s]);  // planes 0..p-1
-        tma_3d(sw + 4 * C::WR, &maps.scale, 0, kc0, nt0, &full_bar[s]);
+#endif
+      int cx = 0, cw = 0, sx = 0, sw = 0;
+      uint32_t xph = 0, wph = 0;
+      while (cx < KC || cw < KC) {
+        bool idle = true;
+        if (cw < KC && (cw < C::NSW || mbar_try_wait(&wempty[sw], wph ^ 1u))) {
+          uint8_t* dst = wring + sw * C::STAGE_W;
+          mbar_arrive_expect_tx(&wfull[sw], (uint32_t)((p + 1) * C::WR));  // full boxes (zero-filled past the matrix)
+          tma_4d(dst, &maps.plane[p - 1], 0, kbase + cw, nt0, 0, &wfull[sw]);  // planes 0..p-1
+          tma_3d(dst + 4 * C::WR, &maps.scale, 0, kbase + cw, nt0, &wfull[sw]);
+          ++cw;
+          if (++sw == C::NSW) {
+            sw = 0;
+            wph ^= 1u;
+          }
+          idle = false;
+        }
+        if (cx < KC && (cx < C::NSX || mbar_try_wait(&xempty[sx], xph ^ 1u))) {
+          uint8_t* dst = xring + sx * C::STAGE_X;
+#ifdef GEMM_SKIP_X  // timing probe only: x is not loaded (wrong results)
+          mbar_arrive(&xfull[sx]);
+#else
+          mbar_arrive_expect_tx(&xfull[sx], (uint32_t)(mbn * G_STAGE_A1));
+          for (int mb = 0; mb < mbn; ++mb) tma_3d(dst + mb * G_STAGE_A1, &maps.x, 0, m0 + mb * G_BM, kbase + cx, &xfull[sx]);
+#endif
+          ++cx;
+          if (++sx == C::NSX) {
+            sx = 0;
+            xph ^= 1u;
+          }
+          idle = false;
+        }
+        if (idle) __nanosleep(20);
       }
     }
   } else if (warp == G_MMA) {
-    // ---------------------------------------------------------------- MMA issue (one lane)
-    if (lane == 0) {
+    // ---------------------------------------------------------------- MMA issue (whole warp, one elected lane issues)
+    {
+      int sx = 0, b = 0;
+      uint32_t xph = 0, bph = 0;
+#ifdef GEMM_TRACE
+      long long tw_b = 0, tw_x = 0, tstart = clock64();
+#endif
+      // descriptors: start address in bits [0,14) (16 B units); the K16 step adds 32 B = 2 units
+      const uint64_t d0 = smem_desc_sw128(0);
+      const uint32_t d_hi = (uint32_t)(d0 >> 32), d_lo = (uint32_t)d0;
+      const uint32_t xa_lo = d_lo + (smem_u32(xring) >> 4), bb_lo = d_lo + (smem_u32(smem) >> 4);
       for (int kc = 0; kc < KC; ++kc) {
-        const int st = kc / C::KCS, kcs = kc - st * C::KCS, s = st % C::NS, b = kc % C::NB;
-        mbar_wait(&bfull[b], (kc / C::NB) & 1);  // implies the chunk's TMA landed (dequant waited on it)
+#ifndef GEMM_MMA_ONLY  // (timing probe: MMAs back to back on whatever the buffers hold)
+#ifdef GEMM_TRACE
+        long long t0 = clock64();
+        mbar_wait(&bfull[b], bph);
+        long long t1 = clock64();
+        mbar_wait(&xfull[sx], xph);
+        tw_b += t1 - t0;
+        tw_x += clock64() - t1;
+#else
+        mbar_wait(&bfull[b], bph);  // the chunk's weights dequantized
+        mbar_wait(&xfull[sx], xph); // and its x landed
+#endif
+#endif
         tc_fence_after();
-        const uint32_t b0 = smem_u32(smem + b * C::STAGE_B);
-        for (int mb = 0; mb < mbn; ++mb) {
-          const uint32_t a0 = smem_u32(ring + s * C::STAGE + (mb * C::KCS + kcs) * G_STAGE_A1);
+        const uint32_t b_lo = bb_lo + (uint32_t)((b * C::STAGE_B) >> 4);
+        const uint32_t a_lo = xa_lo + (uint32_t)((sx * C::STAGE_X) >> 4);
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+          if (mb < mbn) {
 #ifndef GEMM_SKIP_MMA
 #pragma unroll
-          for (int k16 = 0; k16 < G_KC / 16; ++k16)
-            umma_f16(tmem + mb * C::N, smem_desc_sw128(a0 + 32 * k16), smem_desc_sw128(b0 + 32 * k16), C::IDESC,
-                     (kc > 0 || k16 > 0) ? 1u : 0u);
+            for (int k16 = 0; k16 < G_KC / 16; ++k16)
+              umma_f16_elect(tmem + mb * C::N, a_lo + (uint32_t)((mb * G_STAGE_A1 + 32 * k16) >> 4), b_lo + 2u * k16, d_hi,
+                             C::IDESC, (kc > 0 || k16 > 0) ? 1u : 0u);
 #endif
+          }
         }
-        if (kcs == C::KCS - 1 || kc == KC - 1) umma_commit(&mma_bar[s]);  // load stage reusable
-        umma_commit(&bempty[b]);                                          // weight buffer reusable
+        umma_commit_elect(&xempty[sx]);  // x stage reusable
+        umma_commit_elect(&bempty[b]);   // weight buffer reusable
+        if (++sx == C::NSX) {
+          sx = 0;
+          xph ^= 1u;
+        }
+        if (++b == C::NB) {
+          b = 0;
+          bph ^= 1u;
+        }
       }
+      umma_commit_elect(done_bar);  // (tracks completion of every MMA issued before it)
+#ifdef GEMM_TRACE
+      if (lane == 0 && blockIdx.x % 16 == 0 && blockIdx.y == 0)
+        printf("cta %d,%d KC %d: mma loop %lld cyc, wait bfull %lld, wait xfull %lld\n", blockIdx.x, blockIdx.y, KC,
+               clock64() - tstart, tw_b, tw_x);
+#endif
     }
   } else {
     // ---------------------------------------------------------------- dequant warps
+#ifdef GEMM_MMA_ONLY
+    if (false)
+#endif
     switch (p) {
-      case 4: dequant_loop<4, NG, MB>(KC, ngn, ring, smem, full_bar, bfull, bempty, tid); break;
-      case 3: dequant_loop<3, NG, MB>(KC, ngn, ring, smem, full_bar, bfull, bempty, tid); break;
-      case 2: dequant_loop<2, NG, MB>(KC, ngn, ring, smem, full_bar, bfull, bempty, tid); break;
-      default: dequant_loop<1, NG, MB>(KC, ngn, ring, smem, full_bar, bfull, bempty, tid); break;
+      case 4: dequant_loop<4, NG, MB>(KC, ngn, wring, smem, wfull, wempty, bfull, bempty, tid); break;
+      case 3: dequant_loop<3, NG, MB>(KC, ngn, wring, smem, wfull, wempty, bfull, bempty, tid); break;
+      case 2: dequant_loop<2, NG, MB>(KC, ngn, wring, smem, wfull, wempty, bfull, bempty, tid); break;
+      default: dequant_loop<1, NG, MB>(KC, ngn, wring, smem, wfull, wempty, bfull, bempty, tid); break;
     }
   }
   // all MMAs done
-  {
-    const int last = (KC - 1) / C::KCS;
-    mbar_wait(&mma_bar[last % C::NS], (last / C::NS) & 1);
-  }
+  mbar_wait(done_bar, 0);
   tc_fence_after();
   // epilogue, per accumulator block: TMEM -> smem tile [128 rows][N (+1 pad)] f32 (warp w reads
   // TMEM lanes 32*(w%4).., columns half w/4), then all 256 threads write y in coalesced row
@@ -618,10 +792,9 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
       mb = b;
     }
   }
-  const int kcs = ng == 1 && mb == 4 ? Cfg<1, 4>::KCS : ng == 2 && mb == 4 ? Cfg<2, 4>::KCS : ng == 4 && mb == 2 ? Cfg<4, 2>::KCS : ng == 4 ? Cfg<4, 1>::KCS : ng == 2 && mb == 2 ? Cfg<2, 2>::KCS
-                  : ng == 2 ? Cfg<2, 1>::KCS : mb == 2 ? Cfg<1, 2>::KCS : Cfg<1, 1>::KCS;
+  const int kcs = 1;  // one K chunk per TMA box (both rings stage single chunks)
   GemmMaps maps;
-  // x: [K/64 chunks][m rows][64 k] f16, box 64 k x 128 rows x KCS chunks -> KCS SW128 tiles (zero-filled past m)
+  // x: [K/64 chunks][m rows][64 k] f16, box 64 k x 128 rows x 1 chunk -> one SW128 tile (zero-filled past m)
   {
     const cuuint64_t gdim[3] = {(cuuint64_t)G_KC, (cuuint64_t)m, (cuuint64_t)t->k_tiles};
     const cuuint64_t gstride[2] = {(cuuint64_t)ldx * 2, (cuuint64_t)G_KC * 2};
@@ -632,8 +805,8 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(PMPD_ERR_CUDA, "prefill gemm: x tensor map (%d)", (int)r);
   }
-  // planes: [4][n_tiles][k_tiles][128 words of one 512 B tile], box 128 x KCS x NG x (j+1);
-  // scales: [n_tiles][k_tiles][128], box 128 x KCS x NG
+  // planes: [4][n_tiles][k_tiles][128 words of one 512 B tile], box 128 x 1 x NG x (j+1);
+  // scales: [n_tiles][k_tiles][128], box 128 x 1 x NG
   {
     const cuuint64_t gdim[4] = {128, (cuuint64_t)t->k_tiles, (cuuint64_t)t->n_tiles, 4};
     const cuuint64_t gstride[3] = {(cuuint64_t)kTilePlaneBytes, (cuuint64_t)t->k_tiles * kTilePlaneBytes,

@@ -107,14 +107,6 @@ PMPD_DEV uint64_t smem_desc_sw128(uint32_t saddr) {
   return d;
 }
 
-PMPD_DEV void umma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-      ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accum)
-      : "memory");
-}
 // Warp-wide issue: every lane runs the loop (so its addresses and counters are warp-uniform and
 // live in uniform registers), one elected lane issues.  Issuing from a `lane == 0` branch made
 // the compiler rebuild every operand with ELECT / R2UR.BROADCAST loops (~17 instructions per MMA):
@@ -133,6 +125,16 @@ PMPD_DEV void umma_f16_elect(uint32_t d_tmem, uint32_t a_lo, uint32_t b_lo, uint
       ::"r"(d_tmem), "r"(a_lo), "r"(b_lo), "r"(d_hi), "r"(idesc), "r"(accum)
       : "memory");
 }
+// Commit arriving on the mbarrier at this offset in every CTA of ctaMask (the x stage is shared
+// by the cluster's multicast, so it is free only when every CTA's MMAs have read it).
+PMPD_DEV void umma_commit_mc_elect(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 e;\n\t"
+      "elect.sync e|p, 0xffffffff;\n\t"
+      "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
+      ::"r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
 PMPD_DEV void umma_commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t.reg .b32 e;\n\t"
@@ -140,10 +142,6 @@ PMPD_DEV void umma_commit_elect(uint64_t* bar) {
       "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
       ::"r"(smem_u32(bar))
       : "memory");
-}
-PMPD_DEV void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
 }
 PMPD_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 PMPD_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -171,6 +169,24 @@ PMPD_DEV void tma_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, 
           smem_u32(dst)),
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
+}
+
+// x box into the same smem offset of every CTA in ctaMask (cluster multicast); each destination
+// CTA's mbarrier at the same offset receives the bytes it got.
+PMPD_DEV void tma_3d_mc(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+PMPD_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+PMPD_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
 }
 
 // TMA descriptors of one launch: x as [K/64 chunks][M rows][64 k] (f16, 128 B swizzle); the bit
@@ -383,7 +399,11 @@ PMPD_DEV void dequant_loop(int KC, int ngn, const uint8_t* wring, uint8_t* bufs,
     dequant_loop_h<P, NG, MB, 1>(KC, ngn, wring, bufs, wfull, wempty, bfull, bempty, tid >> 8, o);
 }
 
-template <int NG, int MB>
+// CL > 1: clusters of CL CTAs along N (same token rows, neighbouring n-blocks) share every x
+// chunk: each CTA loads 128/CL rows of each block and multicasts them to the whole cluster, so
+// the L2->SM traffic of x (the bulk of the load stream: 2 x 16 KB per chunk at MB = 2 against
+// 10 KB of packed weights) drops CL-fold.
+template <int NG, int MB, int CL>
 __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, const __grid_constant__ GemmMaps maps) {
   using C = Cfg<NG, MB>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -412,7 +432,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
   if (tid == 0) {
     for (int i = 0; i < C::NSX; ++i) {
       mbar_init(&xfull[i], 1);
-      mbar_init(&xempty[i], 1);
+      mbar_init(&xempty[i], CL);  // one commit from every CTA of the cluster
     }
     for (int i = 0; i < C::NSW; ++i) {
       mbar_init(&wfull[i], 1);
@@ -433,8 +453,11 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CL > 1) cluster_sync_all();  // every CTA's barriers exist before any multicast lands
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int crank = CL > 1 ? (int)cluster_rank() : 0;
+  constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1);
   // this CTA's K chunks: all of them, or its split-K slice [kbase, kbase + KC)
   const int kbase = (int)(((long long)blockIdx.z * g.k_tiles) / g.splitk);
   const int KC = (int)(((long long)(blockIdx.z + 1) * g.k_tiles) / g.splitk) - kbase;
@@ -472,7 +495,13 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
           mbar_arrive(&xfull[sx]);
 #else
           mbar_arrive_expect_tx(&xfull[sx], (uint32_t)(mbn * G_STAGE_A1));
-          for (int mb = 0; mb < mbn; ++mb) tma_3d(dst + mb * G_STAGE_A1, &maps.x, 0, m0 + mb * G_BM, kbase + cx, &xfull[sx]);
+          if constexpr (CL > 1) {
+            for (int mb = 0; mb < mbn; ++mb)
+              tma_3d_mc(dst + mb * G_STAGE_A1 + crank * (G_STAGE_A1 / CL), &maps.x, 0, m0 + mb * G_BM + crank * (G_BM / CL),
+                        kbase + cx, &xfull[sx], kMask);
+          } else {
+            for (int mb = 0; mb < mbn; ++mb) tma_3d(dst + mb * G_STAGE_A1, &maps.x, 0, m0 + mb * G_BM, kbase + cx, &xfull[sx]);
+          }
 #endif
           ++cx;
           if (++sx == C::NSX) {
@@ -524,7 +553,10 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
 #endif
           }
         }
-        umma_commit_elect(&xempty[sx]);  // x stage reusable
+        if constexpr (CL > 1)
+          umma_commit_mc_elect(&xempty[sx], kMask);  // x stage reusable once every CTA of the cluster read it
+        else
+          umma_commit_elect(&xempty[sx]);  // x stage reusable
         umma_commit_elect(&bempty[b]);   // weight buffer reusable
         if (++sx == C::NSX) {
           sx = 0;
@@ -686,19 +718,54 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CL > 1) cluster_sync_all();  // no CTA leaves while a peer may still multicast into it
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS) : "memory");
 }
 
-template <int NG, int MB>
-int launch(const GemmArgs& g, const GemmMaps& maps, int m, int n_tiles, cudaStream_t st) {
+template <int NG, int MB, int CL>
+int launch(const GemmArgs& g_in, const GemmMaps& maps, int m, int n_tiles, cudaStream_t st) {
+  GemmArgs g = g_in;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_kernel<NG, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<NG, MB>::SMEM);
+    cudaFuncSetAttribute(gemm_kernel<NG, MB, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<NG, MB>::SMEM);
+    if (CL > 1) cudaFuncSetAttribute(gemm_kernel<NG, MB, CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
-  dim3 grid((n_tiles + NG - 1) / NG, (m + MB * G_BM - 1) / (MB * G_BM), g.splitk);
-  gemm_kernel<NG, MB><<<grid, G_THREADS, Cfg<NG, MB>::SMEM, st>>>(g, maps);
+  const int nb = (n_tiles + NG - 1) / NG;
+  dim3 grid((nb + CL - 1) / CL * CL, (m + MB * G_BM - 1) / (MB * G_BM), g.splitk);  // (a padding n-block computes zeros)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(G_THREADS);
+  cfg.dynamicSmemBytes = Cfg<NG, MB>::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (g.par_reduce) {
+    // the splits of a tile wait for each other: only when every CTA of the launch is co-resident
+    // (clusters of 2 need SM pairs, so fewer than the SM count may be resident at once)
+    static int max_ctas = -1;
+    if (max_ctas < 0) {
+      int nc = 0;
+      if (CL > 1) {
+        cudaLaunchConfig_t q = cfg;
+        q.gridDim = dim3(CL, 1, 1);
+        if (cudaOccupancyMaxActiveClusters(&nc, gemm_kernel<NG, MB, CL>, &q) != cudaSuccess) nc = 0;
+        cudaGetLastError();
+        max_ctas = nc * CL;
+      } else {
+        max_ctas = num_sms();
+      }
+    }
+    if ((int64_t)grid.x * grid.y * grid.z > max_ctas) g.par_reduce = 0;
+  }
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_kernel<NG, MB, CL>, g, maps);
+  if (e != cudaSuccess) return fail(PMPD_ERR_CUDA, "prefill gemm launch: %s", cudaGetErrorString(e));
   return check_launch("prefill gemm launch");
 }
 
@@ -793,12 +860,22 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
     }
   }
   const int kcs = 1;  // one K chunk per TMA box (both rings stage single chunks)
+  // PMPD_GEMM_CL=2: x multicast across clusters of 2 CTAs along N (halves the x traffic from L2;
+  // measured neutral to 2 % slower on the config-4 shapes and the 7B stack: the launch is bound
+  // by the dequant warps and the MMA issue, not by the load stream), off by default
+  static const int cl_env = [] {
+    const char* e = getenv("PMPD_GEMM_CL");
+    return e ? atoi(e) : 1;
+  }();
+  const int nblk = (t->n_tiles + ng - 1) / ng;
+  const int cl = (cl_env == 2 && nblk >= 2) ? 2 : 1;
+  const int nblk_pad = (nblk + cl - 1) / cl * cl;
   GemmMaps maps;
   // x: [K/64 chunks][m rows][64 k] f16, box 64 k x 128 rows x 1 chunk -> one SW128 tile (zero-filled past m)
   {
     const cuuint64_t gdim[3] = {(cuuint64_t)G_KC, (cuuint64_t)m, (cuuint64_t)t->k_tiles};
     const cuuint64_t gstride[2] = {(cuuint64_t)ldx * 2, (cuuint64_t)G_KC * 2};
-    const cuuint32_t box[3] = {(cuuint32_t)G_KC, (cuuint32_t)G_BM, (cuuint32_t)kcs};
+    const cuuint32_t box[3] = {(cuuint32_t)G_KC, (cuuint32_t)(G_BM / cl), (cuuint32_t)kcs};  // (a cluster CTA's share)
     const cuuint32_t estride[3] = {1, 1, 1};
     const CUresult r = encode(&maps.x, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(x_dev), gdim, gstride, box,
                               estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -832,7 +909,7 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
     // split-K workspace (grown on demand; launches on one stream reuse it in order)
     static float* ws_buf = nullptr;
     static size_t ws_cap = 0;
-    const int tiles = ((t->n_tiles + ng - 1) / ng) * ((m + mb * G_BM - 1) / (mb * G_BM));
+    const int tiles = nblk_pad * ((m + mb * G_BM - 1) / (mb * G_BM));
     const size_t need = (size_t)splitk * m * g.ldw * sizeof(float);
     if (tiles > kGemmSems || need > ((size_t)1 << 30)) {
       splitk = 1;
@@ -854,12 +931,15 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
     }
     g.splitk = splitk;
   }
-  if (ng == 1 && mb == 4) return launch<1, 4>(g, maps, m, t->n_tiles, st);
-  if (ng == 2 && mb == 4) return launch<2, 4>(g, maps, m, t->n_tiles, st);
-  if (ng == 4 && mb == 2) return launch<4, 2>(g, maps, m, t->n_tiles, st);
-  if (ng == 4) return launch<4, 1>(g, maps, m, t->n_tiles, st);
-  if (ng == 2 && mb == 2) return launch<2, 2>(g, maps, m, t->n_tiles, st);
-  if (ng == 2) return launch<2, 1>(g, maps, m, t->n_tiles, st);
-  if (mb == 2) return launch<1, 2>(g, maps, m, t->n_tiles, st);
-  return launch<1, 1>(g, maps, m, t->n_tiles, st);
+#define PMPD_GEMM_LAUNCH(NG_, MB_) \
+  return cl == 2 ? launch<NG_, MB_, 2>(g, maps, m, t->n_tiles, st) : launch<NG_, MB_, 1>(g, maps, m, t->n_tiles, st)
+  if (ng == 1 && mb == 4) PMPD_GEMM_LAUNCH(1, 4);
+  if (ng == 2 && mb == 4) PMPD_GEMM_LAUNCH(2, 4);
+  if (ng == 4 && mb == 2) PMPD_GEMM_LAUNCH(4, 2);
+  if (ng == 4) PMPD_GEMM_LAUNCH(4, 1);
+  if (ng == 2 && mb == 2) PMPD_GEMM_LAUNCH(2, 2);
+  if (ng == 2) PMPD_GEMM_LAUNCH(2, 1);
+  if (mb == 2) PMPD_GEMM_LAUNCH(1, 2);
+  PMPD_GEMM_LAUNCH(1, 1);
+#undef PMPD_GEMM_LAUNCH
 }

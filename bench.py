@@ -307,6 +307,44 @@ def emit(obj: dict) -> None:
         sys.stdout.flush()
 
 
+def tp_probe() -> int:
+    """Child of one rank (bench.py --tp-probe): a few tensor-parallel engine tokens on a small stack
+    in a process group of its own.  Its ranks' kernels add into each other's symmetric memory over
+    NVLink; if that protocol cannot complete here, the parent kills this process instead of its own
+    (a kernel waiting on a peer cannot be recovered inside the process that launched it)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2410_13461_b200.stack import MOBILELLAMA_1B4, TPEngineStack
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    import datetime
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local), timeout=datetime.timedelta(seconds=120))
+    world, rank = dist.get_world_size(), dist.get_rank()
+    st = TPEngineStack(MOBILELLAMA_1B4, 16, world, seed=7, group=dist.group.WORLD, rank=rank)
+    for _ in range(4):
+        st.token()
+    torch.cuda.synchronize()
+    dist.barrier()
+    dist.destroy_process_group()
+    print(f"tensor-parallel engine probe: rank {rank} of {world} completed 4 tokens", file=sys.stderr)
+    return 0
+
+
+def run_tp_probe(timeout_s: float = 240.0) -> bool:
+    """Run tp_probe() in a child process per rank (own rendezvous port); True when it finished."""
+    import subprocess
+    env = dict(os.environ)
+    env["MASTER_PORT"] = str(int(os.environ.get("MASTER_PORT", "29500")) + 11)
+    env.setdefault("MASTER_ADDR", "127.0.0.1")
+    env.pop("TORCHELASTIC_USE_AGENT_STORE", None)  # (torchrun's agent hosts the parent's store, not this one)
+    try:
+        r = subprocess.run([sys.executable, os.path.abspath(__file__), "--tp-probe"], env=env, timeout=timeout_s,
+                           stdout=sys.stderr, stderr=sys.stderr)
+        return r.returncode == 0
+    except subprocess.TimeoutExpired:
+        return False
+
+
 def main():
     global _REAL_STDOUT
     sys.stdout.flush()
@@ -322,7 +360,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--no-prefill", action="store_true", help="skip the prefill GEMM section")
     ap.add_argument("--no-model", action="store_true", help="skip the model-level (BASELINE config 2) section")
+    ap.add_argument("--tp-probe", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.tp_probe:
+        return tp_probe()
 
     from paper_2410_13461_b200.stack import LLAMA2_7B, MOBILELLAMA_1B4, algorithmic_bytes
     shape = LLAMA2_7B if args.shape == "7b" else MOBILELLAMA_1B4
@@ -340,13 +381,26 @@ def main():
     # PMPD_BENCH_TP=1 runs the tensor-parallel branch at world 1 under torchrun (a 1-GPU check of
     # the NCCL-in-graph path the driver's N>1 runs take)
     tp_mode = world > 1 or os.environ.get("PMPD_BENCH_TP") == "1"
+    # N > 1: tensor parallelism inside the engine by default (PMPD_TP_ENGINE=0: per-op GEMVs + NCCL)
+    tp_engine = tp_mode and os.environ.get("PMPD_TP_ENGINE", "1") == "1"
+    probe_ok = True
+    probe = tp_engine and (world > 1 or os.environ.get("PMPD_TP_PROBE") == "1")  # (the latter: a 1-GPU check)
+    if probe:
+        probe_ok = run_tp_probe()
     if tp_mode:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if probe:
+            flag = torch.tensor([1 if probe_ok else 0], dtype=torch.int32, device="cuda")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 0:
+                # the fused path did not complete on every rank in the probe: measure the per-op
+                # GEMV + NCCL tensor-parallel path instead of hanging the job
+                print("tensor-parallel engine probe failed on some rank: falling back to per-op GEMVs + NCCL",
+                      file=sys.stderr)
+                os.environ["PMPD_TP_ENGINE"] = "0"
+                tp_engine = False
     assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
-
-    # N > 1: tensor parallelism inside the engine by default (PMPD_TP_ENGINE=0: per-op GEMVs + NCCL)
-    tp_engine = tp_mode and os.environ.get("PMPD_TP_ENGINE", "1") == "1"
     if tp_engine:
         # tensor parallel INSIDE the engine: each rank one launch per token, the row-parallel
         # all-reduce = counted additions into every rank's symmetric-memory copy over NVLink

@@ -118,6 +118,22 @@ struct TileCursor {
   PMPD_DEV int stage_end(int T1, int KT) const { return min(min(t + STILES, T1), t - kt + KT); }
 };
 
+// packed f32x2 arithmetic (sm_100 FMUL2 / FFMA2: each lane an IEEE mul.rn / fma.rn)
+PMPD_DEV float2 fmul2(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "mul.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+PMPD_DEV float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("{\n\t.reg .b64 a, b, c, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\tmov.b64 c, {%6, %7};\n\t"
+      "fma.rn.f32x2 d, a, b, c;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+
 // ---------------------------------------------------------------- consumer
 // State of one consumer warp; run() is instantiated per (layout, p_max, p) so
 // that the whole tile loop is specialised for the active precision.
@@ -141,10 +157,37 @@ struct Consumer {
   float bias[MB];  // KN: this lane's part of sum_k x*min
   float qs[MB];    // KN: activation quantisation scale 32767 / (max|x_b| * max step_g)
   float ql[2];     // KN: qs of this lane's flush rows b = 2*tig + {0,1} (keeps qs[] in registers)
+  // KN at batch 5..8: f16 HMMA (mma.sync m16n8k16, the batch rows are the 8 B columns).  The
+  // decoded u8 bucket bytes become f16 SUBNORMALS (byte * 2^-24, exact: high byte zero) with one
+  // PRMT per pair, and B = x * step * s (s a per-row power of two) is built in registers per tile
+  // with no shared-memory round trip; f32 accumulation across the n-group's tiles.  The int8 path
+  // re-quantised x * step per tile and row (~80 instructions per tile and row pair) and needed a
+  // second IMMA per fragment at batch 8: batch 8 cost 2.8-4x batch 1.  (Batch 2..4 keep the
+  // balanced-digit IMMA: one IMMA per fragment there, measured faster than this path.)
+  static constexpr bool KH = KN && MB == MAXM;
+  float2 hbias2; // KH: this lane's part of sum_k x[gq][k] * min (row gq), two partial sums
+  const __half* xrow;  // KH, staged x: this lane's row gq
+  float hs;      // KH: B scale of row gq (power of two: max |x * step * s| <= 2^14)
+  float hl[2];   // KH: 1 / s of the lane's output rows 2 tig + {0, 1}
   // KN with unstaged activations: this lane's x pairs (raw half2) of the current stage's
   // tiles, loaded one stage ahead so the L2 latency overlaps the previous stage's MMAs
-  static constexpr bool PF = KN && !XS;
+  static constexpr bool PF = KN && !XS && !KH;
   uint32_t xw[TPW][MB];
+  // KH with unstaged activations: this lane's 16 x of row gq per tile, loaded one stage ahead
+  static constexpr bool HPF = KH && !XS;
+  uint2 xh[TPW][2][2];
+  PMPD_DEV void prefetch_xh(uint2 (&dst)[TPW][2][2], int kt0, int cnt) const {
+    const bool rowok = gq < M;
+#pragma unroll
+    for (int q = 0; q < TPW; ++q)
+#pragma unroll
+      for (int cch = 0; cch < 2; ++cch)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int k = (kt0 + warp + q * NCW) * kTile + 32 * cch + 16 * h + 4 * tig;
+          dst[q][cch][h] = (rowok && warp + q * NCW < cnt) ? make_uint2(xword(gq, k), xword(gq, k + 2)) : make_uint2(0u, 0u);
+        }
+  }
   // KN, batch <= 4: balanced digits v = 256*hi + lo (both s8), hi of row b in B column 2b and lo in
   // column 2b+1 -> ONE u8 x s8 IMMA per fragment (lane tig = b holds both sums); batch 8 keeps two
   static constexpr bool BAL = KN && MB <= 4;
@@ -171,12 +214,28 @@ struct Consumer {
       }
 #pragma unroll
     for (int b = 0; b < MB; ++b) bias[b] = 0.f;
+    hbias2 = make_float2(0.f, 0.f);
+  }
+
+  // floor to a power of two, clamped to [2^-100, 2^100]
+  static PMPD_DEV float pow2_floor(float v) {
+    v = fminf(fmaxf(v, 7.8886091e-31f), 1.2676506e30f);
+    return __uint_as_float(__float_as_uint(v) & 0x7F800000u);
   }
 
   // set the KN activation scale for n-group ng
   PMPD_DEV void enter_group(int ng) {
     (void)kQMax;  // KN only
-    if constexpr (KN) {
+    if constexpr (KH) {
+      const float idm = __ldg(a.aux + ng);
+      const float mg = mx[min(gq, MB - 1)];
+      hs = (mg > 0.f && idm > 0.f) ? pow2_floor(16384.f * idm / mg) : 1.f;
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const float m = mx[min(2 * tig + cc, MB - 1)];
+        hl[cc] = (m > 0.f && idm > 0.f) ? 1.f / pow2_floor(16384.f * idm / m) : 1.f;
+      }
+    } else if constexpr (KN) {
       const float idm = __ldg(a.aux + ng);
 #pragma unroll
       for (int b = 0; b < MB; ++b) {
@@ -321,6 +380,88 @@ struct Consumer {
     }
   }
 
+  // ------------------------------------------------------------- KN tiles at batch 2..8 (HMMA)
+  // The u8 fragments of tile_kn, read as f16 pairs: for k-chunk cch, A' = {a0 bytes 0-1, a1 bytes
+  // 0-1, a0 bytes 2-3, a1 bytes 2-3} (and a2/a3 for the chunk's upper 16 k) is an m16n8k16 A
+  // fragment whose logical k 2tig + e / 2tig + 8 + e are the physical k 4tig + e / 4tig + 2 + e;
+  // B carries x * step of row gq at the same physical k, so each lane's B values are 4 runs of 4
+  // consecutive k of its own row.
+  template <int P>
+  PMPD_DEV void tile_kh(const uint8_t* st, int wslot, int kt, int cnt) {
+    uint32_t pw[TPW][4][4];
+    bool live[TPW];
+#pragma unroll
+    for (int q = 0; q < TPW; ++q) {
+      const int sl = wslot + q * NCW;
+      live[q] = sl < cnt;
+      if (live[q]) load_planes<P>(st, sl, pw[q]);
+    }
+    const bool rowok = gq < M;
+#pragma unroll
+    for (int q = 0; q < TPW; ++q) {
+      if (!live[q]) continue;
+      const int sl = wslot + q * NCW;
+      const float* sc = reinterpret_cast<const float*>(st + PMAX * STILES * kTilePlaneBytes + sl * kTileScaleBytes);
+      const int k0 = (kt + q * NCW) * kTile;
+      // this lane's 16 x of row gq: staged rows are zero past M and past K (one 8-byte load per
+      // 4 k); unstaged rows come from global memory with bounds
+      uint2 xr[2][2];
+#pragma unroll
+      for (int cch = 0; cch < 2; ++cch)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int k = k0 + 32 * cch + 16 * h + 4 * tig;
+          if constexpr (XS) {
+            xr[cch][h] = *reinterpret_cast<const uint2*>(xrow + k);
+          } else {
+            xr[cch][h] = xh[q][cch][h];  // (prefetched a stage ahead by run())
+            (void)rowok;
+          }
+        }
+      uint32_t bfr[2][2][2];  // [cch][h][b0 | b1]
+      const float2 hs2 = make_float2(hs, hs);
+#pragma unroll
+      for (int cch = 0; cch < 2; ++cch)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int kl = 32 * cch + 16 * h + 4 * tig;
+          const float2 x01 = __half22float2(*reinterpret_cast<const __half2*>(&xr[cch][h].x));
+          const float2 x23 = __half22float2(*reinterpret_cast<const __half2*>(&xr[cch][h].y));
+          const float4 d = *reinterpret_cast<const float4*>(sc + kl);
+          const float4 mn = *reinterpret_cast<const float4*>(sc + 64 + kl);
+          hbias2 = ffma2(x01, make_float2(mn.x, mn.y), hbias2);
+          hbias2 = ffma2(x23, make_float2(mn.z, mn.w), hbias2);
+          const float2 v01 = fmul2(fmul2(x01, make_float2(d.x, d.y)), hs2);
+          const float2 v23 = fmul2(fmul2(x23, make_float2(d.z, d.w)), hs2);
+          const __half2 b0 = __floats2half2_rn(v01.x, v01.y);
+          const __half2 b1 = __floats2half2_rn(v23.x, v23.y);
+          bfr[cch][h][0] = *reinterpret_cast<const uint32_t*>(&b0);
+          bfr[cch][h][1] = *reinterpret_cast<const uint32_t*>(&b1);
+        }
+#pragma unroll
+      for (int cch = 0; cch < 2; ++cch) {
+        const uint32_t pe[4] = {pw[q][0][2 * cch], pw[q][1][2 * cch], pw[q][2][2 * cch], pw[q][3][2 * cch]};
+        const uint32_t po[4] = {pw[q][0][2 * cch + 1], pw[q][1][2 * cch + 1], pw[q][2][2 * cch + 1],
+                                pw[q][3][2 * cch + 1]};
+#define PMPD_KH_MTILE(T)                                                                                  \
+  {                                                                                                       \
+    uint32_t a0, a1, a2, a3;                                                                              \
+    nibble_to_u8<PMAX, P, T>(merge_planes<PMAX, P, T>(pe), a0, a1);                                       \
+    nibble_to_u8<PMAX, P, T>(merge_planes<PMAX, P, T>(po), a2, a3);                                       \
+    mma_f16_16816(acc[T], __byte_perm(a0, 0u, 0x4140), __byte_perm(a1, 0u, 0x4140), __byte_perm(a0, 0u, 0x4342), \
+                  __byte_perm(a1, 0u, 0x4342), bfr[cch][0][0], bfr[cch][0][1]);                           \
+    mma_f16_16816(acc[T], __byte_perm(a2, 0u, 0x4140), __byte_perm(a3, 0u, 0x4140), __byte_perm(a2, 0u, 0x4342), \
+                  __byte_perm(a3, 0u, 0x4342), bfr[cch][1][0], bfr[cch][1][1]);                           \
+  }
+        PMPD_KH_MTILE(0)
+        PMPD_KH_MTILE(1)
+        PMPD_KH_MTILE(2)
+        PMPD_KH_MTILE(3)
+#undef PMPD_KH_MTILE
+      }
+    }
+  }
+
   // ------------------------------------------------------------- NK tile (HMMA)
   template <int P>
   PMPD_DEV void tile_nk(const uint8_t* st, int wslot, int kt) {
@@ -402,7 +543,10 @@ struct Consumer {
           const int b = BAL ? tig : 2 * tig + cc;
           if (b < Me && (!BAL || cc == 0)) {
             float v;
-            if constexpr (BAL) {
+            if constexpr (KH) {
+              // f16 subnormal weights carry 2^-24, m-tile T bytes 2^T, B the row's scale s
+              v = acc[t][2 * h + cc] * (16777216.f / (float)(1 << t)) * hl[cc];
+            } else if constexpr (BAL) {
               // columns 2b / 2b+1 of this lane = high / low digit sums of row b
               const float q = ql[0];
               const float ds = q > 0.f ? __fdividef(1.f, q) * (1.f / (float)(1 << t)) : 0.f;
@@ -418,7 +562,13 @@ struct Consumer {
             rw[(16 * t + gq + 8 * h) * MB + b] = v;
           }
         }
-    if constexpr (KN) {
+    if constexpr (KH) {
+      // this lane's bias is row gq's: sum over the 4 lanes of the row
+      float hb = hbias2.x + hbias2.y;
+      hb += __shfl_xor_sync(0xffffffffu, hb, 1);
+      hb += __shfl_xor_sync(0xffffffffu, hb, 2);
+      if (tig == 0 && gq < Me) redb[warp * MB + gq] = hb;
+    } else if constexpr (KN) {
 #pragma unroll
       for (int b = 0; b < MB; ++b)
         if (MB == 1 || b < M) {
@@ -488,10 +638,18 @@ struct Consumer {
     TileCursor cur{T0, T0 / KT, T0 % KT};
     enter_group(cur.ng);
     if constexpr (PF) prefetch_x(xw, cur.kt, cur.stage_end(T1, KT) - cur.t);
+    if constexpr (HPF) prefetch_xh(xh, cur.kt, cur.stage_end(T1, KT) - cur.t);
     while (cur.t < T1) {
       const int end = cur.stage_end(T1, KT);
       const int slot = si % PL::kNst;
       uint32_t xn[TPW][MB];
+      uint2 xhn[TPW][2][2];
+      if constexpr (HPF) {
+        int nkt = cur.kt + (end - cur.t);
+        if (nkt == KT) nkt = 0;
+        const TileCursor nx{end, 0, nkt};
+        prefetch_xh(xhn, nkt, end < T1 ? nx.stage_end(T1, KT) - end : 0);
+      }
       if constexpr (PF) {
         int nkt = cur.kt + (end - cur.t);
         if (nkt == KT) nkt = 0;
@@ -506,7 +664,9 @@ struct Consumer {
 #else
       if (warp < end - cur.t) {
 #endif
-        if constexpr (KN) {
+        if constexpr (KH) {
+          tile_kh<P>(smem + PL::kRing + slot * PL::kStage, warp, cur.kt + warp, end - cur.t);
+        } else if constexpr (KN) {
           tile_kn<P>(smem + PL::kRing + slot * PL::kStage, warp, cur.kt + warp, end - cur.t);
         } else {
 #pragma unroll
@@ -524,6 +684,14 @@ struct Consumer {
         for (int q = 0; q < TPW; ++q)
 #pragma unroll
           for (int b = 0; b < MB; ++b) xw[q][b] = xn[q][b];
+      }
+      if constexpr (HPF) {
+#pragma unroll
+        for (int q = 0; q < TPW; ++q)
+#pragma unroll
+          for (int cch = 0; cch < 2; ++cch)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) xh[q][cch][h] = xhn[q][cch][h];
       }
       const int ng = cur.ng;
       cur.kt += end - cur.t;
@@ -708,10 +876,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) qgemv_kernel(const GemvArgs a) {
       named_bar_sync(1, NCW * 32);
     }
   }
+  if constexpr (XS && LAYOUT == PMPD_LAYOUT_KN && MB == MAXM) {
+    // the f16 HMMA path reads row gq of every lane: rows past m are zero
+    __half* xs = reinterpret_cast<__half*>(smem_raw + PL::kXs);
+    const int kp = KT * kTile;
+    for (int i = Me * kp + threadIdx.x * 8; i < MB * kp; i += NCW * 32 * 8)
+      *reinterpret_cast<uint4*>(xs + i) = make_uint4(0u, 0u, 0u, 0u);
+  }
   named_bar_sync(1, NCW * 32);
   if constexpr (XS) {
     cs.xs = reinterpret_cast<__half*>(smem_raw + PL::kXs);
     cs.xld = xsld;
+    cs.xrow = cs.xs + (int64_t)cs.gq * xsld;
   } else {
     cs.xs = a.x;
     cs.xld = a.ldx;
@@ -758,6 +934,12 @@ int launch_m(const GemvArgs& a, int grid, cudaStream_t s) {
   return PMPD_OK;
 }
 
+// rows of x the batch-2..8 kernel stages: KN at batch 5..8 reads all 8 rows (the rows past m are
+// zero-filled for the f16 HMMA path), NK and the smaller row bounds the m given
+inline int rows_staged(int layout, int m) {
+  return layout == PMPD_LAYOUT_KN && m > 4 ? MAXM : m;
+}
+
 template <int LAYOUT, int PMAX>
 int launch(const GemvArgs& a, int grid, cudaStream_t s) {
   if (a.m == 1)
@@ -765,7 +947,7 @@ int launch(const GemvArgs& a, int grid, cudaStream_t s) {
                                         : launch_m<LAYOUT, PMAX, 1, false>(a, grid, s);
   // batch 2..8: the row count is a template bound (2, 4 or 8) so every per-row loop unrolls
   // into registers; rows past m are masked
-  const bool xs = a.m * a.k_tiles * kTile <= kXsMulti;
+  const bool xs = rows_staged(LAYOUT, a.m) * a.k_tiles * kTile <= kXsMulti;
   if (a.m == 2)
     return xs ? launch_m<LAYOUT, PMAX, 2, true>(a, grid, s) : launch_m<LAYOUT, PMAX, 2, false>(a, grid, s);
   if (a.m <= 4)
@@ -885,7 +1067,7 @@ int gemv_impl(const pmpd_qtensor* t, const GemvIn& in, int32_t m, const int32_t*
   a.u_off = in.u_off;
   if (in.mode != 0) {
     const int kp = t->k_tiles * kTile;
-    const bool staged = m == 1 ? kp <= kXsMaxK : m * kp <= kXsMulti;
+    const bool staged = m == 1 ? kp <= kXsMaxK : rows_staged(t->layout, m) * kp <= kXsMulti;
     if (!staged) return fail(PMPD_ERR_CONFIG, "fused GEMV input needs the staged-activation path (m*K too large)");
     if (in.mode == 1 && !in.gain) return fail(PMPD_ERR_CONFIG, "RMSNorm input needs a gain vector");
     if (in.mode == 2 && in.u_off < t->k) return fail(PMPD_ERR_CONFIG, "SwiGLU input needs u_off >= K");

@@ -27,6 +27,7 @@
 // Epilogue: tcgen05.ld (32x32b) of the accumulator rows -> smem tile -> alpha * acc (+ y) -> y
 // in coalesced row segments.
 #include <cuda.h>
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cuda_fp16.h>
@@ -906,7 +907,9 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
   g.ldw = t->n_tiles * G_NG1;
   g.par_reduce = 0;
   if (splitk > 1) {
-    // split-K workspace (grown on demand; launches on one stream reuse it in order)
+    // split-K workspace (grown on demand; launches on one stream reuse it in order). A buffer
+    // that is outgrown is retired, never freed: a CUDA graph captured earlier (the model's graphed
+    // prefill) still holds its address.
     static float* ws_buf = nullptr;
     static size_t ws_cap = 0;
     const int tiles = nblk_pad * ((m + mb * G_BM - 1) / (mb * G_BM));
@@ -915,11 +918,11 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
       splitk = 1;
     } else {
       if (need > ws_cap) {
-        if (ws_buf) cudaFree(ws_buf);
-        ws_buf = nullptr;
-        ws_cap = 0;
-        if (cudaMalloc(&ws_buf, need) != cudaSuccess) return fail(PMPD_ERR_CUDA, "prefill gemm: split-K workspace");
-        ws_cap = need;
+        const size_t want = std::max(need, std::min(2 * ws_cap, (size_t)1 << 30));
+        float* nb = nullptr;
+        if (cudaMalloc(&nb, want) != cudaSuccess) return fail(PMPD_ERR_CUDA, "prefill gemm: split-K workspace");
+        ws_buf = nb;
+        ws_cap = want;
       }
       void* sp = nullptr;
       if (cudaGetSymbolAddress(&sp, g_gemm_sem) != cudaSuccess) return fail(PMPD_ERR_CUDA, "prefill gemm counters");

@@ -501,6 +501,8 @@ def _forward(model: ModelVariants, p: int, tokens: Sequence[int], cache: KVCache
     if ids.size and (ids.min() < 0 or ids.max() >= cfg.vocab_size):
         raise InputError(f"token id outside vocabulary of size {cfg.vocab_size}")
     dw = model.device()
+    if T0 == 0 and n > 1 and _PREFILL_GRAPH:
+        return _prefill_graphed(model, dw, p, ids, cache)
     buf = _Buffers(cfg, n, dw.ws_bytes)
     buf.ids.copy_(torch.from_numpy(ids.astype(np.int32)))
     buf.p.fill_(p if p != FULL_PRECISION else 0)
@@ -508,6 +510,61 @@ def _forward(model: ModelVariants, p: int, tokens: Sequence[int], cache: KVCache
     _capi.call("pmpd_add_i32", cache.T_dev.data_ptr(), n, _stream())
     cache.T = T0 + n
     return buf.logits[:n]
+
+
+_PREFILL_GRAPH = os.environ.get("PMPD_PREFILL_GRAPH", "1") == "1"
+_PREFILL_GRAPHS_KEPT = 4
+
+
+class _PrefillGraph:
+    """A prompt pass of n rows at precision p from an empty cache as ONE CUDA graph (the ~10
+    launches per layer of `_run_layers` are ctypes calls at ~5 µs of host time each, so an eager
+    short-prompt prefill is host-bound). The graph runs on its own static buffers and an n-row KV
+    cache; a replay is followed by copying those rows into the caller's cache."""
+
+    def __init__(self, model: ModelVariants, dw: _DeviceWeights, p: int, n: int):
+        cfg = model.config
+        self.n, self.p = n, p
+        self.buf = _Buffers(cfg, n, dw.ws_bytes)
+        self.buf.p.fill_(p if p != FULL_PRECISION else 0)
+        self.cache = KVCache(cfg.n_layers, cfg.d_model, n)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm-up pass: lazy attributes, tensor maps, library handles
+            _run_layers(model, dw, self.buf, n, self.cache, p)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            _run_layers(model, dw, self.buf, n, self.cache, p)
+        torch.cuda.synchronize()
+        self.graph = g
+
+    def run(self, ids: np.ndarray, cache: KVCache) -> torch.Tensor:
+        n = self.n
+        self.buf.ids.copy_(torch.from_numpy(ids.astype(np.int32)), non_blocking=False)
+        self.graph.replay()
+        cache.k[:, :n].copy_(self.cache.k)
+        cache.v[:, :n].copy_(self.cache.v)
+        # the static buffers are reused by the next replay: hand the caller its own logits
+        return self.buf.logits[:n].clone()
+
+
+def _prefill_graphed(model: ModelVariants, dw: _DeviceWeights, p: int, ids: np.ndarray,
+                     cache: KVCache) -> torch.Tensor:
+    n = int(ids.size)
+    graphs = model.__dict__.setdefault("_prefill_graphs", {})
+    key = (n, p, id(dw))
+    pg = graphs.pop(key, None)
+    if pg is None:
+        while len(graphs) >= _PREFILL_GRAPHS_KEPT:  # keep the most recently used shapes
+            graphs.pop(next(iter(graphs)))
+        pg = _PrefillGraph(model, dw, p, n)
+    graphs[key] = pg
+    logits = pg.run(ids, cache)
+    _capi.call("pmpd_add_i32", cache.T_dev.data_ptr(), n, _stream())
+    cache.T = n
+    return logits
 
 
 def prefill(model: ModelVariants, p: int, prompt: Sequence[int], collect_attn: list | None = None):

@@ -328,3 +328,24 @@ def test_device_status_word_raises():
     with pytest.raises(ContractViolation):
         ws.check()
     assert ws.status() == 0
+
+
+@pytest.mark.parametrize("p", [4, 2, 16])
+def test_prefill_graph_bit_identical_to_eager(toy, p, monkeypatch):
+    """The graphed prompt pass (one CUDA graph per (rows, p), replayed into the caller's cache) gives
+    bit-identical logits and KV rows to the eager pass, on its first call (capture) and on replays
+    with different prompts of the same length; decoding continues identically from either cache."""
+    rng = np.random.default_rng(5)
+    prompts = [rng.integers(0, toy.config.vocab_size, size=40).tolist() for _ in range(3)]
+    for prompt in prompts:
+        monkeypatch.setattr(tinylm, "_PREFILL_GRAPH", False)
+        le, ce = tinylm.prefill(toy, p, prompt)
+        monkeypatch.setattr(tinylm, "_PREFILL_GRAPH", True)
+        lg, cg = tinylm.prefill(toy, p, prompt)
+        assert torch.equal(le, lg)
+        assert cg.T == ce.T == len(prompt) and int(cg.T_dev) == len(prompt)
+        assert torch.equal(ce.k, cg.k) and torch.equal(ce.v, cg.v)
+        tok = int(torch.argmax(le))
+        de, _ = tinylm.decode_step(toy, p, tok, ce)
+        dg, _ = tinylm.decode_step(toy, p, tok, cg)
+        assert torch.equal(de, dg)

@@ -382,6 +382,8 @@ _FUSE_DECODE = os.environ.get("PMPD_FUSE_DECODE", "0") == "1"  # fused norm/SwiG
 
 # prefill rows from which causal self-attention over an empty cache goes through torch SDPA
 _SDPA_MIN_ROWS = int(os.environ.get("PMPD_SDPA_MIN_ROWS", "256"))
+# the same inside a graphed prefill, where the library call's host overhead is paid once at capture
+_SDPA_MIN_ROWS_GRAPHED = int(os.environ.get("PMPD_SDPA_MIN_ROWS_GRAPHED", "16"))
 
 
 def _fused_linear(pks: list, mode: int, xf: torch.Tensor, gain, u_off: int, out: torch.Tensor, buf: _Buffers,
@@ -396,7 +398,7 @@ def _fused_linear(pks: list, mode: int, xf: torch.Tensor, gain, u_off: int, out:
 
 
 def _run_layers(model: ModelVariants, dw: _DeviceWeights, buf: _Buffers, n: int, cache: KVCache, p_host,
-                seq_caches: list | None = None) -> None:
+                seq_caches: list | None = None, sdpa_min_rows: int | None = None) -> None:
     """Embedding + all blocks + final norm + head for n tokens in buf.ids; logits -> buf.logits[:n].
     ``seq_caches``: the n rows are the next tokens of n independent sequences (batched decode),
     row j attending over seq_caches[j]; the linear layers run as one n-row GEMV."""
@@ -440,7 +442,7 @@ def _run_layers(model: ModelVariants, dw: _DeviceWeights, buf: _Buffers, n: int,
             _capi.call("pmpd_rope_kv", qkv.data_ptr(), 3 * d, n, d, dh, dw.cos.data_ptr(), dw.sin.data_ptr(),
                        cache.T_dev.data_ptr(), cache.capacity, q.data_ptr(), cache.k[i].data_ptr(),
                        cache.v[i].data_ptr(), s)
-            if n >= _SDPA_MIN_ROWS and cache.T == 0:
+            if n >= (_SDPA_MIN_ROWS if sdpa_min_rows is None else sdpa_min_rows) and cache.T == 0:
                 # long-prompt prefill from an empty cache (>= 256 rows; below that the per-query kernel
                 # wins over the library call overhead): causal attention of the n new rows over
                 # themselves (tinylm.py:349-358) through torch's fused SDPA (a library kernel, like
@@ -531,12 +533,12 @@ class _PrefillGraph:
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):  # warm-up pass: lazy attributes, tensor maps, library handles
-            _run_layers(model, dw, self.buf, n, self.cache, p)
+            _run_layers(model, dw, self.buf, n, self.cache, p, sdpa_min_rows=_SDPA_MIN_ROWS_GRAPHED)
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            _run_layers(model, dw, self.buf, n, self.cache, p)
+            _run_layers(model, dw, self.buf, n, self.cache, p, sdpa_min_rows=_SDPA_MIN_ROWS_GRAPHED)
         torch.cuda.synchronize()
         self.graph = g
 

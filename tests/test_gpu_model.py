@@ -29,6 +29,12 @@ def toy():
     return tinylm.ModelVariants.from_random(cfg, quant.PrecisionSet((4, 3, 2)), seed=11)
 
 
+@pytest.fixture(scope="module")
+def oracle_toy():
+    return om.Model.from_random(om.Config(n_layers=4, n_heads=4, d_model=128, d_ff=256, max_context=256), (4, 3, 2),
+                                seed=11)
+
+
 def host(t):
     return t.double().cpu().numpy()
 
@@ -335,6 +341,8 @@ def test_prefill_graph_bit_identical_to_eager(toy, p, monkeypatch):
     """The graphed prompt pass (one CUDA graph per (rows, p), replayed into the caller's cache) gives
     bit-identical logits and KV rows to the eager pass, on its first call (capture) and on replays
     with different prompts of the same length; decoding continues identically from either cache."""
+    # same attention kernel on both paths (the graphed pass otherwise switches to SDPA from 16 rows)
+    monkeypatch.setattr(tinylm, "_SDPA_MIN_ROWS_GRAPHED", tinylm._SDPA_MIN_ROWS)
     rng = np.random.default_rng(5)
     prompts = [rng.integers(0, toy.config.vocab_size, size=40).tolist() for _ in range(3)]
     for prompt in prompts:
@@ -349,3 +357,19 @@ def test_prefill_graph_bit_identical_to_eager(toy, p, monkeypatch):
         de, _ = tinylm.decode_step(toy, p, tok, ce)
         dg, _ = tinylm.decode_step(toy, p, tok, cg)
         assert torch.equal(de, dg)
+
+
+@pytest.mark.parametrize("n", [16, 40, 100])
+def test_prefill_graph_sdpa_matches_oracle(toy, oracle_toy, n):
+    """The graphed prompt pass runs causal attention through SDPA from 16 rows: its logits and the
+    decode step that follows stay within the north-star tolerance of the oracle."""
+    rng = np.random.default_rng(n)
+    prompt = rng.integers(0, toy.config.vocab_size, size=n).tolist()
+    for p in (4, 2):
+        lg, cache = tinylm.prefill(toy, p, prompt)
+        ref, rc = om.prefill(oracle_toy, p, prompt)
+        assert rel_l2(host(lg), ref) < TOL, (n, p)
+        tok = om.greedy(ref)
+        d, _ = tinylm.decode_step(toy, p, tok, cache)
+        rd, _ = om.decode_step(oracle_toy, p, tok, rc)
+        assert rel_l2(host(d), rd) < TOL, (n, p)

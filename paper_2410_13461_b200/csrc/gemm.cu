@@ -44,6 +44,9 @@ namespace {
 constexpr int kGemmSems = 1 << 16;
 __device__ unsigned g_gemm_sem[kGemmSems];
 
+#ifndef PMPD_GEMM_PDL
+#define PMPD_GEMM_PDL 1  // programmatic dependent launch (weights streamed before the wait on x)
+#endif
 constexpr int G_BM = 128;       // tokens per UMMA M block
 constexpr int G_NG1 = 64;       // outputs per packed n-group
 constexpr int G_KC = 64;        // K per chunk (one packed tile)
@@ -457,6 +460,9 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
   if constexpr (CL > 1) cluster_sync_all();  // every CTA's barriers exist before any multicast lands
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: the next kernel of the stream may start its prologue (and, when
+  // it is a GEMM, its weight stream and dequantization) once every CTA of this grid is running
+  if (PMPD_GEMM_PDL) pdl_launch_dependents();
   const int crank = CL > 1 ? (int)cluster_rank() : 0;
   constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1);
   // this CTA's K chunks: all of them, or its split-K slice [kbase, kbase + KC)
@@ -476,8 +482,16 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
 #endif
       int cx = 0, cw = 0, sx = 0, sw = 0;
       uint32_t xph = 0, wph = 0;
+      // x is the previous kernel's output: it is loaded only after griddepcontrol.wait, which
+      // this thread reaches once the weight ring's first fill is issued (the weights and the
+      // precision word do not depend on the previous kernel)
+      bool xok = !PMPD_GEMM_PDL;
       while (cx < KC || cw < KC) {
         bool idle = true;
+        if (!xok && (cw == KC || cw == C::NSW)) {
+          pdl_wait();
+          xok = true;
+        }
         if (cw < KC && (cw < C::NSW || mbar_try_wait(&wempty[sw], wph ^ 1u))) {
           uint8_t* dst = wring + sw * C::STAGE_W;
           mbar_arrive_expect_tx(&wfull[sw], (uint32_t)((p + 1) * C::WR));  // full boxes (zero-filled past the matrix)
@@ -490,7 +504,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
           }
           idle = false;
         }
-        if (cx < KC && (cx < C::NSX || mbar_try_wait(&xempty[sx], xph ^ 1u))) {
+        if (xok && cx < KC && (cx < C::NSX || mbar_try_wait(&xempty[sx], xph ^ 1u))) {
           uint8_t* dst = xring + sx * C::STAGE_X;
 #ifdef GEMM_SKIP_X  // timing probe only: x is not loaded (wrong results)
           mbar_arrive(&xfull[sx]);
@@ -590,6 +604,9 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
   // all MMAs done
   mbar_wait(done_bar, 0);
   tc_fence_after();
+  // (the producer's griddepcontrol.wait returned before any MMA: the previous kernel has
+  // completed; this makes its writes to y, the split-K workspace and the counters visible here)
+  if (PMPD_GEMM_PDL) pdl_wait();
   // epilogue, per accumulator block: TMEM -> smem tile [128 rows][N (+1 pad)] f32 (warp w reads
   // TMEM lanes 32*(w%4).., columns half w/4), then all 256 threads write y in coalesced row
   // segments (the operand ring is free: every MMA has completed and every TMA landed).
@@ -740,13 +757,15 @@ int launch(const GemmArgs& g_in, const GemmMaps& maps, int m, int n_tiles, cudaS
   cfg.blockDim = dim3(G_THREADS);
   cfg.dynamicSmemBytes = Cfg<NG, MB>::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = CL;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = PMPD_GEMM_PDL ? 2 : 1;
   if (g.par_reduce) {
     // the splits of a tile wait for each other: only when every CTA of the launch is co-resident
     // (clusters of 2 need SM pairs, so fewer than the SM count may be resident at once)

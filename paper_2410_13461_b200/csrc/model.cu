@@ -49,6 +49,7 @@ PMPD_DEV float block_max(float v, float* sh) {
 // out[m][i] = f16(x[m][i] / sqrt(mean(x[m]^2) + eps) * gain[i])   (tinylm.py:293-295)
 __global__ void rmsnorm_kernel(const float* __restrict__ x, int ldx, const float* __restrict__ gain, int d, float eps,
                                __half* __restrict__ out, int ldo) {
+  pdl_launch_dependents();  // a following PDL GEMV / GEMM may stream its weights meanwhile
   __shared__ float sh[32];
   const float* xr = x + (int64_t)blockIdx.x * ldx;
   float ss = 0.f;
@@ -113,6 +114,7 @@ __global__ void rope_kv_kernel(const float* __restrict__ qkv, int ldq, int d, in
 __global__ void attention_kernel(const float* __restrict__ q, int d, int dh, const __half* __restrict__ kc,
                                  const __half* __restrict__ vc, const int32_t* __restrict__ T_dev, int max_ctx,
                                  float scale, __half* __restrict__ out) {
+  pdl_launch_dependents();  // a following PDL GEMV / GEMM may stream its weights meanwhile
   extern __shared__ float sm[];  // [max_ctx] scores + [dh] q + 32 scratch
   float* sc = sm;
   float* qs = sm + max_ctx;
@@ -200,6 +202,7 @@ __global__ void __cluster_dims__(kSplit, 1, 1) __launch_bounds__(kAttnWarps * 32
                            const int32_t* __restrict__ T_dev, int max_ctx, float scale, __half* __restrict__ out,
                            const float* __restrict__ cos_t, const float* __restrict__ sin_t, int ldq = 0,
                            int64_t sstride = 0) {
+  pdl_launch_dependents();  // the o GEMV (PDL) may stream its weights meanwhile
   constexpr int DH = 32 * DPL;
   __shared__ float w_ml[kAttnWarps][2];
   __shared__ float w_acc[kAttnWarps][DH];
@@ -356,6 +359,7 @@ template <int R>
 __global__ void __launch_bounds__(512) rmsnorm_vec_kernel(const float* __restrict__ x, int ldx,
                                                          const float* __restrict__ gain, int d, float eps,
                                                          __half* __restrict__ out, int ldo) {
+  pdl_launch_dependents();  // a following PDL GEMV / GEMM may stream its weights meanwhile
   __shared__ float sh[32];
   const float4* xr = reinterpret_cast<const float4*>(x + (int64_t)blockIdx.x * ldx);
   const int n4 = d >> 2;
@@ -393,6 +397,7 @@ PMPD_DEV float silu_times(float g, float up) { return g / (1.f + __expf(-g)) * u
 
 __global__ void silu_mul_kernel(const float* __restrict__ u, int ldu, int ff, int m, __half* __restrict__ out,
                                 int ldo, int vec) {
+  pdl_launch_dependents();  // a following PDL GEMV / GEMM may stream its weights meanwhile
   const int r = blockIdx.y;
   const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (r >= m || j0 >= ff) return;

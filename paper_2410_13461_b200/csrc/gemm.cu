@@ -184,6 +184,17 @@ PMPD_DEV void tma_3d_mc(void* dst, const CUtensorMap* map, int c0, int c1, int c
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "h"(mask)
       : "memory");
 }
+// f32 load from the same shared-memory offset in cluster CTA `rank` (distributed shared memory)
+PMPD_DEV uint32_t dsmem_addr(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+PMPD_DEV float ld_dsmem_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr));  // (ordered by the volatile cluster barriers)
+  return v;
+}
 PMPD_DEV void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -219,6 +230,8 @@ struct GemmArgs {
   int ldw;
   int par_reduce; // 1: every CTA of the launch is resident at once, so the S splits of a tile wait for
                   // each other and each sums 1/S of the tile's rows (else the last arriver sums all)
+  int dsm_reduce; // 1: the S splits of a tile are one thread-block cluster (along z) and sum their
+                  // partial tiles through distributed shared memory (no workspace, no counters)
 };
 
 // ------------------------------------------------------------------ weight dequant
@@ -618,6 +631,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
     // when accumulating) and writes y.  The sum order is fixed, so results are bit-reproducible
     // run to run, and no split waits for another (non-last splits simply exit).
     const int sk = g.splitk;
+    const bool dsm = sk > 1 && g.dsm_reduce;
     const int n0 = nt0 * G_NG1;
     constexpr int Q = C::N / 4;  // 4-column quads per row
     for (int mb = 0; mb < mbn; ++mb) {
@@ -631,6 +645,53 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
       }
       named_bar_sync(1, G_DQ);
       const int rows = min(G_BM, g.M - (m0 + mb * G_BM));
+      if (dsm) {
+        // split z of the cluster sums rows [z*rows/S, (z+1)*rows/S) of this block over the S
+        // partial tiles in split order 0..S-1 (the arithmetic of the workspace path below, so the
+        // result is the same bits) and writes y
+        cluster_sync_all();  // every split's partial tile of this block is in its shared memory
+        const int z = blockIdx.z;
+        const int r_lo = (z * rows) / sk, r_hi = ((z + 1) * rows) / sk;
+        for (int qi = tid + r_lo * Q; qi < r_hi * Q; qi += G_DQ) {
+          const int rr = qi / Q, c4 = (qi % Q) * 4, n = n0 + c4;
+          if (n >= g.n_real) continue;
+          const uint32_t la = smem_u32(tile + rr * LDT + c4);
+          float o[4] = {0.f, 0.f, 0.f, 0.f};
+          // every split's 4 values are requested before any is used (one DSMEM round trip)
+          float q[4][4];
+#pragma unroll
+          for (int zz = 0; zz < 4; ++zz) {
+            if (zz < sk) {
+              const uint32_t ra = dsmem_addr(la, (uint32_t)zz);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) q[zz][i] = ld_dsmem_f32(ra + 4u * i);
+            }
+          }
+#pragma unroll
+          for (int zz = 0; zz < 4; ++zz)  // fixed order
+            if (zz < sk) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) o[i] = __fadd_rn(o[i], __fmul_rn(g.alpha, q[zz][i]));  // (no FMA contraction)
+            }
+          const int64_t m = m0 + mb * G_BM + rr;
+          float* yr = static_cast<float*>(g.y) + m * g.ldy + n;
+          if (n + 4 <= g.n_real && (((uintptr_t)yr) & 15) == 0) {
+            float4 ov = make_float4(o[0], o[1], o[2], o[3]);
+            if (g.accumulate) {
+              const float4 yq = *reinterpret_cast<const float4*>(yr);
+              ov.x += yq.x;
+              ov.y += yq.y;
+              ov.z += yq.z;
+              ov.w += yq.w;
+            }
+            *reinterpret_cast<float4*>(yr) = ov;
+          } else {
+            for (int i = 0; i < 4 && n + i < g.n_real; ++i) yr[i] = o[i] + (g.accumulate ? yr[i] : 0.f);
+          }
+        }
+        cluster_sync_all();  // every split has read this block's tiles: they may be overwritten / freed
+        continue;
+      }
       for (int qi = tid; qi < rows * Q; qi += G_DQ) {
         const int rr = qi / Q, c4 = (qi % Q) * 4, n = n0 + c4;
         if (n >= g.n_real) continue;
@@ -671,7 +732,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
       }
       named_bar_sync(1, G_DQ);  // the tile is reused by the next block
     }
-    if (sk > 1) {
+    if (sk > 1 && !dsm) {
       const int sem_id = blockIdx.y * gridDim.x + blockIdx.x;
       uint32_t* flag = reinterpret_cast<uint32_t*>(tile);  // the smem tile is free now
       int r_lo = 0, r_hi = min(mbn * G_BM, g.M - m0);        // rows of the tile this CTA sums
@@ -734,6 +795,14 @@ __global__ void __launch_bounds__(G_THREADS, 1) gemm_kernel(const GemmArgs g, co
       }
     }
   }
+  else if (g.splitk > 1 && g.dsm_reduce) {
+    // barrier.cluster counts every thread of the cluster: the producer and MMA warps take part in
+    // the epilogue's two cluster barriers per accumulator block
+    for (int mb = 0; mb < mbn; ++mb) {
+      cluster_sync_all();
+      cluster_sync_all();
+    }
+  }
   tc_fence_before();
   __syncthreads();
   if constexpr (CL > 1) cluster_sync_all();  // no CTA leaves while a peer may still multicast into it
@@ -761,12 +830,12 @@ int launch(const GemmArgs& g_in, const GemmMaps& maps, int m, int n_tiles, cudaS
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = CL;
   at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
+  at[0].val.clusterDim.z = g.dsm_reduce ? g.splitk : 1;  // (split-K through DSMEM: the splits of a tile)
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = PMPD_GEMM_PDL ? 2 : 1;
-  if (g.par_reduce) {
+  if (g.par_reduce && !g.dsm_reduce) {
     // the splits of a tile wait for each other: only when every CTA of the launch is co-resident
     // (clusters of 2 need SM pairs, so fewer than the SM count may be resident at once)
     static int max_ctas = -1;
@@ -925,7 +994,15 @@ extern "C" int pmpd_gemm(const pmpd_qtensor* t, const void* x_dev, int32_t ldx, 
   g.ws = nullptr;
   g.ldw = t->n_tiles * G_NG1;
   g.par_reduce = 0;
-  if (splitk > 1) {
+  g.dsm_reduce = 0;
+  // PMPD_GEMM_DSM=1: the splits of a tile as one cluster reducing through DSMEM. Measured slower
+  // (7B stack at 512 rows 10.3 vs 8.85 ms; 4096^2 at M=512 56 vs 37 us): clusters of 2-4 CTAs
+  // with ~200 KB of shared memory each co-schedule worse than independent CTAs. Off by default.
+  const char* dsm_e = getenv("PMPD_GEMM_DSM");
+  const bool dsm_env = dsm_e ? atoi(dsm_e) != 0 : false;
+  if (splitk > 1 && cl == 1 && dsm_env) {
+    g.dsm_reduce = 1;  // no workspace, no counters: the clusters reduce on chip
+  } else if (splitk > 1) {
     // split-K workspace (grown on demand; launches on one stream reuse it in order). A buffer
     // that is outgrown is retired, never freed: a CUDA graph captured earlier (the model's graphed
     // prefill) still holds its address.

@@ -106,3 +106,27 @@ def test_gemm_split_k_is_bit_reproducible():
         assert torch.equal(a, accs[0])
     assert float((outs[0] - ref).norm() / ref.norm()) < 2e-3
     assert float((accs[0] - base - ref).norm() / ref.norm()) < 2e-3
+
+
+@pytest.mark.parametrize("split", [2, 4])
+@pytest.mark.parametrize("M,K,N", [(512, 4096, 1024), (77, 1024, 1000), (300, 2048, 384)])
+def test_gemm_split_k_dsmem_equals_workspace(split, M, K, N, monkeypatch):
+    """Split-K reduced on chip (the splits of a tile form a cluster and sum their partial tiles
+    through distributed shared memory) gives the same bits as the global-workspace reduction, with
+    and without accumulate, into a strided y."""
+    g = torch.Generator(device="cuda").manual_seed(M + K + N + split)
+    pk = quantize_tensor(torch.randn((K, N), generator=g, device="cuda") * 0.02, 4, 64).packed(_capi.LAYOUT_KN)
+    x = torch.randn((M, K), generator=g, device="cuda").half()
+    base = torch.randn((M, N + 8), generator=g, device="cuda")
+    monkeypatch.setenv("PMPD_GEMM_SPLITK", str(split))
+    outs = {}
+    for dsm in ("0", "1"):
+        monkeypatch.setenv("PMPD_GEMM_DSM", dsm)
+        y0 = gemm(pk, x, _pdev(3), alpha=0.5)
+        big = base.clone()
+        gemm(pk, x, _pdev(3), out=big[:, :N], alpha=0.5, accumulate=True)
+        outs[dsm] = (y0, big)
+    torch.cuda.synchronize()
+    assert torch.equal(outs["0"][0], outs["1"][0])
+    assert torch.equal(outs["0"][1], outs["1"][1])
+    assert torch.equal(outs["1"][1][:, N:], base[:, N:])

@@ -55,6 +55,9 @@ constexpr int MAXM = 8;
 // one status word, then the split-K partials.
 constexpr int kWsCounters = 16384;
 constexpr int64_t kWsHead = (int64_t)kWsCounters * 4 + 256;
+#ifndef PMPD_GEMV_ONEPASS
+#define PMPD_GEMV_ONEPASS 1  // activations of every row staged / max-reduced in one pass (0: row by row)
+#endif
 constexpr int kXsMaxK = 12288;          // activations staged in smem when K <= this (batch 1)
 constexpr int kXsMulti = 32768;         // batch 2..8: staged when m * K_pad <= this (64 KB)
 
@@ -111,6 +114,15 @@ struct Plan {
   static constexpr int kMx = kRedb + NCW * MB * 4;  // per-row max |x| (KN)
   static constexpr int kBytes = kMx + MAXM * 4 + 32 * 4;
 };
+
+// 8 activations x[0..8) with x[i] = 0 for i >= n (the row's ragged end or an unaligned row),
+// kept out of line so that the staging loop's many load sites stay small
+__device__ __noinline__ uint4 load_x8_tail(const __half* src, int n) {
+  __half tmp[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) tmp[i] = i < n ? src[i] : __float2half(0.f);
+  return *reinterpret_cast<const uint4*>(tmp);
+}
 
 // Tile iteration without integer division: stages never straddle an n-group.
 struct TileCursor {
@@ -793,6 +805,64 @@ __global__ void __launch_bounds__(NTHREADS, 1) qgemv_kernel(const GemvArgs a) {
   const int Me = MB == 1 ? 1 : a.m;
   const int xsld = MB == 1 ? kXsMaxK : KT * kTile;  // staged row stride (XS)
   float* red32 = reinterpret_cast<float*>(smem_raw + PL::kMx) + MAXM;  // 32 floats of scratch
+  if (PMPD_GEMV_ONEPASS && ((XS && a.in_mode == 0) || (!XS && LAYOUT == PMPD_LAYOUT_KN))) {
+    // Every row in one pass: a thread issues its loads of all rows of a K chunk before it uses
+    // any (one L2 round trip per chunk, not one per row), and the per-row max |x| of every row is
+    // reduced across warps with ONE barrier (the per-row form below paid a round trip and two
+    // barriers per row: batch 8 spent most of a small GEMV staging its activations).
+    constexpr int STEP = NCW * 32 * 8;  // halves per pass of the CTA (8 per thread, one uint4)
+    constexpr int R = MB <= 2 ? 4 : 2;  // passes per chunk (MB x R load sites: keeps the code small)
+    const int kp = XS ? KT * kTile : a.k_real;
+    const bool vec_ok = ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0) && ((a.ldx & 7) == 0);
+    __half* xs = reinterpret_cast<__half*>(smem_raw + PL::kXs);
+    float mr[MB];
+#pragma unroll
+    for (int b = 0; b < MB; ++b) mr[b] = 0.f;
+    for (int k0 = 0; k0 < kp; k0 += R * STEP) {
+      uint4 v[MB][R];
+#pragma unroll
+      for (int b = 0; b < MB; ++b)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int k = k0 + r * STEP + (int)threadIdx.x * 8;
+          v[b][r] = make_uint4(0u, 0u, 0u, 0u);
+          if ((MB == 1 || b < Me) && k < kp) {
+            const __half* src = a.x + (int64_t)b * a.ldx + k;
+            v[b][r] = (vec_ok && k + 8 <= a.k_real) ? __ldg(reinterpret_cast<const uint4*>(src))
+                                                    : load_x8_tail(src, a.k_real - k);
+          }
+        }
+#pragma unroll
+      for (int b = 0; b < MB; ++b)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int k = k0 + r * STEP + (int)threadIdx.x * 8;
+          if ((MB == 1 || b < Me) && k < kp) {
+            const __half2* h2 = reinterpret_cast<const __half2*>(&v[b][r]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 fv = __half22float2(h2[i]);
+              mr[b] = fmaxf(mr[b], fmaxf(fabsf(fv.x), fabsf(fv.y)));
+            }
+            if constexpr (XS) *reinterpret_cast<uint4*>(xs + b * xsld + k) = v[b][r];
+          }
+        }
+    }
+    if constexpr (LAYOUT == PMPD_LAYOUT_KN) {
+      float* rmx = reinterpret_cast<float*>(smem_raw + PL::kRed);  // [NCW][MB] (free until the first flush)
+#pragma unroll
+      for (int b = 0; b < MB; ++b) {
+        const float m = warp_max(mr[b]);
+        if (lane == 0) rmx[warp * MB + b] = m;
+      }
+      named_bar_sync(1, NCW * 32);
+      if ((int)threadIdx.x < Me) {
+        float r = 0.f;
+        for (int w = 0; w < NCW; ++w) r = fmaxf(r, rmx[w * MB + threadIdx.x]);
+        mxs[threadIdx.x] = r;
+      }
+    }
+  } else
   for (int b = 0; b < Me; ++b) {
     float m = 0.f;
     if constexpr (XS) {

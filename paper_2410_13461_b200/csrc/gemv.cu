@@ -60,6 +60,10 @@ constexpr int64_t kWsHead = (int64_t)kWsCounters * 4 + 256;
 #endif
 constexpr int kXsMaxK = 12288;          // activations staged in smem when K <= this (batch 1)
 constexpr int kXsMulti = 32768;         // batch 2..8: staged when m * K_pad <= this (64 KB)
+constexpr int kXsBig = 49152;           // ... or <= this with a 2-stage ring (96 KB)
+#ifndef PMPD_GEMV_XS2
+#define PMPD_GEMV_XS2 1
+#endif
 
 struct GemvArgs {
   const uint8_t* planes;
@@ -98,14 +102,15 @@ struct Smem {  // fits in the first 128 bytes of dynamic shared memory
 // [Smem | ring: NSTAGE x (PMAX planes + scales) x STILES tiles | xs: staged
 //  activations (XS) | xq: per-warp int8 activation fragments (KN) |
 //  red/redb: cross-warp sums | qsc: per-n-group activation scales (KN)]
-template <int PMAX, int MB, bool XS>
+template <int PMAX, int MB, int XS>
 struct Plan {
   static constexpr int kStage = STILES * (PMAX + 1) * kTilePlaneBytes;
   static constexpr int kRing = 128;
-  // batch 2..8 with staged activations trades one ring stage for the 64 KB of x
-  static constexpr int kNst = (MB > 1 && XS) ? 3 : NSTAGE;
+  // batch 2..8 with staged activations trades one ring stage for the 64 KB of x (XS = 1), or two
+  // for 96 KB (XS = 2: e.g. 8 rows of K = 5632, 4 rows of K = 11008)
+  static constexpr int kNst = (MB > 1 && XS) ? (XS == 2 ? 2 : 3) : NSTAGE;
   static constexpr int kXs = kRing + kNst * kStage;
-  static constexpr int kXsBytes = XS ? (MB == 1 ? kXsMaxK * 2 : kXsMulti * 2) : 0;
+  static constexpr int kXsBytes = XS ? (MB == 1 ? kXsMaxK * 2 : (XS == 2 ? kXsBig : kXsMulti) * 2) : 0;
   static constexpr int kXq = kXs + kXsBytes;
   static constexpr int kXqRows = MB;
   static constexpr int kXqWarp = TPW * kXqRows * 2 * 64;  // lo + hi bytes per row and tile
@@ -149,7 +154,7 @@ PMPD_DEV float2 ffma2(float2 a, float2 b, float2 c) {
 // ---------------------------------------------------------------- consumer
 // State of one consumer warp; run() is instantiated per (layout, p_max, p) so
 // that the whole tile loop is specialised for the active precision.
-template <int LAYOUT, int PMAX, int MB, bool XS>
+template <int LAYOUT, int PMAX, int MB, int XS>
 struct Consumer {
   using PL = Plan<PMAX, MB, XS>;
   static constexpr bool KN = LAYOUT == PMPD_LAYOUT_KN;
@@ -720,7 +725,7 @@ struct Consumer {
 };
 
 // ---------------------------------------------------------------- kernel
-template <int LAYOUT, int PMAX, int MB, bool XS>
+template <int LAYOUT, int PMAX, int MB, int XS>
 __global__ void __launch_bounds__(NTHREADS, 1) qgemv_kernel(const GemvArgs a) {
   using PL = Plan<PMAX, MB, XS>;
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -978,7 +983,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) qgemv_kernel(const GemvArgs a) {
   }
 }
 
-template <int LAYOUT, int PMAX, int MB, bool XS>
+template <int LAYOUT, int PMAX, int MB, int XS>
 int launch_m(const GemvArgs& a, int grid, cudaStream_t s) {
   using PL = Plan<PMAX, MB, XS>;
   static_assert(PL::kBytes <= 232448, "GEMV shared-memory plan exceeds 227 KB");
@@ -1013,16 +1018,20 @@ inline int rows_staged(int layout, int m) {
 template <int LAYOUT, int PMAX>
 int launch(const GemvArgs& a, int grid, cudaStream_t s) {
   if (a.m == 1)
-    return a.k_tiles * kTile <= kXsMaxK ? launch_m<LAYOUT, PMAX, 1, true>(a, grid, s)
-                                        : launch_m<LAYOUT, PMAX, 1, false>(a, grid, s);
+    return a.k_tiles * kTile <= kXsMaxK ? launch_m<LAYOUT, PMAX, 1, 1>(a, grid, s)
+                                        : launch_m<LAYOUT, PMAX, 1, 0>(a, grid, s);
   // batch 2..8: the row count is a template bound (2, 4 or 8) so every per-row loop unrolls
   // into registers; rows past m are masked
-  const bool xs = rows_staged(LAYOUT, a.m) * a.k_tiles * kTile <= kXsMulti;
-  if (a.m == 2)
-    return xs ? launch_m<LAYOUT, PMAX, 2, true>(a, grid, s) : launch_m<LAYOUT, PMAX, 2, false>(a, grid, s);
-  if (a.m <= 4)
-    return xs ? launch_m<LAYOUT, PMAX, 4, true>(a, grid, s) : launch_m<LAYOUT, PMAX, 4, false>(a, grid, s);
-  return xs ? launch_m<LAYOUT, PMAX, MAXM, true>(a, grid, s) : launch_m<LAYOUT, PMAX, MAXM, false>(a, grid, s);
+  const int staged = rows_staged(LAYOUT, a.m) * a.k_tiles * kTile;
+  const int xs = staged <= kXsMulti ? 1 : (PMPD_GEMV_XS2 && a.in_mode == 0 && staged <= kXsBig ? 2 : 0);
+#define PMPD_GEMV_XS_LAUNCH(MB_)                                      \
+  return xs == 1 ? launch_m<LAYOUT, PMAX, MB_, 1>(a, grid, s)         \
+       : xs == 2 ? launch_m<LAYOUT, PMAX, MB_, 2>(a, grid, s)         \
+                 : launch_m<LAYOUT, PMAX, MB_, 0>(a, grid, s)
+  if (a.m == 2) PMPD_GEMV_XS_LAUNCH(2);
+  if (a.m <= 4) PMPD_GEMV_XS_LAUNCH(4);
+  PMPD_GEMV_XS_LAUNCH(MAXM);
+#undef PMPD_GEMV_XS_LAUNCH
 }
 
 int ctas_per_sm() {

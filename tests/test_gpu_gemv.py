@@ -51,10 +51,11 @@ def test_gemv_parity(layout, N, K, M):
         assert err < 2e-3, (layout, N, K, M, p, err)  # expected ~1e-4; budget is 1e-2
 
 
-@pytest.mark.parametrize("N,K", [(4096, 4096), (1000, 200), (320, 11008)])
-@pytest.mark.parametrize("M", [2, 4, 5])
+@pytest.mark.parametrize("N,K", [(4096, 4096), (1000, 200), (320, 11008), (256, 5632)])
+@pytest.mark.parametrize("M", [2, 3, 4, 5, 8])
 def test_gemv_parity_batch_variants(N, K, M):
-    """Batch 2 / 4 / 5-8 instantiations (KN), staged (m*K <= 32768) and unstaged activations."""
+    """Batch 2 / 4 / 5-8 instantiations (KN), activations staged with a 3-stage ring (m*K <= 32768),
+    with a 2-stage ring (<= 49152: 3-4 rows of K = 11008, 8 rows of K = 5632) and unstaged."""
     w, x = _case(N, K, _capi.LAYOUT_KN, N * 17 + K + M, M)
     ref = oq.quantize(w, 4, 64)
     pk = quant.quantize_tensor(w, 4, 64).packed(_capi.LAYOUT_KN)

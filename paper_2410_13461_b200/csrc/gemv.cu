@@ -25,6 +25,7 @@
 //     (atomic ticket) sums the partials in CTA order -> deterministic.
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "decode_core.cuh"
@@ -108,9 +109,10 @@ struct Plan {
   static constexpr int kRing = 128;
   // batch 2..8 with staged activations trades one ring stage for the 64 KB of x (XS = 1), or two
   // for 96 KB (XS = 2: e.g. 8 rows of K = 5632, 4 rows of K = 11008)
-  static constexpr int kNst = (MB > 1 && XS) ? (XS == 2 ? 2 : 3) : NSTAGE;
+  // XS = 3: as 2, but only the CTA's own k-tiles are staged (a circular k range, see xmap)
+  static constexpr int kNst = (MB > 1 && XS) ? (XS >= 2 ? 2 : 3) : NSTAGE;
   static constexpr int kXs = kRing + kNst * kStage;
-  static constexpr int kXsBytes = XS ? (MB == 1 ? kXsMaxK * 2 : (XS == 2 ? kXsBig : kXsMulti) * 2) : 0;
+  static constexpr int kXsBytes = XS ? (MB == 1 ? kXsMaxK * 2 : (XS >= 2 ? kXsBig : kXsMulti) * 2) : 0;
   static constexpr int kXq = kXs + kXsBytes;
   static constexpr int kXqRows = MB;
   static constexpr int kXqWarp = TPW * kXqRows * 2 * 64;  // lo + hi bytes per row and tile
@@ -267,10 +269,18 @@ struct Consumer {
     }
   }
 
+  // XS = 3: the staged row holds the CTA's k-tiles only, from k = xkb on, wrapping past the last
+  // k-tile to 0 (a stream-K range that crosses an n-group boundary)
+  int xkb = 0, xkp = 0;
+  PMPD_DEV int xmap(int k) const {
+    if constexpr (XS == 3) return k >= xkb ? k - xkb : k - xkb + xkp;
+    return k;
+  }
+
   // x[b][k..k+1] as float2 (zero outside [0, k_real))
   PMPD_DEV float2 xpair(int b, int k) const {
     if constexpr (XS) {
-      return __half22float2(*reinterpret_cast<const __half2*>(xs + b * xld + k));
+      return __half22float2(*reinterpret_cast<const __half2*>(xs + b * xld + xmap(k)));
     } else {
       const __half* xr = xs + (int64_t)b * xld;
       if (k + 1 < a.k_real) return __half22float2(*reinterpret_cast<const __half2*>(xr + k));
@@ -279,7 +289,7 @@ struct Consumer {
   }
   PMPD_DEV uint32_t xword(int b, int k) const {
     if constexpr (XS) {
-      return *reinterpret_cast<const uint32_t*>(xs + b * xld + k);
+      return *reinterpret_cast<const uint32_t*>(xs + b * xld + xmap(k));
     } else {
       const __half* xr = xs + (int64_t)b * xld;
       if (k + 1 < a.k_real) return __ldg(reinterpret_cast<const unsigned int*>(xr + k));
@@ -429,7 +439,7 @@ struct Consumer {
         for (int h = 0; h < 2; ++h) {
           const int k = k0 + 32 * cch + 16 * h + 4 * tig;
           if constexpr (XS) {
-            xr[cch][h] = *reinterpret_cast<const uint2*>(xrow + k);
+            xr[cch][h] = *reinterpret_cast<const uint2*>(xrow + xmap(k));
           } else {
             xr[cch][h] = xh[q][cch][h];  // (prefetched a stage ahead by run())
             (void)rowok;
@@ -808,16 +818,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) qgemv_kernel(const GemvArgs a) {
   }
   pdl_wait();  // activations and the workspace belong to the predecessor until here
   const int Me = MB == 1 ? 1 : a.m;
-  const int xsld = MB == 1 ? kXsMaxK : KT * kTile;  // staged row stride (XS)
+  // XS = 3: this CTA's k-tiles [kt0, kt0 + nkt) mod KT (all of them once the range spans KT)
+  const int nkt = XS == 3 ? min(T1 - T0, KT) : KT;
+  const int xkb = XS == 3 && T1 - T0 < KT ? (T0 % KT) * kTile : 0;
+  const int xsld = MB == 1 ? kXsMaxK : (XS == 3 ? ((NT + G - 1) / G < KT ? (NT + G - 1) / G : KT) : KT) * kTile;
   float* red32 = reinterpret_cast<float*>(smem_raw + PL::kMx) + MAXM;  // 32 floats of scratch
-  if (PMPD_GEMV_ONEPASS && ((XS && a.in_mode == 0) || (!XS && LAYOUT == PMPD_LAYOUT_KN))) {
+  if ((PMPD_GEMV_ONEPASS || XS == 3) && ((XS && a.in_mode == 0) || (!XS && LAYOUT == PMPD_LAYOUT_KN))) {
     // Every row in one pass: a thread issues its loads of all rows of a K chunk before it uses
     // any (one L2 round trip per chunk, not one per row), and the per-row max |x| of every row is
     // reduced across warps with ONE barrier (the per-row form below paid a round trip and two
     // barriers per row: batch 8 spent most of a small GEMV staging its activations).
     constexpr int STEP = NCW * 32 * 8;  // halves per pass of the CTA (8 per thread, one uint4)
     constexpr int R = MB <= 2 ? 4 : 2;  // passes per chunk (MB x R load sites: keeps the code small)
-    const int kp = XS ? KT * kTile : a.k_real;
+    const int kp = XS ? nkt * kTile : a.k_real;  // staged (local) columns per row
+    const int kfull = KT * kTile;
     const bool vec_ok = ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0) && ((a.ldx & 7) == 0);
     __half* xs = reinterpret_cast<__half*>(smem_raw + PL::kXs);
     float mr[MB];
@@ -832,9 +846,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) qgemv_kernel(const GemvArgs a) {
           const int k = k0 + r * STEP + (int)threadIdx.x * 8;
           v[b][r] = make_uint4(0u, 0u, 0u, 0u);
           if ((MB == 1 || b < Me) && k < kp) {
-            const __half* src = a.x + (int64_t)b * a.ldx + k;
-            v[b][r] = (vec_ok && k + 8 <= a.k_real) ? __ldg(reinterpret_cast<const uint4*>(src))
-                                                    : load_x8_tail(src, a.k_real - k);
+            int kg = k;  // the column in x of local column k
+            if constexpr (XS == 3) {
+              kg = k + xkb;
+              if (kg >= kfull) kg -= kfull;
+            }
+            const __half* src = a.x + (int64_t)b * a.ldx + kg;
+            v[b][r] = (vec_ok && kg + 8 <= a.k_real) ? __ldg(reinterpret_cast<const uint4*>(src))
+                                                     : load_x8_tail(src, a.k_real - kg);
           }
         }
 #pragma unroll
@@ -954,8 +973,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) qgemv_kernel(const GemvArgs a) {
   if constexpr (XS && LAYOUT == PMPD_LAYOUT_KN && MB == MAXM) {
     // the f16 HMMA path reads row gq of every lane: rows past m are zero
     __half* xs = reinterpret_cast<__half*>(smem_raw + PL::kXs);
-    const int kp = KT * kTile;
-    for (int i = Me * kp + threadIdx.x * 8; i < MB * kp; i += NCW * 32 * 8)
+    for (int i = Me * xsld + threadIdx.x * 8; i < MB * xsld; i += NCW * 32 * 8)
       *reinterpret_cast<uint4*>(xs + i) = make_uint4(0u, 0u, 0u, 0u);
   }
   named_bar_sync(1, NCW * 32);
@@ -963,6 +981,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) qgemv_kernel(const GemvArgs a) {
     cs.xs = reinterpret_cast<__half*>(smem_raw + PL::kXs);
     cs.xld = xsld;
     cs.xrow = cs.xs + (int64_t)cs.gq * xsld;
+    cs.xkb = xkb;
+    cs.xkp = KT * kTile;
   } else {
     cs.xs = a.x;
     cs.xld = a.ldx;
@@ -1023,10 +1043,17 @@ int launch(const GemvArgs& a, int grid, cudaStream_t s) {
   // batch 2..8: the row count is a template bound (2, 4 or 8) so every per-row loop unrolls
   // into registers; rows past m are masked
   const int staged = rows_staged(LAYOUT, a.m) * a.k_tiles * kTile;
-  const int xs = staged <= kXsMulti ? 1 : (PMPD_GEMV_XS2 && a.in_mode == 0 && staged <= kXsBig ? 2 : 0);
+  // ranged (XS = 3): the most k-tiles one CTA of this grid touches
+  const int64_t ntl = (int64_t)a.n_tiles * a.k_tiles;
+  const int per_cta = (int)std::min<int64_t>((ntl + grid - 1) / grid, a.k_tiles);
+  const int ranged = rows_staged(LAYOUT, a.m) * per_cta * kTile;
+  const int xs = staged <= kXsMulti ? 1
+               : (PMPD_GEMV_XS2 && a.in_mode == 0 && staged <= kXsBig) ? 2
+               : (PMPD_GEMV_XS2 && a.in_mode == 0 && ranged <= kXsBig) ? 3 : 0;
 #define PMPD_GEMV_XS_LAUNCH(MB_)                                      \
   return xs == 1 ? launch_m<LAYOUT, PMAX, MB_, 1>(a, grid, s)         \
        : xs == 2 ? launch_m<LAYOUT, PMAX, MB_, 2>(a, grid, s)         \
+       : xs == 3 ? launch_m<LAYOUT, PMAX, MB_, 3>(a, grid, s)         \
                  : launch_m<LAYOUT, PMAX, MB_, 0>(a, grid, s)
   if (a.m == 2) PMPD_GEMV_XS_LAUNCH(2);
   if (a.m <= 4) PMPD_GEMV_XS_LAUNCH(4);

@@ -35,7 +35,7 @@ def _oracle_y(ref, x, p, layout):
 
 @pytest.mark.parametrize("layout", [_capi.LAYOUT_KN, _capi.LAYOUT_NK])
 @pytest.mark.parametrize("N,K", [(64, 64), (256, 256), (4096, 4096), (320, 1024), (1000, 200), (257, 64),
-                                 (2048, 5632), (11008 // 2, 1024)])
+                                 (2048, 5632), (11008 // 2, 1024), (320, 11008)])
 @pytest.mark.parametrize("M", [1, 3, 8])
 def test_gemv_parity(layout, N, K, M):
     w, x = _case(N, K, layout, N * 31 + K + M, M)
@@ -55,7 +55,8 @@ def test_gemv_parity(layout, N, K, M):
 @pytest.mark.parametrize("M", [2, 3, 4, 5, 8])
 def test_gemv_parity_batch_variants(N, K, M):
     """Batch 2 / 4 / 5-8 instantiations (KN), activations staged with a 3-stage ring (m*K <= 32768),
-    with a 2-stage ring (<= 49152: 3-4 rows of K = 11008, 8 rows of K = 5632) and unstaged."""
+    with a 2-stage ring (<= 49152: 3-4 rows of K = 11008, 8 rows of K = 5632), or only the CTA's own
+    k-tiles (5-8 rows of K = 11008 on the split-K grid, ranges wrapping across n-groups)."""
     w, x = _case(N, K, _capi.LAYOUT_KN, N * 17 + K + M, M)
     ref = oq.quantize(w, 4, 64)
     pk = quant.quantize_tensor(w, 4, 64).packed(_capi.LAYOUT_KN)

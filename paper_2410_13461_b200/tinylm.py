@@ -555,15 +555,19 @@ class _PrefillGraph:
 def _prefill_graphed(model: ModelVariants, dw: _DeviceWeights, p: int, ids: np.ndarray,
                      cache: KVCache) -> torch.Tensor:
     n = int(ids.size)
-    graphs = model.__dict__.setdefault("_prefill_graphs", {})
-    key = (n, p, id(dw))
-    pg = graphs.pop(key, None)
-    if pg is None:
-        while len(graphs) >= _PREFILL_GRAPHS_KEPT:  # keep the most recently used shapes
-            graphs.pop(next(iter(graphs)))
-        pg = _PrefillGraph(model, dw, p, n)
-    graphs[key] = pg
-    logits = pg.run(ids, cache)
+    # (the graphs' static buffers are shared by every caller of the model: one prompt pass at a
+    # time, enqueued on the caller's current stream)
+    lock = model.__dict__.setdefault("_prefill_lock", threading.Lock())
+    with lock:
+        graphs = model.__dict__.setdefault("_prefill_graphs", {})
+        key = (n, p, id(dw))
+        pg = graphs.pop(key, None)
+        if pg is None:
+            while len(graphs) >= _PREFILL_GRAPHS_KEPT:  # keep the most recently used shapes
+                graphs.pop(next(iter(graphs)))
+            pg = _PrefillGraph(model, dw, p, n)
+        graphs[key] = pg
+        logits = pg.run(ids, cache)
     _capi.call("pmpd_add_i32", cache.T_dev.data_ptr(), n, _stream())
     cache.T = n
     return logits

@@ -373,3 +373,16 @@ def test_prefill_graph_sdpa_matches_oracle(toy, oracle_toy, n):
         d, _ = tinylm.decode_step(toy, p, tok, cache)
         rd, _ = om.decode_step(oracle_toy, p, tok, rc)
         assert rel_l2(host(d), rd) < TOL, (n, p)
+
+
+def test_prefill_graph_table_evicts_and_recaptures(toy, oracle_toy):
+    """More prompt lengths than the graph table keeps: the oldest shapes are evicted and captured
+    again on reuse; every pass still tracks the oracle and the table stays bounded."""
+    rng = np.random.default_rng(3)
+    lengths = [20, 24, 28, 32, 36, 20, 36]
+    for n in lengths:
+        prompt = rng.integers(0, toy.config.vocab_size, size=n).tolist()
+        lg, _ = tinylm.prefill(toy, 3, prompt)
+        ref, _ = om.prefill(oracle_toy, 3, prompt)
+        assert rel_l2(host(lg), ref) < TOL, n
+    assert len(toy.__dict__.get("_prefill_graphs", {})) <= tinylm._PREFILL_GRAPHS_KEPT

@@ -1040,6 +1040,9 @@ int launch(const GemvArgs& a, int grid, cudaStream_t s) {
   if (a.m == 1)
     return a.k_tiles * kTile <= kXsMaxK ? launch_m<LAYOUT, PMAX, 1, 1>(a, grid, s)
                                         : launch_m<LAYOUT, PMAX, 1, 0>(a, grid, s);
+#ifdef PMPD_GEMV_ONLY_B1  // (experiment builds: batch-1 instantiations only)
+  return fail(PMPD_ERR_CONFIG, "this build has batch-1 GEMVs only");
+#else
   // batch 2..8: the row count is a template bound (2, 4 or 8) so every per-row loop unrolls
   // into registers; rows past m are masked
   const int staged = rows_staged(LAYOUT, a.m) * a.k_tiles * kTile;
@@ -1059,6 +1062,7 @@ int launch(const GemvArgs& a, int grid, cudaStream_t s) {
   if (a.m <= 4) PMPD_GEMV_XS_LAUNCH(4);
   PMPD_GEMV_XS_LAUNCH(MAXM);
 #undef PMPD_GEMV_XS_LAUNCH
+#endif
 }
 
 int ctas_per_sm() {
